@@ -1,0 +1,305 @@
+/*
+ * jenga_gpu.h — C ABI of the B200-native Jenga KV-cache hot path.
+ *
+ * This is the drop-in boundary between the reference's host-side allocator /
+ * page-table API (the reference headers under proj/include/jenga) and the
+ * sm_100a kernels.  Everything here is `extern "C"`, plain pointers and sizes,
+ * int status codes, no exceptions and no torch types.  Device launches are
+ * asynchronous on a caller-provided cudaStream_t (passed as void*).
+ *
+ * Two halves:
+ *   (1) host API — a C++ re-implementation of the reference's Jenga allocator
+ *       (ModelSpec / LargePagePool / TypeAllocator / KvAllocator / AddressMap /
+ *       LayerPolicy) plus the per-request page-list runtime that
+ *       SimEngine::store_position maintains.  Each entry cites the reference
+ *       interface it replaces.
+ *   (2) device API — one contiguous HBM arena per GPU, block-table and slot-
+ *       mapping construction, reshape_and_cache, paged decode attention
+ *       (full / sliding-window / cross), Mamba state gather/scatter and page
+ *       copy.
+ *
+ * Status codes map onto the reference's exception types
+ * (reference proj/include/jenga/util.hpp:11-21):
+ *   JENGA_ERR_CONFIG    <-> jenga::ConfigError   (config, byte overflow)
+ *   JENGA_ERR_INVARIANT <-> jenga::InvariantError (JENGA_CHECK violations)
+ *   JENGA_ERR_OOM       <-> std::nullopt from KvAllocator::allocate
+ *                           (reference kv_allocator.hpp:77-80)
+ * jenga_last_error() returns the message of the last failure on this thread.
+ */
+#ifndef JENGA_GPU_H_
+#define JENGA_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JENGA_ABI_VERSION 1
+
+enum jenga_status {
+  JENGA_OK = 0,
+  JENGA_ERR_CONFIG = 1,
+  JENGA_ERR_INVARIANT = 2,
+  JENGA_ERR_OOM = 3,
+  JENGA_ERR_CUDA = 4,
+  JENGA_ERR_ARG = 5,
+  JENGA_ERR_UNSUPPORTED = 6,
+};
+
+/* reference model_config.hpp:15-21 (LayerKind), same numbering. */
+enum jenga_layer_kind {
+  JENGA_KIND_FULL = 0,
+  JENGA_KIND_SLIDING_WINDOW = 1,
+  JENGA_KIND_MAMBA = 2,
+  JENGA_KIND_CROSS_ATTENTION = 3,
+  JENGA_KIND_VISION_EMBEDDING = 4,
+};
+
+enum jenga_dtype { JENGA_F32 = 0, JENGA_BF16 = 1, JENGA_F16 = 2 };
+
+/* reference type_allocator.hpp:22-33 (SmallPageId{LargePageId large; u32 slot}). */
+typedef struct jenga_small_page {
+  uint32_t large;
+  uint32_t slot;
+} jenga_small_page;
+
+/* reference memory_layout.hpp:14-23 (ByteRange). */
+typedef struct jenga_byte_range {
+  uint64_t begin;
+  uint64_t end;
+} jenga_byte_range;
+
+/* reference memory_layout.hpp:25-32 (LayerView) — the kernel contract. */
+typedef struct jenga_layer_view {
+  uint64_t start_offset;
+  uint64_t page_stride;
+  uint64_t exec_page_size;
+} jenga_layer_view;
+
+typedef struct jenga_spec jenga_spec;       /* ModelSpec */
+typedef struct jenga_kv jenga_kv;           /* KvAllocator (Jenga strategy) */
+typedef struct jenga_addr jenga_addr;       /* AddressMap */
+typedef struct jenga_pages jenga_pages;     /* per-request page lists (SimEngine GroupRuntime) */
+typedef struct jenga_arena jenga_arena;     /* one HBM arena per GPU */
+
+int jenga_abi_version(void);
+const char* jenga_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * ModelSpec — reference model_config.hpp:26-54, model_config.cpp:41-127
+ * ---------------------------------------------------------------------- */
+int jenga_spec_create(const char* name, jenga_spec** out);
+/* Parses the reference's JSON config format (model_config.cpp:196-243). */
+int jenga_spec_from_json(const char* json_text, jenga_spec** out);
+void jenga_spec_destroy(jenga_spec* spec);
+int jenga_spec_add_group(jenga_spec* spec, const char* name, int kind,
+                         uint32_t num_layers, uint64_t bytes_per_token_per_layer,
+                         uint32_t tokens_per_page, uint64_t window_tokens,
+                         uint64_t checkpoint_interval_tokens);
+int jenga_spec_validate(const jenga_spec* spec);
+int jenga_spec_num_groups(const jenga_spec* spec);
+/* small_page_size(group g) — model_config.cpp:85-89 */
+int jenga_spec_small_page_size(const jenga_spec* spec, int g, uint64_t* out);
+/* compatible_page_size(spec, kLcm) — model_config.cpp:100-107 */
+int jenga_spec_lcm_page_size(const jenga_spec* spec, uint64_t* out);
+/* lcm_blowup_ratio — model_config.cpp:129-142 */
+int jenga_spec_lcm_blowup_ratio(const jenga_spec* spec, double* out);
+
+/* ------------------------------------------------------------------------
+ * AddressMap — reference memory_layout.hpp:34-69, memory_layout.cpp:10-55
+ * ---------------------------------------------------------------------- */
+int jenga_addr_create(const jenga_spec* spec, jenga_addr** out);
+void jenga_addr_destroy(jenga_addr* map);
+uint64_t jenga_addr_large_page_bytes(const jenga_addr* map);
+int jenga_addr_group_info(const jenga_addr* map, int g, uint64_t* small_page_bytes,
+                          uint64_t* per_layer_bytes, uint32_t* slots_per_large);
+int jenga_addr_global_page_index(const jenga_addr* map, int g, jenga_small_page page,
+                                 uint64_t* out);
+int jenga_addr_address_of(const jenga_addr* map, int g, uint32_t layer,
+                          jenga_small_page page, jenga_byte_range* out);
+int jenga_addr_layer_view(const jenga_addr* map, int g, uint32_t layer,
+                          jenga_layer_view* out);
+int jenga_addr_view_address(const jenga_addr* map, int g, uint32_t layer,
+                            jenga_small_page page, jenga_byte_range* out);
+
+/* ------------------------------------------------------------------------
+ * KvAllocator, Jenga strategy — reference kv_allocator.hpp:62-119,
+ * kv_allocator.cpp:67-79 (geometry), 154-239 (allocate/free/pin/evict).
+ * ---------------------------------------------------------------------- */
+int jenga_kv_create(const jenga_spec* spec, uint64_t budget_bytes, jenga_kv** out);
+void jenga_kv_destroy(jenga_kv* kv);
+int jenga_kv_num_groups(const jenga_kv* kv);
+/* EngineGeometry (kv_allocator.hpp:27-35): one LCM pool. */
+int jenga_kv_pool_info(const jenga_kv* kv, uint64_t* large_page_bytes,
+                       uint32_t* num_large_pages, uint64_t* reserved_remainder);
+/* Five-step allocate (kv_allocator.cpp:154-197). JENGA_ERR_OOM = nullopt. */
+int jenga_kv_allocate(jenga_kv* kv, int g, uint64_t request, jenga_small_page* page,
+                      int* step);
+/* free(g, page, cached) (kv_allocator.cpp:199-208). has_content=0 -> nullopt.
+ * Content = BlockContent{key, parent_key, tokens} (prefix_cache.hpp:20-29). */
+int jenga_kv_free(jenga_kv* kv, int g, jenga_small_page page, int has_content,
+                  uint64_t key, uint64_t parent_key, const uint64_t* tokens,
+                  size_t n_tokens);
+int jenga_kv_pin(jenga_kv* kv, int g, jenga_small_page page, uint64_t request);
+/* evict_lru_large_page (kv_allocator.cpp:218-239). *evicted = UINT32_MAX if none. */
+int jenga_kv_evict_lru_large_page(jenga_kv* kv, uint32_t* evicted);
+int jenga_kv_touch(jenga_kv* kv, int g, jenga_small_page page, uint64_t step);
+int jenga_kv_set_prefix_length(jenga_kv* kv, int g, jenga_small_page page, uint64_t len);
+int jenga_kv_set_request_aware(jenga_kv* kv, int on);
+/* record(id) (type_allocator.hpp:35-42): state 0 Empty, 1 Evictable, 2 Used. */
+int jenga_kv_page_record(const jenga_kv* kv, int g, jenga_small_page page, int* state,
+                         uint64_t* associated_request, uint64_t* last_access,
+                         uint64_t* prefix_length);
+/* PrefixCache::find (prefix_cache.cpp:77-87): *found=0 when absent. */
+int jenga_kv_cache_find(const jenga_kv* kv, int g, uint64_t key, uint64_t parent_key,
+                        const uint64_t* tokens, size_t n_tokens, int* found,
+                        jenga_small_page* page);
+/* counters: used/evictable/empty small pages, owned units (type_allocator.hpp:133-136) */
+int jenga_kv_group_counts(const jenga_kv* kv, int g, uint64_t* used, uint64_t* evictable,
+                          uint64_t* empty, uint64_t* owned_units);
+int jenga_kv_pool_free_pages(const jenga_kv* kv, uint32_t* num_free);
+/* fragmentation_report (type_allocator.cpp:261-281) */
+int jenga_kv_fragmentation(const jenga_kv* kv, int g, uint64_t* used_bytes,
+                           uint64_t* evictable_bytes, uint64_t* empty_stranded_bytes);
+int jenga_kv_alloc_step_counts(const jenga_kv* kv, uint64_t counts[6]);
+int jenga_kv_check_invariants(const jenga_kv* kv);
+
+/* ------------------------------------------------------------------------
+ * LayerPolicy — reference layer_policies.cpp:79-120
+ * ---------------------------------------------------------------------- */
+int jenga_policy_needs_token(const jenga_spec* spec, int g, uint64_t i,
+                             uint64_t new_tokens, uint64_t consumed_tokens, int* out);
+int jenga_policy_accessed_range(const jenga_spec* spec, int g, uint64_t prev_tokens,
+                                uint64_t new_tokens, uint64_t* lo, uint64_t* hi);
+
+/* ------------------------------------------------------------------------
+ * Per-request page lists — the state SimEngine keeps per (request, group)
+ * (reference simulator.hpp:123-139) and updates in store_position
+ * (simulator.cpp:217-282), group_stores_position (:151-158),
+ * free_block (:284-312), release_all_pages (:314-327).
+ * The page-list object borrows the allocator (single owner, not thread-safe,
+ * as the reference: SPEC.md:170).
+ * ---------------------------------------------------------------------- */
+int jenga_pages_create(jenga_kv* kv, int prefix_caching, jenga_pages** out);
+void jenga_pages_destroy(jenga_pages* pl);
+int jenga_pages_add_request(jenga_pages* pl, uint64_t request);
+/* Append one sequence position to every group that stores it (decode_one,
+ * simulator.cpp:549-566).  image_ordinal is the eviction ordinal image-storing
+ * groups record for an image position (simulator.cpp:160-162, 261-270).
+ * OOM returns JENGA_ERR_OOM; the request must then be released (preempted,
+ * simulator.cpp:329-338) before it is appended to again. */
+int jenga_pages_append(jenga_pages* pl, uint64_t request, uint64_t token_id,
+                       int is_image, uint64_t image_ordinal, uint64_t now_step);
+/* One decode step for a batch: append one position (token_ids[i], is_image
+ * may be NULL = text) to each request ids[i], in the given order.  Stops at
+ * the first OOM (JENGA_ERR_OOM, *n_done = requests fully appended). */
+int jenga_pages_append_batch(jenga_pages* pl, const uint64_t* ids, int n,
+                             const uint64_t* token_ids, const uint8_t* is_image,
+                             uint64_t now_step, int* n_done);
+/* Append one position to ONE group (prefill / vision paths drive groups
+ * separately in the reference). */
+int jenga_pages_store(jenga_pages* pl, uint64_t request, int g, uint64_t pos,
+                      uint64_t now_step);
+int jenga_pages_release(jenga_pages* pl, uint64_t request, int allow_cache,
+                        uint64_t now_step);
+int jenga_pages_seq_len(const jenga_pages* pl, uint64_t request, uint64_t* len);
+/* Per-group state of one request. */
+int jenga_pages_group_state(const jenga_pages* pl, uint64_t request, int g,
+                            uint64_t* stored, uint64_t* num_blocks,
+                            uint64_t* freed_blocks, uint64_t* held_tokens,
+                            int* has_working_page, jenga_small_page* working_page);
+/* Copy the block list (dead blocks included, flagged live=0). */
+int jenga_pages_blocks(const jenga_pages* pl, uint64_t request, int g,
+                       jenga_small_page* pages, uint8_t* live, uint64_t capacity,
+                       uint64_t* n);
+/* Pack the CSR page lists of `n_req` requests for group g, ready for
+ * jenga_build_block_tables:
+ *   offsets[n_req+1], pages[offsets[n_req]], first_live_block[n_req],
+ *   n_stored[n_req] (stored ordinals; for mamba groups 1 page = working).
+ * Pass pages=NULL to query offsets only. */
+int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64_t* requests,
+                         int n_req, int32_t* offsets, jenga_small_page* pages,
+                         int32_t* first_live_block, int32_t* n_stored);
+
+/* ------------------------------------------------------------------------
+ * Device API (sm_100a).  One arena per GPU: num_large_pages x large_page_bytes
+ * (= LargePagePool sizing, lcm_allocator.cpp:12-18), 4 KiB aligned.
+ * All launches are async on `stream` (cudaStream_t). Pointers are device
+ * pointers unless stated.
+ * ---------------------------------------------------------------------- */
+int jenga_arena_create(int device, uint64_t num_large_pages, uint64_t large_page_bytes,
+                       jenga_arena** out);
+void jenga_arena_destroy(jenga_arena* arena);
+void* jenga_arena_base(const jenga_arena* arena);
+uint64_t jenga_arena_bytes(const jenga_arena* arena);
+
+/* AddressMap::global_page_index + slot mapping on device
+ * (memory_layout.cpp:22-27; slot = global*tpp + (ord-1)%tpp).
+ *   offsets[B+1], pages[], first_live_block[B], n_stored[B]  — CSR page lists
+ *   block_table[B][max_blocks] (int32, -1 = dead or absent)
+ *   slot_mapping[B] (int64): slot of each request's newest stored ordinal
+ *   (n_stored[b]) or -1 if n_stored[b]==0; may be NULL.
+ *   seq_lens[B] (int32) = n_stored; may be NULL. */
+int jenga_build_block_tables(const int32_t* offsets, const jenga_small_page* pages,
+                             const int32_t* first_live_block, const int32_t* n_stored,
+                             int batch, uint32_t slots_per_large, uint32_t tokens_per_page,
+                             int max_blocks, int32_t* block_table, int64_t* slot_mapping,
+                             int32_t* seq_lens, void* stream);
+
+/* Slot mapping for a run of new tokens (prefill chunk):
+ *   token t of request req[t] at 1-based ordinal ord[t] ->
+ *   block_table[req][(ord-1)/tpp]*tpp + (ord-1)%tpp. */
+int jenga_slot_mapping(const int32_t* block_table, int max_blocks, const int32_t* req,
+                       const int32_t* ord, int n_tokens, uint32_t tokens_per_page,
+                       int64_t* slot_mapping, void* stream);
+
+/* Intra-slice layout (documented in DESIGN.md): one layer's slice of one small
+ * page is [K|V][Hkv][tpp][D] of dtype — exec_page_size = 2*Hkv*D*e*tpp.
+ * Scatter K/V[T][Hkv][D] (row stride kv_row_stride elements between tokens)
+ * into their slots; slot < 0 skips. */
+int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view, int dtype,
+                            int num_kv_heads, int head_dim, uint32_t tokens_per_page,
+                            const void* key, const void* value, int64_t kv_token_stride,
+                            const int64_t* slot_mapping, int n_tokens, void* stream);
+
+/* Paged decode attention through the two-level table.
+ *   kind: JENGA_KIND_FULL / SLIDING_WINDOW / CROSS_ATTENTION
+ *   q[B][Hq][D], out[B][Hq][D] (dtype), block_table[B][max_blocks],
+ *   seq_lens[B] = live length n (ordinals 1..n stored; SWA attends (n-W, n]).
+ *   workspace: device scratch of jenga_paged_decode_workspace_size() bytes;
+ *   the counters region must be zero before the first call (kernels re-zero
+ *   it themselves).  softcap <= 0 disables logit soft-capping. */
+size_t jenga_paged_decode_workspace_size(int batch, int num_q_heads, int num_kv_heads,
+                                         int head_dim, int max_blocks,
+                                         uint32_t tokens_per_page);
+int jenga_paged_decode(void* arena_base, jenga_layer_view view, int kind, int dtype,
+                       uint64_t window, const void* q, void* out, const int32_t* block_table,
+                       const int32_t* seq_lens, int batch, int max_blocks, int num_q_heads,
+                       int num_kv_heads, int head_dim, uint32_t tokens_per_page,
+                       float scale, float softcap, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Mamba last-token state (one working page per request, tpp=1):
+ * gather dense[B][exec_page_size] <- arena slice; scatter the reverse
+ * (simulator.cpp:222-244 keeps the working page). page_globals[b] < 0 skips. */
+int jenga_mamba_state_gather(const void* arena_base, jenga_layer_view view,
+                             const int64_t* page_globals, int batch, void* dense,
+                             void* stream);
+int jenga_mamba_state_scatter(void* arena_base, jenga_layer_view view,
+                              const int64_t* page_globals, int batch, const void* dense,
+                              void* stream);
+/* Whole-small-page copy (all layers of a group): checkpoint snapshot / restore
+ * (simulator.cpp:231-242). Addresses = global * small_page_bytes. */
+int jenga_page_copy(void* arena_base, uint64_t small_page_bytes, const int64_t* src_globals,
+                    const int64_t* dst_globals, int n_pages, void* stream);
+
+/* Number of device kernels launched by this library since load (evidence). */
+uint64_t jenga_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* JENGA_GPU_H_ */

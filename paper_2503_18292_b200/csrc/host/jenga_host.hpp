@@ -1,0 +1,405 @@
+// B200-native Jenga host runtime: model geometry, the two-level (LCM large
+// page -> per-type small page) allocator, the page-layer address map and the
+// per-request page lists that feed the device block tables.
+//
+// The public surface mirrors the reference C++ API (reference
+// proj/include/jenga/*.hpp) name for name so that host code written against
+// the reference drops in; the internals are our own: bitmap free lists with
+// a summary level instead of std::set, flat per-large-page unit tables instead
+// of std::map, and owner ids instead of owner strings.  Exported only through
+// the C ABI in include/jenga_gpu.h (the .so is built -fvisibility=hidden).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+namespace jenga {
+
+// reference util.hpp:11-21
+class ConfigError : public std::runtime_error {
+ public:
+  explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+class InvariantError : public std::logic_error {
+ public:
+  explicit InvariantError(const std::string& m) : std::logic_error(m) {}
+};
+
+#define JENGA_CHECK(cond, msg)                                                  \
+  do {                                                                          \
+    if (!(cond)) throw ::jenga::InvariantError(std::string(msg) + " [" #cond "]"); \
+  } while (0)
+
+uint64_t checked_mul(uint64_t a, uint64_t b, const char* what);
+uint64_t checked_add(uint64_t a, uint64_t b, const char* what);
+
+// splitmix64 finalizer (reference util.hpp:47-55) and FNV-1a (:57-64): the
+// prefix-cache block keys must hash identically to the reference's.
+inline uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+inline uint64_t mix64(uint64_t a, uint64_t b) { return mix64(a ^ mix64(b)); }
+uint64_t hash_str(const std::string& s);
+
+// ---------------------------------------------------------------- geometry
+enum class LayerKind : int {
+  kFullAttention = 0,
+  kSlidingWindow = 1,
+  kMamba = 2,
+  kCrossAttention = 3,
+  kVisionEmbedding = 4,
+};
+const char* layer_kind_name(LayerKind k);
+LayerKind layer_kind_from_name(const std::string& s);
+
+struct LayerGroupSpec {
+  std::string name;
+  LayerKind kind = LayerKind::kFullAttention;
+  uint32_t num_layers = 0;
+  uint64_t bytes_per_token_per_layer = 0;
+  uint32_t tokens_per_page = 1;
+  uint64_t window_tokens = 0;
+  uint64_t checkpoint_interval_tokens = 0;
+  bool stores_image_tokens() const {
+    return kind == LayerKind::kCrossAttention || kind == LayerKind::kVisionEmbedding;
+  }
+};
+
+struct ModelSpec {
+  std::string name;
+  std::vector<LayerGroupSpec> groups;
+  void validate() const;
+  bool has_cross_attention() const;
+  bool decoder_stores_images() const { return !has_cross_attention(); }
+};
+
+uint64_t small_page_size(const LayerGroupSpec& g);
+uint64_t lcm_page_size(const ModelSpec& spec);
+double lcm_blowup_ratio(const ModelSpec& spec);
+ModelSpec parse_model_spec_json(const std::string& text);
+
+// ---------------------------------------------------------------- ids
+struct LargePageId {
+  uint32_t index = UINT32_MAX;
+  bool valid() const { return index != UINT32_MAX; }
+  friend bool operator==(LargePageId a, LargePageId b) { return a.index == b.index; }
+};
+struct SmallPageId {
+  LargePageId large;
+  uint32_t slot = 0;
+  friend bool operator==(const SmallPageId& a, const SmallPageId& b) {
+    return a.large == b.large && a.slot == b.slot;
+  }
+};
+
+inline constexpr uint64_t kNoRequest = UINT64_MAX;
+enum class SmallPageState : uint8_t { kEmpty = 0, kEvictable = 1, kUsed = 2 };
+
+struct SmallPageRecord {
+  SmallPageState state = SmallPageState::kEmpty;
+  bool has_cache_key = false;
+  uint64_t associated_request = kNoRequest;
+  uint64_t last_access = 0;
+  uint64_t prefix_length = 0;
+  uint64_t cache_key = 0;
+};
+
+// Lowest-set-bit search over a dense bitmap with one summary word per 64
+// words: find_first is two ctz scans, set/clear are O(1).  Replaces the
+// reference's ordered std::set free lists (lcm_allocator.hpp:57,
+// type_allocator.hpp:179) with identical lowest-index-first order.
+class FirstFitBitmap {
+ public:
+  void resize(uint64_t nbits);
+  void set(uint64_t i);
+  void clear(uint64_t i);
+  bool test(uint64_t i) const { return (words_[i >> 6] >> (i & 63)) & 1ULL; }
+  uint64_t find_first() const;  // UINT64_MAX when empty
+  uint64_t count() const { return count_; }
+  uint64_t size() const { return nbits_; }
+
+ private:
+  uint64_t nbits_ = 0, count_ = 0;
+  std::vector<uint64_t> words_, summary_, top_;
+};
+
+// ---------------------------------------------------------------- level 1
+// reference lcm_allocator.hpp:29-59 / lcm_allocator.cpp:7-40
+class LargePagePool {
+ public:
+  LargePagePool(uint64_t capacity_bytes, uint64_t large_page_bytes);
+  std::optional<LargePageId> request_large_page(int owner);
+  void return_large_page(LargePageId id);
+  bool is_free(LargePageId id) const;
+  int owner_of(LargePageId id) const;
+  uint32_t num_pages() const { return static_cast<uint32_t>(owners_.size()); }
+  uint32_t num_free() const { return static_cast<uint32_t>(free_.count()); }
+  uint64_t large_page_bytes() const { return page_bytes_; }
+  uint64_t free_bytes() const { return uint64_t{num_free()} * page_bytes_; }
+  uint64_t reserved_remainder_bytes() const { return remainder_; }
+  void check_conservation() const;
+
+ private:
+  uint64_t page_bytes_ = 0, remainder_ = 0;
+  std::vector<int16_t> owners_;  // -1 = free
+  FirstFitBitmap free_;
+};
+
+// ---------------------------------------------------------------- level 2
+struct GroupGeometry {
+  std::string group_name;
+  uint64_t small_page_bytes = 0;
+  uint32_t slots_per_large = 1;
+};
+
+struct UnitEvictionCandidate {
+  uint64_t lru_timestamp = 0;
+  uint64_t max_prefix_length = 0;
+  uint32_t first_index = 0;
+  bool better_than(const UnitEvictionCandidate& o) const {
+    if (lru_timestamp != o.lru_timestamp) return lru_timestamp < o.lru_timestamp;
+    if (max_prefix_length != o.max_prefix_length) return max_prefix_length > o.max_prefix_length;
+    return first_index < o.first_index;
+  }
+};
+
+struct FragmentationReport {
+  uint64_t used_bytes = 0, evictable_bytes = 0, empty_stranded_bytes = 0;
+};
+
+// reference type_allocator.hpp:81-182.  Jenga geometry only (LCM >= every
+// small page, so one unit == one large page).
+class TypeAllocator {
+ public:
+  TypeAllocator(GroupGeometry geo, int owner_id, LargePagePool* pool);
+  const GroupGeometry& geometry() const { return geo_; }
+
+  std::optional<SmallPageId> try_allocate_associated(uint64_t request);
+  std::optional<SmallPageId> try_allocate_from_new_unit(uint64_t request);
+  std::optional<SmallPageId> try_allocate_any(uint64_t request);
+  std::optional<SmallPageId> lru_evictable_small() const;
+  uint64_t evict_small(SmallPageId id);
+  void allocate_slot(SmallPageId id, uint64_t request);
+  void free(SmallPageId id, std::optional<uint64_t> cache_key);
+  void pin(SmallPageId id, uint64_t request);
+  void touch(SmallPageId id, uint64_t step);
+  void set_prefix_length(SmallPageId id, uint64_t len);
+  const SmallPageRecord& record(SmallPageId id) const;
+  bool tracks(SmallPageId id) const;
+  std::vector<UnitEvictionCandidate> fully_evictable_units() const;
+  std::vector<uint64_t> clear_unit(uint32_t first_index);
+  FragmentationReport fragmentation_report() const;
+
+  uint64_t used_pages() const { return used_; }
+  uint64_t evictable_pages() const { return lru_.size(); }
+  uint64_t empty_pages() const { return empty_.count(); }
+  uint64_t owned_units() const { return owned_units_; }
+  bool has_associated_empty(uint64_t request) const;
+  void check_invariants() const;
+
+  uint64_t global_index(uint32_t large, uint32_t slot) const {
+    return uint64_t{large} * geo_.slots_per_large + slot;
+  }
+  SmallPageId from_global(uint64_t g) const {
+    return SmallPageId{LargePageId{static_cast<uint32_t>(g / geo_.slots_per_large)},
+                       static_cast<uint32_t>(g % geo_.slots_per_large)};
+  }
+
+ private:
+  struct Unit {
+    bool owned = false;
+    uint32_t empty_count = 0, evictable_count = 0;
+    std::vector<SmallPageRecord> slots;  // allocated while owned
+  };
+  using LruKey = std::tuple<uint64_t, uint64_t, uint64_t>;  // (last_access, ~prefix, global)
+
+  Unit& unit_of(SmallPageId id);
+  const Unit& unit_of(SmallPageId id) const;
+  SmallPageRecord& rec(SmallPageId id);
+  void index_on_empty(uint64_t g, const SmallPageRecord& r);
+  void unindex_on_empty(uint64_t g, const SmallPageRecord& r);
+  void release_unit(uint32_t large);
+  static LruKey lru_key(const SmallPageRecord& r, uint64_t g) {
+    return LruKey{r.last_access, UINT64_MAX - r.prefix_length, g};
+  }
+
+  GroupGeometry geo_;
+  int owner_id_;
+  LargePagePool* pool_;
+  std::vector<Unit> units_;               // indexed by large page index
+  uint64_t owned_units_ = 0;
+  std::set<LruKey> lru_;                  // begin() = eviction front
+  FirstFitBitmap empty_;                  // global indices of empty owned slots
+  // request -> its associated empty slots (global indices, kept sorted)
+  std::unordered_map<uint64_t, std::vector<uint64_t>> empty_by_request_;
+  std::set<uint32_t> fully_evictable_;    // units whose every slot is evictable
+  uint64_t used_ = 0;
+};
+
+// ---------------------------------------------------------------- prefix cache
+// reference prefix_cache.hpp:20-80
+struct BlockContent {
+  uint64_t key = 0, parent_key = 0;
+  std::vector<uint64_t> tokens;
+  bool matches(const BlockContent& o) const {
+    return key == o.key && parent_key == o.parent_key && tokens == o.tokens;
+  }
+};
+uint64_t block_chain_salt(const std::string& group_name);
+uint64_t chain_block_key(uint64_t parent, const std::vector<uint64_t>& tokens);
+
+class PrefixCache {
+ public:
+  explicit PrefixCache(size_t n) : by_group_(n) {}
+  void register_block(size_t g, const BlockContent& c, SmallPageId page);
+  void unregister(size_t g, uint64_t key, SmallPageId page);
+  std::optional<SmallPageId> find(size_t g, const BlockContent& c) const;
+  uint64_t entries(size_t g) const;
+
+ private:
+  struct Entry {
+    BlockContent content;
+    SmallPageId page;
+  };
+  std::vector<std::unordered_map<uint64_t, std::vector<Entry>>> by_group_;
+};
+
+// ---------------------------------------------------------------- engine
+struct AllocResult {
+  SmallPageId page;
+  int step = 0;
+};
+
+// reference kv_allocator.hpp:62-119 (Jenga strategy: one LCM pool).
+class KvAllocator {
+ public:
+  KvAllocator(const ModelSpec& spec, uint64_t budget_bytes);
+  size_t num_groups() const { return spec_.groups.size(); }
+  const LayerGroupSpec& group(size_t g) const { return spec_.groups[g]; }
+  const ModelSpec& spec() const { return spec_; }
+  TypeAllocator& type_allocator(size_t g) { return *types_[g]; }
+  const TypeAllocator& type_allocator(size_t g) const { return *types_[g]; }
+  LargePagePool& pool() { return *pool_; }
+  const LargePagePool& pool() const { return *pool_; }
+  PrefixCache& cache() { return cache_; }
+  const PrefixCache& cache() const { return cache_; }
+
+  std::optional<AllocResult> allocate(size_t g, uint64_t request);
+  void free(size_t g, SmallPageId page, const std::optional<BlockContent>& cached);
+  void pin(size_t g, SmallPageId page, uint64_t request);
+  std::optional<LargePageId> evict_lru_large_page();
+  void set_request_aware(bool on) { request_aware_ = on; }
+  uint64_t budget_bytes() const { return budget_; }
+  const uint64_t* alloc_step_counts() const { return step_counts_; }
+  void check_invariants() const;
+
+ private:
+  ModelSpec spec_;
+  uint64_t budget_ = 0;
+  bool request_aware_ = true;
+  std::unique_ptr<LargePagePool> pool_;
+  std::vector<std::unique_ptr<TypeAllocator>> types_;
+  PrefixCache cache_;
+  uint64_t step_counts_[6] = {0, 0, 0, 0, 0, 0};
+};
+
+// ---------------------------------------------------------------- address map
+struct ByteRange {
+  uint64_t begin = 0, end = 0;
+};
+struct LayerView {
+  uint64_t start_offset = 0, page_stride = 0, exec_page_size = 0;
+};
+
+// reference memory_layout.hpp:34-69
+class AddressMap {
+ public:
+  explicit AddressMap(const ModelSpec& spec);
+  uint64_t large_page_bytes() const { return large_; }
+  size_t num_groups() const { return spec_.groups.size(); }
+  uint64_t small_page_bytes(size_t g) const { return small_[g]; }
+  uint64_t per_layer_bytes(size_t g) const { return per_layer_[g]; }
+  uint32_t slots_per_large(size_t g) const { return slots_[g]; }
+  uint64_t global_page_index(size_t g, SmallPageId p) const;
+  ByteRange address_of(size_t g, uint32_t layer, SmallPageId p) const;
+  LayerView layer_view(size_t g, uint32_t layer) const;
+  ByteRange view_address(size_t g, uint32_t layer, SmallPageId p) const;
+
+ private:
+  ModelSpec spec_;
+  uint64_t large_ = 0;
+  std::vector<uint64_t> small_, per_layer_;
+  std::vector<uint32_t> slots_;
+};
+
+// ---------------------------------------------------------------- policies
+// reference layer_policies.cpp:79-120
+bool needs_token(const LayerGroupSpec& g, uint64_t i, uint64_t new_tokens,
+                 uint64_t consumed_tokens);
+std::pair<uint64_t, uint64_t> accessed_range(const LayerGroupSpec& g, uint64_t prev_tokens,
+                                             uint64_t new_tokens);
+
+// ---------------------------------------------------------------- page lists
+// The per-(request, group) page lists of reference simulator.hpp:123-139,
+// maintained with the semantics of store_position / free_block /
+// release_all_pages (simulator.cpp:196-327).
+class PageLists {
+ public:
+  PageLists(KvAllocator* kv, bool prefix_caching);
+
+  struct Block {
+    SmallPageId page;
+    bool live = false;
+  };
+  struct GroupRuntime {
+    uint64_t stored = 0;
+    std::vector<uint64_t> stored_positions;
+    std::vector<Block> blocks;
+    std::vector<BlockContent> chain;
+    uint64_t freed_blocks = 0, held_tokens = 0, live_blocks = 0;
+    std::optional<SmallPageId> working_page;
+    uint64_t checkpoints = 0;
+  };
+  struct Request {
+    uint64_t id = 0;
+    std::vector<uint64_t> tokens;
+    std::vector<uint8_t> is_image;
+    std::vector<uint64_t> image_ordinal;  // per position (image tokens only)
+    std::vector<GroupRuntime> groups;
+    bool needs_release = false;  // set by a failed (OOM) append
+  };
+
+  void add_request(uint64_t id);
+  bool has_request(uint64_t id) const { return index_.count(id) != 0; }
+  // decode_one-style append of one position to every group storing it
+  // (vision-embedding groups excluded, as prefill_some / decode do).
+  // Returns false on OOM (caller preempts).
+  bool append(uint64_t id, uint64_t token, bool is_image, uint64_t image_ordinal,
+              uint64_t now);
+  bool store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now);
+  void release(uint64_t id, bool allow_cache, uint64_t now);
+  const Request& request(uint64_t id) const;
+  bool group_stores_position(size_t g, const Request& r, uint64_t pos) const;
+
+ private:
+  Request& req(uint64_t id);
+  void append_chain(Request& r, size_t g);
+  void free_block(Request& r, size_t g, uint64_t b, bool allow_cache, uint64_t now);
+
+  KvAllocator* kv_;
+  bool prefix_caching_;
+  std::vector<Request> requests_;
+  std::unordered_map<uint64_t, size_t> index_;
+};
+
+}  // namespace jenga

@@ -1,0 +1,185 @@
+// Per-request page lists: the producer of every block table.  Semantics are
+// those of the reference simulator's GroupRuntime bookkeeping (cited per
+// method); scheduling, metrics and preemption policy stay with the caller.
+#include "jenga_host.hpp"
+
+namespace jenga {
+
+PageLists::PageLists(KvAllocator* kv, bool prefix_caching)
+    : kv_(kv), prefix_caching_(prefix_caching) {
+  JENGA_CHECK(kv_ != nullptr, "page lists need an allocator");
+}
+
+void PageLists::add_request(uint64_t id) {
+  if (index_.count(id)) throw ConfigError("duplicate request id " + std::to_string(id));
+  index_[id] = requests_.size();
+  Request r;
+  r.id = id;
+  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  requests_.push_back(std::move(r));
+}
+
+PageLists::Request& PageLists::req(uint64_t id) {
+  auto it = index_.find(id);
+  JENGA_CHECK(it != index_.end(), "unknown request");
+  return requests_[it->second];
+}
+
+const PageLists::Request& PageLists::request(uint64_t id) const {
+  auto it = index_.find(id);
+  JENGA_CHECK(it != index_.end(), "unknown request");
+  return requests_[it->second];
+}
+
+// reference simulator.cpp:151-158
+bool PageLists::group_stores_position(size_t g, const Request& r, uint64_t pos) const {
+  const LayerGroupSpec& grp = kv_->group(g);
+  const bool image = r.is_image[pos - 1] != 0;
+  if (grp.stores_image_tokens()) return image;
+  return !image || kv_->spec().decoder_stores_images();
+}
+
+// reference simulator.cpp:196-215
+void PageLists::append_chain(Request& r, size_t g) {
+  if (!prefix_caching_) return;
+  GroupRuntime& rt = r.groups[g];
+  const LayerGroupSpec& grp = kv_->group(g);
+  const uint64_t t = grp.kind == LayerKind::kMamba ? grp.checkpoint_interval_tokens
+                                                   : grp.tokens_per_page;
+  while ((rt.chain.size() + 1) * t <= rt.stored) {
+    BlockContent c;
+    c.parent_key = rt.chain.empty() ? block_chain_salt(grp.name) : rt.chain.back().key;
+    const uint64_t first = rt.chain.size() * t;
+    c.tokens.reserve(t);
+    for (uint64_t i = 0; i < t; ++i) c.tokens.push_back(r.tokens[rt.stored_positions[first + i] - 1]);
+    c.key = chain_block_key(c.parent_key, c.tokens);
+    rt.chain.push_back(std::move(c));
+  }
+}
+
+// reference simulator.cpp:217-282
+bool PageLists::store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now) {
+  Request& r = req(id);
+  JENGA_CHECK(g < r.groups.size(), "group index out of range");
+  JENGA_CHECK(pos >= 1 && pos <= r.tokens.size(), "position beyond the sequence");
+  GroupRuntime& rt = r.groups[g];
+  const LayerGroupSpec& grp = kv_->group(g);
+  TypeAllocator& ta = kv_->type_allocator(g);
+
+  if (grp.kind == LayerKind::kMamba) {
+    if (!rt.working_page.has_value()) {
+      auto res = kv_->allocate(g, id);
+      if (!res) return false;
+      rt.working_page = res->page;
+      ta.set_prefix_length(*rt.working_page, 0);
+    }
+    rt.stored++;
+    rt.stored_positions.push_back(pos);
+    append_chain(r, g);
+    const uint64_t k = grp.checkpoint_interval_tokens;
+    if (prefix_caching_ && rt.stored % k == 0) {
+      auto res = kv_->allocate(g, id);
+      if (!res) return false;
+      ta.set_prefix_length(res->page, pos);
+      ta.touch(res->page, now);
+      rt.checkpoints = rt.stored / k;
+      kv_->free(g, res->page, rt.chain[rt.checkpoints - 1]);
+    }
+    return true;
+  }
+
+  rt.stored++;
+  rt.stored_positions.push_back(pos);
+  const uint64_t t = grp.tokens_per_page;
+  const uint64_t bidx = (rt.stored - 1) / t;
+  if (bidx >= rt.blocks.size()) {
+    auto res = kv_->allocate(g, id);
+    if (!res) {
+      // Leave the ordinal un-stored so a retry after preemption is clean.
+      rt.stored--;
+      rt.stored_positions.pop_back();
+      return false;
+    }
+    rt.blocks.push_back(Block{res->page, true});
+    rt.live_blocks++;
+  } else {
+    JENGA_CHECK(rt.blocks[bidx].live, "stored into a dead block");
+  }
+  rt.held_tokens++;
+  append_chain(r, g);
+  const uint64_t ordinal_value = grp.stores_image_tokens() ? r.image_ordinal[pos - 1] : pos;
+  ta.set_prefix_length(rt.blocks[bidx].page, ordinal_value);
+
+  if (grp.kind == LayerKind::kSlidingWindow) {
+    const uint64_t w = grp.window_tokens;
+    if (rt.stored > w) {
+      const uint64_t exited = rt.stored - w;
+      while (rt.freed_blocks * t + t <= exited) free_block(r, g, rt.freed_blocks, true, now);
+    }
+  }
+  return true;
+}
+
+// reference simulator.cpp:284-312
+void PageLists::free_block(Request& r, size_t g, uint64_t b, bool allow_cache, uint64_t now) {
+  GroupRuntime& rt = r.groups[g];
+  JENGA_CHECK(b < rt.blocks.size(), "free of unknown block");
+  Block& blk = rt.blocks[b];
+  JENGA_CHECK(blk.live, "free of a dead block");
+  const uint64_t t = kv_->group(g).tokens_per_page;
+  const uint64_t covered = std::min(rt.stored, (b + 1) * t) - b * t;
+  kv_->type_allocator(g).touch(blk.page, now);
+  const bool cacheable = allow_cache && prefix_caching_ && b < rt.chain.size();
+  if (cacheable) kv_->free(g, blk.page, rt.chain[b]);
+  else kv_->free(g, blk.page, std::nullopt);
+  blk.live = false;
+  rt.live_blocks--;
+  rt.held_tokens -= covered;
+  while (rt.freed_blocks < rt.blocks.size() && !rt.blocks[rt.freed_blocks].live) rt.freed_blocks++;
+}
+
+// reference simulator.cpp:549-566 (decode_one) / 504-523 (prefill_some):
+// one position, every storing group in group order; vision-embedding groups
+// are driven separately by the caller (jenga_pages_store).
+bool PageLists::append(uint64_t id, uint64_t token, bool is_image, uint64_t image_ordinal,
+                       uint64_t now) {
+  Request& r = req(id);
+  JENGA_CHECK(!r.needs_release, "append after OOM: release (preempt) the request first");
+  r.tokens.push_back(token);
+  r.is_image.push_back(is_image ? 1 : 0);
+  r.image_ordinal.push_back(image_ordinal);
+  const uint64_t pos = r.tokens.size();
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    if (kv_->group(g).kind == LayerKind::kVisionEmbedding) continue;
+    if (!group_stores_position(g, r, pos)) continue;
+    if (!store_position(id, g, pos, now)) {
+      // The reference pops the token on a failed decode (simulator.cpp:557-561).
+      Request& rr = req(id);
+      rr.tokens.pop_back();
+      rr.is_image.pop_back();
+      rr.image_ordinal.pop_back();
+      rr.needs_release = true;
+      return false;
+    }
+  }
+  return true;
+}
+
+// reference simulator.cpp:314-327
+void PageLists::release(uint64_t id, bool allow_cache, uint64_t now) {
+  Request& r = req(id);
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    GroupRuntime& rt = r.groups[g];
+    for (uint64_t b = 0; b < rt.blocks.size(); ++b)
+      if (rt.blocks[b].live) free_block(r, g, b, allow_cache && prefix_caching_, now);
+    if (rt.working_page.has_value()) {
+      kv_->type_allocator(g).touch(*rt.working_page, now);
+      kv_->free(g, *rt.working_page, std::nullopt);
+      rt.working_page.reset();
+    }
+  }
+  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  r.needs_release = false;
+}
+
+}  // namespace jenga

@@ -1,0 +1,72 @@
+// One contiguous HBM arena per GPU: the device image of the reference's
+// LargePagePool capacity (lcm_allocator.cpp:7-19, pages = capacity / LCM).
+// Large page i occupies bytes [i*LCM, (i+1)*LCM); small page g of a group is
+// at g*small_page_bytes (memory_layout.cpp:29-39), so the arena is addressed
+// purely by the AddressMap arithmetic — no per-layer tensors.
+#include <mutex>
+
+#include "common.cuh"
+
+namespace jenga_dev {
+std::atomic<uint64_t> g_launches{0};
+}  // namespace jenga_dev
+
+// The host half owns jenga_last_error(); kernels report through it too.
+extern "C" const char* jenga_last_error(void);
+namespace jenga_host_err {
+int set(int code, const char* msg);
+}
+
+namespace jenga_dev {
+int set_error(int code, const std::string& msg) { return jenga_host_err::set(code, msg.c_str()); }
+}  // namespace jenga_dev
+
+struct jenga_arena {
+  int device = 0;
+  void* base = nullptr;
+  uint64_t bytes = 0;
+};
+
+JENGA_EXPORT int jenga_arena_create(int device, uint64_t num_large_pages, uint64_t large_page_bytes,
+                                    jenga_arena** out) {
+  using namespace jenga_dev;
+  if (out == nullptr || large_page_bytes == 0) return set_error(JENGA_ERR_ARG, "invalid arena arguments");
+  uint64_t bytes = 0;
+  if (__builtin_mul_overflow(num_large_pages, large_page_bytes, &bytes))
+    return set_error(JENGA_ERR_CONFIG, "byte arithmetic overflow in arena size");
+  if (large_page_bytes % 16 != 0)
+    return set_error(JENGA_ERR_CONFIG, "large page bytes must be a multiple of 16 for vector access");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_error(JENGA_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  void* p = nullptr;
+  e = cudaMalloc(&p, bytes ? bytes : 256);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess)
+    return set_error(JENGA_ERR_CUDA, std::string("arena cudaMalloc(") + std::to_string(bytes) +
+                                         "): " + cudaGetErrorString(e));
+  auto* a = new jenga_arena;
+  a->device = device;
+  a->base = p;
+  a->bytes = bytes;
+  *out = a;
+  return JENGA_OK;
+}
+
+JENGA_EXPORT void jenga_arena_destroy(jenga_arena* arena) {
+  if (arena == nullptr) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(arena->device);
+  cudaFree(arena->base);
+  cudaSetDevice(prev);
+  delete arena;
+}
+
+JENGA_EXPORT void* jenga_arena_base(const jenga_arena* arena) { return arena ? arena->base : nullptr; }
+JENGA_EXPORT uint64_t jenga_arena_bytes(const jenga_arena* arena) { return arena ? arena->bytes : 0; }
+
+JENGA_EXPORT uint64_t jenga_kernel_launch_count(void) {
+  return jenga_dev::g_launches.load(std::memory_order_relaxed);
+}

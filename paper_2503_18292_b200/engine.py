@@ -1,0 +1,161 @@
+"""Per-GPU decode harness: the device-side replacement of the reference's
+SimEngine::decode_one / step data path (reference simulator.cpp:549-566,
+642-677).  Per step it (1) runs the native Jenga allocator on the host
+(store_position semantics), (2) packs each group's page lists and uploads
+them from pinned memory, (3) builds block tables / slot mappings on the
+device, and (4) per layer scatters new K/V and runs paged decode against the
+layer view of the single HBM arena.  Scheduling policy stays with the caller.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from ._lib import check, lib
+from .geometry import GroupGeometry, ModelGeometry
+from .jenga import AddressMap, KvAllocator, LayerKind, LayerView, PageLists
+
+
+@dataclass
+class GroupTables:
+    geom: GroupGeometry
+    slots_per_large: int
+    small_page_bytes: int
+    max_blocks: int
+    block_table: torch.Tensor      # int32 [max_batch, max_blocks]
+    seq_lens: torch.Tensor         # int32 [max_batch]
+    slot_mapping: torch.Tensor     # int64 [max_batch] (newest ordinal of each request)
+    h_offsets: torch.Tensor        # pinned int32 [max_batch+1]
+    h_pages: torch.Tensor          # pinned int32 [max_batch*max_blocks, 2]
+    h_first_live: torch.Tensor     # pinned int32 [max_batch]
+    h_n_stored: torch.Tensor       # pinned int32 [max_batch]
+    d_offsets: torch.Tensor
+    d_pages: torch.Tensor
+    d_first_live: torch.Tensor
+    d_n_stored: torch.Tensor
+    workspace: Optional[ops.DecodeWorkspace] = None
+
+
+class DecodeEngine:
+    def __init__(self, geom: ModelGeometry, num_large_pages: int, max_batch: int, max_tokens: int,
+                 device: Optional[torch.device] = None, prefix_caching: bool = False):
+        self.geom = geom
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        self.spec = geom.spec()
+        self.addr = AddressMap(self.spec)
+        self.large_page_bytes = self.addr.large_page_bytes()
+        self.kv = KvAllocator(self.spec, num_large_pages * self.large_page_bytes)
+        self.pages = PageLists(self.kv, prefix_caching)
+        self.arena = ops.Arena(num_large_pages, self.large_page_bytes, self.device.index)
+        self.max_batch = max_batch
+        self.requests: List[int] = []
+        self._req_arr = np.zeros(max_batch, dtype=np.uint64)
+        self.now = 0
+        self.tables: List[GroupTables] = []
+        for g, gg in enumerate(geom.groups):
+            tpp = self.spec.groups[g].tokens_per_page
+            max_blocks = 1 if gg.kind == LayerKind.kMamba else math.ceil(max_tokens / tpp) + 1
+            pin = dict(dtype=torch.int32, pin_memory=True)
+            dev = dict(dtype=torch.int32, device=self.device)
+            t = GroupTables(
+                geom=gg, slots_per_large=self.addr.slots_per_large(g),
+                small_page_bytes=self.addr.small_page_bytes(g), max_blocks=max_blocks,
+                block_table=torch.full((max_batch, max_blocks), -1, **dev),
+                seq_lens=torch.zeros(max_batch, **dev),
+                slot_mapping=torch.full((max_batch,), -1, dtype=torch.int64, device=self.device),
+                h_offsets=torch.zeros(max_batch + 1, **pin),
+                h_pages=torch.zeros((max_batch * max_blocks, 2), **pin),
+                h_first_live=torch.zeros(max_batch, **pin), h_n_stored=torch.zeros(max_batch, **pin),
+                d_offsets=torch.zeros(max_batch + 1, **dev), d_pages=torch.zeros((max_batch * max_blocks, 2), **dev),
+                d_first_live=torch.zeros(max_batch, **dev), d_n_stored=torch.zeros(max_batch, **dev))
+            if gg.is_attention:
+                t.workspace = ops.DecodeWorkspace(max_batch, gg.num_q_heads, gg.num_kv_heads, gg.head_dim,
+                                                  max_blocks, tpp, self.device)
+            self.tables.append(t)
+        self._views: Dict[tuple, LayerView] = {}
+
+    # ------------------------------------------------------------ host side
+    def add_requests(self, ids: Sequence[int]) -> None:
+        for r in ids:
+            self.pages.add_request(int(r))
+            self.requests.append(int(r))
+        if len(self.requests) > self.max_batch:
+            raise ValueError("batch exceeds max_batch")
+        self._req_arr[: len(self.requests)] = self.requests
+
+    def append(self, ids: Optional[Sequence[int]] = None, tokens=None, is_image=None) -> int:
+        """One decode step of the host allocator for `ids` (default: the batch)."""
+        ids = self.requests if ids is None else ids
+        done = self.pages.append_batch(ids, tokens, is_image, now=self.now)
+        self.now += 1
+        return done
+
+    def view(self, g: int, layer: int) -> LayerView:
+        key = (g, layer)
+        v = self._views.get(key)
+        if v is None:
+            v = self._views[key] = self.addr.layer_view(g, layer)
+        return v
+
+    # ------------------------------------------------------------ device tables
+    def sync_tables(self, groups: Optional[Sequence[int]] = None) -> None:
+        """Pack page lists -> pinned -> H2D (async) -> device block-table build."""
+        n = len(self.requests)
+        rp = self._req_arr.ctypes.data_as(C.POINTER(C.c_uint64))
+        for g in (range(len(self.tables)) if groups is None else groups):
+            t = self.tables[g]
+            check(lib.jenga_pages_pack_csr(
+                self.pages.h, g, rp, n, C.cast(t.h_offsets.data_ptr(), C.POINTER(C.c_int32)),
+                C.cast(t.h_pages.data_ptr(), C.POINTER(_lib.SmallPage)),
+                C.cast(t.h_first_live.data_ptr(), C.POINTER(C.c_int32)),
+                C.cast(t.h_n_stored.data_ptr(), C.POINTER(C.c_int32))))
+            total = int(t.h_offsets[n])
+            if total > t.h_pages.shape[0]:
+                raise OverflowError("page lists exceed the table capacity (raise max_tokens)")
+            t.d_offsets[: n + 1].copy_(t.h_offsets[: n + 1], non_blocking=True)
+            if total:
+                t.d_pages[:total].copy_(t.h_pages[:total], non_blocking=True)
+            t.d_first_live[:n].copy_(t.h_first_live[:n], non_blocking=True)
+            t.d_n_stored[:n].copy_(t.h_n_stored[:n], non_blocking=True)
+            tpp = self.spec.groups[g].tokens_per_page
+            ops.build_block_tables(t.d_offsets[: n + 1], t.d_pages, t.d_first_live, t.d_n_stored,
+                                   t.slots_per_large, tpp, t.max_blocks, t.block_table, t.slot_mapping, t.seq_lens)
+
+    # ------------------------------------------------------------ per layer ops
+    def write_kv(self, g: int, layer: int, key: torch.Tensor, value: torch.Tensor,
+                 slots: Optional[torch.Tensor] = None) -> None:
+        t = self.tables[g]
+        n = key.shape[0]
+        ops.reshape_and_cache(self.arena, self.view(g, layer), key, value,
+                              t.slot_mapping[:n] if slots is None else slots, self.spec.groups[g].tokens_per_page)
+
+    def decode(self, g: int, layer: int, q: torch.Tensor, out: torch.Tensor, scale: Optional[float] = None,
+               softcap: Optional[float] = None) -> torch.Tensor:
+        t = self.tables[g]
+        gg = t.geom
+        B = q.shape[0]
+        return ops.paged_decode(self.arena, self.view(g, layer), int(gg.kind), q, out, t.block_table[:B],
+                                t.seq_lens[:B], gg.num_kv_heads, self.spec.groups[g].tokens_per_page,
+                                gg.head_dim ** -0.5 if scale is None else scale, window=gg.window,
+                                softcap=self.geom.softcap if softcap is None else softcap, workspace=t.workspace)
+
+    def mamba_page_globals(self, g: int) -> torch.Tensor:
+        """int64 global index of each request's working state page (-1: none)."""
+        t = self.tables[g]
+        B = len(self.requests)
+        return torch.where(t.seq_lens[:B] > 0, t.block_table[:B, 0].to(torch.int64),
+                           torch.full((B,), -1, dtype=torch.int64, device=self.device))
+
+    def live_tokens(self, g: int) -> np.ndarray:
+        """Host copy of live ordinals per request (SWA: min(W, n))."""
+        t = self.tables[g]
+        n = t.h_n_stored[: len(self.requests)].numpy().astype(np.int64)
+        if t.geom.kind == LayerKind.kSlidingWindow:
+            n = np.minimum(n, t.geom.window)
+        return n

@@ -1,0 +1,163 @@
+"""Device-side operations over the C ABI, taking torch tensors as plumbing.
+
+Every function launches a kernel of libjenga_b200.so on the current torch
+stream; none has a CPU or PyTorch fallback — a missing library or a CPU
+tensor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .jenga import LayerKind, LayerView
+
+DTYPE_CODE = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("jenga ops take CUDA tensors only (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype, name: str):
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class Arena:
+    """One contiguous HBM arena per GPU (jenga_arena_create): num_large_pages
+    x large_page_bytes, the device image of the reference LargePagePool."""
+
+    def __init__(self, num_large_pages: int, large_page_bytes: int, device: Optional[int] = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        self.h = C.c_void_p()
+        check(lib.jenga_arena_create(device, int(num_large_pages), int(large_page_bytes), C.byref(self.h)))
+        self.num_large_pages = int(num_large_pages)
+        self.large_page_bytes = int(large_page_bytes)
+        self.nbytes = int(lib.jenga_arena_bytes(self.h))
+        self.base = int(lib.jenga_arena_base(self.h))
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.base, False), "version": 3,
+                "strides": None}
+
+    def tensor(self) -> torch.Tensor:
+        """Zero-copy uint8 view of the whole arena (for tests / inspection)."""
+        return torch.as_tensor(self, device=f"cuda:{self.device}")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.jenga_arena_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def build_block_tables(offsets: torch.Tensor, pages: torch.Tensor, first_live: torch.Tensor,
+                       n_stored: torch.Tensor, slots_per_large: int, tokens_per_page: int, max_blocks: int,
+                       block_table: torch.Tensor, slot_mapping: Optional[torch.Tensor] = None,
+                       seq_lens: Optional[torch.Tensor] = None) -> None:
+    """CSR page lists -> int32 block_table[B][max_blocks] of AddressMap global
+    indices (-1 dead/absent), plus the newest token's slot and seq_lens."""
+    batch = offsets.numel() - 1
+    _need(offsets, torch.int32, "offsets")
+    _need(block_table, torch.int32, "block_table")
+    if pages.dtype not in (torch.int32,) or pages.dim() != 2 or pages.shape[-1] != 2:
+        raise TypeError("pages must be int32 [N, 2] ({large, slot} pairs)")
+    if block_table.numel() < batch * max_blocks:
+        raise ValueError("block_table too small")
+    check(lib.jenga_build_block_tables(_ptr(offsets), _ptr(pages), _ptr(first_live), _ptr(n_stored), batch,
+                                       slots_per_large, tokens_per_page, max_blocks, _ptr(block_table),
+                                       _ptr(slot_mapping), _ptr(seq_lens), _stream()))
+
+
+def slot_mapping(block_table: torch.Tensor, max_blocks: int, req: torch.Tensor, ordinal: torch.Tensor,
+                 tokens_per_page: int, out: torch.Tensor) -> None:
+    check(lib.jenga_slot_mapping(_ptr(block_table), max_blocks, _ptr(req), _ptr(ordinal), req.numel(),
+                                 tokens_per_page, _ptr(out), _stream()))
+
+
+def reshape_and_cache(arena: Arena, view: LayerView, key: torch.Tensor, value: torch.Tensor,
+                      slots: torch.Tensor, tokens_per_page: int) -> None:
+    """key/value [T, Hkv, D] -> their slots in one layer view."""
+    if key.shape != value.shape or key.dim() != 3:
+        raise ValueError("key/value must both be [T, Hkv, D]")
+    _need(slots, torch.int64, "slot_mapping")
+    if key.stride(-1) != 1 or key.stride(-2) != key.shape[-1] or value.stride() != key.stride():
+        raise ValueError("key/value rows must be contiguous with equal strides")
+    T, hkv, d = key.shape
+    check(lib.jenga_reshape_and_cache(arena.base, view.c(), DTYPE_CODE[key.dtype], hkv, d, tokens_per_page,
+                                      _ptr(key), _ptr(value), key.stride(0), _ptr(slots), T, _stream()))
+
+
+class DecodeWorkspace:
+    """Scratch for split-KV partials + per-(request, head) tickets."""
+
+    def __init__(self, batch, num_q_heads, num_kv_heads, head_dim, max_blocks, tokens_per_page, device=None):
+        self.nbytes = int(lib.jenga_paged_decode_workspace_size(batch, num_q_heads, num_kv_heads, head_dim,
+                                                                max_blocks, tokens_per_page))
+        self.buf = torch.zeros(max(self.nbytes, 256), dtype=torch.uint8, device=device or "cuda")
+
+
+def paged_decode(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out: torch.Tensor,
+                 block_table: torch.Tensor, seq_lens: torch.Tensor, num_kv_heads: int, tokens_per_page: int,
+                 scale: float, window: int = 0, softcap: float = 0.0,
+                 workspace: Optional[DecodeWorkspace] = None) -> torch.Tensor:
+    """q/out [B, Hq, D]; block_table int32 [B, max_blocks]; seq_lens int32 [B]."""
+    B, hq, d = q.shape
+    _need(q, q.dtype, "q")
+    _need(out, q.dtype, "out")
+    _need(block_table, torch.int32, "block_table")
+    _need(seq_lens, torch.int32, "seq_lens")
+    max_blocks = block_table.shape[-1]
+    if workspace is None:
+        workspace = DecodeWorkspace(B, hq, num_kv_heads, d, max_blocks, tokens_per_page, q.device)
+    check(lib.jenga_paged_decode(arena.base, view.c(), int(kind), DTYPE_CODE[q.dtype], int(window), _ptr(q),
+                                 _ptr(out), _ptr(block_table), _ptr(seq_lens), B, max_blocks, hq, num_kv_heads, d,
+                                 tokens_per_page, float(scale), float(softcap), workspace.buf.data_ptr(),
+                                 workspace.nbytes, _stream()))
+    return out
+
+
+def mamba_state_gather(arena: Arena, view: LayerView, page_globals: torch.Tensor, dense: torch.Tensor) -> None:
+    _need(page_globals, torch.int64, "page_globals")
+    check(lib.jenga_mamba_state_gather(arena.base, view.c(), _ptr(page_globals), page_globals.numel(),
+                                       _ptr(dense), _stream()))
+
+
+def mamba_state_scatter(arena: Arena, view: LayerView, page_globals: torch.Tensor, dense: torch.Tensor) -> None:
+    _need(page_globals, torch.int64, "page_globals")
+    check(lib.jenga_mamba_state_scatter(arena.base, view.c(), _ptr(page_globals), page_globals.numel(),
+                                        _ptr(dense), _stream()))
+
+
+def page_copy(arena: Arena, small_page_bytes: int, src_globals: torch.Tensor, dst_globals: torch.Tensor) -> None:
+    _need(src_globals, torch.int64, "src_globals")
+    _need(dst_globals, torch.int64, "dst_globals")
+    check(lib.jenga_page_copy(arena.base, small_page_bytes, _ptr(src_globals), _ptr(dst_globals),
+                              src_globals.numel(), _stream()))
+
+
+def kernel_launch_count() -> int:
+    return int(lib.jenga_kernel_launch_count())
+
+
+KIND = {"full": int(LayerKind.kFullAttention), "sliding_window": int(LayerKind.kSlidingWindow),
+        "cross_attention": int(LayerKind.kCrossAttention)}

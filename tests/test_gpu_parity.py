@@ -1,0 +1,182 @@
+"""GPU parity: every kernel through the C ABI against the CPU oracle on the
+same seeded inputs.  Integer/byte work is bit-exact; attention is within the
+north-star tolerance (fp32 1e-5, bf16 1e-2 relative), written per test."""
+import numpy as np
+import pytest
+import torch
+
+from gpu_scenarios import ORC_DTYPE, TOL, arena_host, fill_group_kv, make_engine, rel_err
+from oracle.oracle import CROSS, FULL, SWA
+from paper_2503_18292_b200 import LayerKind, ops
+from paper_2503_18292_b200.geometry import GroupGeometry, ModelGeometry, toy
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_tables(orc, eng, g):
+    t = eng.tables[g]
+    B = len(eng.requests)
+    off, pages, live0, nst = eng.pages.pack_csr(g, eng.requests)
+    return orc.build_block_tables(off, pages, live0, nst, t.slots_per_large, eng.spec.groups[g].tokens_per_page,
+                                  t.max_blocks)
+
+
+def check_tables(orc, eng):
+    B = len(eng.requests)
+    for g in range(len(eng.tables)):
+        t = eng.tables[g]
+        table, slots, seq = oracle_tables(orc, eng, g)
+        np.testing.assert_array_equal(t.block_table[:B].cpu().numpy(), table)
+        np.testing.assert_array_equal(t.slot_mapping[:B].cpu().numpy(), slots)
+        np.testing.assert_array_equal(t.seq_lens[:B].cpu().numpy(), seq)
+
+
+def run_decode_parity(orc, eng, g, layer, seed=1, softcap=0.0):
+    t = eng.tables[g]
+    gg = t.geom
+    B = len(eng.requests)
+    gen = torch.Generator(device=eng.device).manual_seed(seed)
+    q = torch.randn((B, gg.num_q_heads, gg.head_dim), generator=gen, device=eng.device).to(gg.dtype)
+    out = torch.empty_like(q)
+    scale = gg.head_dim ** -0.5
+    eng.decode(g, layer, q, out, scale=scale, softcap=softcap)
+    torch.cuda.synchronize()
+    arena = arena_host(eng)
+    table = t.block_table[:B].cpu().numpy()
+    seq = t.seq_lens[:B].cpu().numpy()
+    qh = q.view(torch.int16).cpu().numpy() if gg.dtype != torch.float32 else q.cpu().numpy()
+    want = orc.paged_decode(arena, tuple(eng.view(g, layer)), int(gg.kind), ORC_DTYPE[gg.dtype], gg.window, qh,
+                            table, seq, gg.num_q_heads, gg.num_kv_heads, gg.head_dim,
+                            eng.spec.groups[g].tokens_per_page, scale, softcap, nthreads=8)
+    got = out.float().cpu().numpy()
+    assert np.isfinite(got).all()
+    tol = TOL[gg.dtype]
+    err = rel_err(got, want)
+    assert err <= tol, f"relative error {err:.3g} > {tol}"
+    np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
+    return err
+
+
+@pytest.mark.parametrize("tpp", [16, 1])
+def test_toy_config_fp32(orc, tpp):
+    """configs[0]: 1 full + 1 SWA-512, Hkv=8, D=128, Hq=16, B=8 x ~2k, fp32 (tol 1e-5)."""
+    geom = toy(tpp)
+    lens = [2048, 2047, 1, 513, 512, 2000, 1500, 2048]
+    eng, ids = make_engine(geom, lens)
+    check_tables(orc, eng)
+    for g in range(2):
+        fill_group_kv(eng, g, [0], seed=g)
+        run_decode_parity(orc, eng, g, 0)
+
+
+def test_reshape_and_cache_bit_exact(orc):
+    geom = ModelGeometry("rc", [GroupGeometry("full", LayerKind.kFullAttention, 3, 4, 8, 64, torch.bfloat16, 8)])
+    eng, ids = make_engine(geom, [37, 5, 64, 100], poison=False)
+    before = arena_host(eng).copy()
+    req, ords, kvs, slots = fill_group_kv(eng, 0, [1, 2], seed=4)
+    after = arena_host(eng)
+    want = before.copy()
+    sl = slots.cpu().numpy()
+    for layer, (K, V) in zip([1, 2], kvs):
+        orc.reshape_and_cache(want, tuple(eng.view(0, layer)), ORC_DTYPE[torch.bfloat16], 4, 64, 8,
+                              K.view(torch.int16).cpu().numpy(), V.view(torch.int16).cpu().numpy(), sl)
+    np.testing.assert_array_equal(after, want)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("kind", [LayerKind.kFullAttention, LayerKind.kSlidingWindow])
+@pytest.mark.parametrize("hd,hq,hkv,tpp", [(256, 16, 8, 16), (128, 32, 8, 32), (64, 8, 8, 4), (128, 64, 8, 2)])
+def test_decode_shapes(orc, dtype, kind, hd, hq, hkv, tpp):
+    window = 300 if kind == LayerKind.kSlidingWindow else 0
+    geom = ModelGeometry("s", [GroupGeometry("g", kind, 2, hkv, hq, hd, dtype, tpp, window=window)])
+    lens = [1, 17, 299, 300, 301, 1025, 777]
+    eng, ids = make_engine(geom, lens, seed=hd + tpp)
+    check_tables(orc, eng)
+    fill_group_kv(eng, 0, [1], seed=3)
+    run_decode_parity(orc, eng, 0, 1, seed=7)
+
+
+def test_gemma_shapes_bf16_long_context(orc):
+    """Gemma-2-9B head geometry (Hq=16, Hkv=8, D=256, tpp=16), window 4096 at
+    8k context, 2 layers per group to keep the arena small; softcap on."""
+    geom = ModelGeometry("gemma-small", [
+        GroupGeometry("full", LayerKind.kFullAttention, 2, 8, 16, 256, torch.bfloat16, 16),
+        GroupGeometry("window", LayerKind.kSlidingWindow, 2, 8, 16, 256, torch.bfloat16, 16, window=4096)],
+        softcap=50.0)
+    lens = [8192, 4097, 4096, 8191]
+    eng, ids = make_engine(geom, lens)
+    check_tables(orc, eng)
+    for g in range(2):
+        fill_group_kv(eng, g, [1], seed=g)
+        run_decode_parity(orc, eng, g, 1, softcap=50.0)
+
+
+def test_cross_attention_image_tokens(orc):
+    """Llama-3.2-Vision style: self (text only) + cross (image ordinals only),
+    including a request with no image tokens (n=0 -> zero output)."""
+    geom = ModelGeometry("vl", [
+        GroupGeometry("self", LayerKind.kFullAttention, 2, 8, 32, 128, torch.bfloat16, 16),
+        GroupGeometry("cross", LayerKind.kCrossAttention, 2, 8, 32, 128, torch.bfloat16, 16)])
+    img = [lambda p: 5 < p <= 700, lambda p: False, lambda p: p <= 1601, lambda p: 10 < p <= 30]
+    eng, ids = make_engine(geom, [800, 50, 1700, 64], image_flags=img)
+    check_tables(orc, eng)
+    seq_cross = eng.tables[1].seq_lens[:4].cpu().tolist()
+    assert seq_cross == [695, 0, 1601, 20]
+    assert eng.tables[0].seq_lens[:4].cpu().tolist() == [105, 50, 99, 44]
+    for g in range(2):
+        fill_group_kv(eng, g, [0], seed=g)
+        run_decode_parity(orc, eng, g, 0)
+
+
+def test_mamba_state_gather_scatter_and_checkpoint_copy(orc):
+    geom = ModelGeometry("hyb", [
+        GroupGeometry("attn", LayerKind.kFullAttention, 2, 8, 32, 128, torch.bfloat16, 16),
+        GroupGeometry("ssm", LayerKind.kMamba, 4, state_bytes=(8192 * 3 + 8192 * 16) * 4 // 64)])
+    eng, ids = make_engine(geom, [10, 1, 33, 7, 64], poison=False)
+    check_tables(orc, eng)
+    g = 1
+    B = len(ids)
+    pg = eng.mamba_page_globals(g)
+    gen = torch.Generator(device=eng.device).manual_seed(9)
+    for layer in (0, 3):
+        view = eng.view(g, layer)
+        dense = torch.randint(0, 255, (B, view.exec_page_size), generator=gen, device=eng.device,
+                              dtype=torch.uint8)
+        before = arena_host(eng)
+        ops.mamba_state_scatter(eng.arena, view, pg, dense)
+        torch.cuda.synchronize()
+        want = before.copy()
+        orc.mamba_scatter(want, tuple(view), pg.cpu().numpy(), dense.cpu().numpy())
+        np.testing.assert_array_equal(arena_host(eng), want)
+        back = torch.zeros_like(dense)
+        ops.mamba_state_gather(eng.arena, view, pg, back)
+        torch.cuda.synchronize()
+        assert torch.equal(back, dense)
+        np.testing.assert_array_equal(back.cpu().numpy(), orc.mamba_gather(want, tuple(view), pg.cpu().numpy(), B))
+    # checkpoint snapshot: copy request 0's working page to a fresh page
+    small = eng.tables[g].small_page_bytes
+    res = eng.kv.allocate(g, 999)
+    dst = eng.addr.global_page_index(g, res.page)
+    src = pg[:1].clone()
+    dstt = torch.tensor([dst], dtype=torch.int64, device=eng.device)
+    before = arena_host(eng)
+    ops.page_copy(eng.arena, small, src, dstt)
+    torch.cuda.synchronize()
+    want = before.copy()
+    orc.page_copy(want, small, src.cpu().numpy(), [dst])
+    np.testing.assert_array_equal(arena_host(eng), want)
+
+
+def test_launch_counter_and_errors():
+    n0 = ops.kernel_launch_count()
+    geom = toy(16)
+    eng, ids = make_engine(geom, [5, 9])
+    assert ops.kernel_launch_count() > n0
+    from paper_2503_18292_b200 import ConfigError
+    q = torch.zeros((2, 16, 128), device="cuda")
+    with pytest.raises(ConfigError):  # layer view of a bf16 geometry against fp32 data
+        ops.paged_decode(eng.arena, eng.view(0, 0)._replace(exec_page_size=7), 0, q, torch.empty_like(q),
+                         eng.tables[0].block_table[:2], eng.tables[0].seq_lens[:2], 8, 16, 1.0)
+    with pytest.raises(ValueError):
+        ops.paged_decode(eng.arena, eng.view(0, 0), 0, q.cpu(), q.cpu(), eng.tables[0].block_table[:2],
+                         eng.tables[0].seq_lens[:2], 8, 16, 1.0)
