@@ -3,6 +3,7 @@
 // Large page i occupies bytes [i*LCM, (i+1)*LCM); small page g of a group is
 // at g*small_page_bytes (memory_layout.cpp:29-39), so the arena is addressed
 // purely by the AddressMap arithmetic — no per-layer tensors.
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -27,6 +28,23 @@ struct jenga_arena {
   uint64_t bytes = 0;
 };
 
+// Registry of live arenas: kernels that build TMA tensor maps over the whole
+// arena look their extent up by base pointer.
+namespace {
+std::mutex g_arena_mu;
+std::map<uintptr_t, uint64_t> g_arenas;
+}  // namespace
+
+namespace jenga_dev {
+bool arena_extent(const void* base, uint64_t* bytes) {
+  std::lock_guard<std::mutex> lock(g_arena_mu);
+  auto it = g_arenas.find(reinterpret_cast<uintptr_t>(base));
+  if (it == g_arenas.end()) return false;
+  *bytes = it->second;
+  return true;
+}
+}  // namespace jenga_dev
+
 JENGA_EXPORT int jenga_arena_create(int device, uint64_t num_large_pages, uint64_t large_page_bytes,
                                     jenga_arena** out) {
   using namespace jenga_dev;
@@ -50,6 +68,10 @@ JENGA_EXPORT int jenga_arena_create(int device, uint64_t num_large_pages, uint64
   a->device = device;
   a->base = p;
   a->bytes = bytes;
+  {
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    g_arenas[reinterpret_cast<uintptr_t>(p)] = bytes;
+  }
   *out = a;
   return JENGA_OK;
 }
@@ -58,6 +80,10 @@ JENGA_EXPORT void jenga_arena_destroy(jenga_arena* arena) {
   if (arena == nullptr) return;
   int prev = 0;
   cudaGetDevice(&prev);
+  {
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    g_arenas.erase(reinterpret_cast<uintptr_t>(arena->base));
+  }
   cudaSetDevice(arena->device);
   cudaFree(arena->base);
   cudaSetDevice(prev);

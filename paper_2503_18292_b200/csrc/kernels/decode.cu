@@ -26,39 +26,13 @@
 //                 (request, head) merge in-kernel: the last CTA to finish
 //                 (atomic ticket) combines the partials — no second launch.
 #include <algorithm>
+#include <mutex>
 
-#include "common.cuh"
+#include "decode_common.cuh"
 
 namespace {
 
-constexpr int kTile = 16;           // tokens per pipeline stage
-constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr float kLog2e = 1.4426950408889634f;
-
-struct DecodeParams {
-  const uint8_t* arena;
-  uint64_t start_offset;
-  uint64_t page_stride;
-  const void* q;
-  void* out;
-  const int32_t* table;
-  const int32_t* seq_lens;
-  int kind;
-  int64_t window;
-  int max_blocks;
-  int hq;
-  int hkv;
-  int tpp;
-  int tiles_per_split;
-  int max_splits;
-  float qscale;       // scale*log2e, or scale when soft-capping
-  float cap_log2;     // softcap*log2e (0: off)
-  float inv_cap;      // 1/softcap
-  float* part_acc;    // [B][Hkv][max_splits][G][D]
-  float* part_ml;     // [B][Hkv][max_splits][G][2]
-  int* counters;      // [B][Hkv]
-};
+using namespace jenga_decode;
 
 template <int NB>
 __device__ __forceinline__ void load_words(const uint8_t* p, uint32_t* w) {
@@ -133,18 +107,9 @@ __global__ void __launch_bounds__(kThreads) paged_decode_kernel(const DecodePara
   const int h = blockIdx.y;
   const int split = blockIdx.x;
 
-  const int n = p.seq_lens[b];
-  int lo = 0;
-  if (p.kind == JENGA_KIND_SLIDING_WINDOW && n > p.window) lo = static_cast<int>(n - p.window);
-  const int tile_lo = lo / kTile;
-  const int tile_hi = (n + kTile - 1) / kTile;
-  const int ntiles = n > 0 ? tile_hi - tile_lo : 0;
-  int nsplit = (ntiles + p.tiles_per_split - 1) / p.tiles_per_split;
-  nsplit = max(1, min(nsplit, p.max_splits));
-  if (split >= nsplit) return;
-  const int per = ntiles / nsplit, rem = ntiles % nsplit;
-  const int t_begin = tile_lo + split * per + min(split, rem);
-  const int t_count = per + (split < rem ? 1 : 0);
+  const Work wk = assign_work(p, b, split);
+  if (split >= wk.nsplit) return;
+  const int n = wk.n, lo = wk.lo, nsplit = wk.nsplit, t_begin = wk.t_begin, t_count = wk.t_count;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -309,7 +274,7 @@ __global__ void __launch_bounds__(kThreads) paged_decode_kernel(const DecodePara
   // -------------------------------------------------- merge the 4 warps
   // All consumers are past their last full-barrier wait and the producer's
   // copies for this CTA have all been consumed, so the ring can be reused.
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+  consumers_sync();
   float* s_acc = reinterpret_cast<float*>(smem);                  // [4][G][D]
   float* s_ml = s_acc + kConsumerWarps * G * D;                   // [4][G][2]
 #pragma unroll
@@ -321,65 +286,10 @@ __global__ void __launch_bounds__(kThreads) paged_decode_kernel(const DecodePara
       s_ml[(warp * G + g) * 2 + 1] = l[g];
     }
   }
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
-
-  const int tid = threadIdx.x;  // 0..127
-  const int64_t bh = static_cast<int64_t>(b) * p.hkv + h;
-  T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(b) * p.hq + h * G) * D;
-  for (int i = tid; i < G * D; i += kConsumerWarps * 32) {
-    const int g = i / D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, s_ml[(w * G + g) * 2]);
-    float a = 0.f, L = 0.f;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      const float mw = s_ml[(w * G + g) * 2];
-      const float wt = mw == -INFINITY ? 0.f : jenga_dev::fast_exp2(mw - M);
-      a += wt * s_acc[(w * G) * D + i];
-      L += wt * s_ml[(w * G + g) * 2 + 1];
-    }
-    if (nsplit == 1) {
-      outp[i] = jenga_dev::DT<T>::from_f(L > 0.f ? a / L : 0.f);
-    } else {
-      const int64_t slot = bh * p.max_splits + split;
-      p.part_acc[slot * G * D + i] = a;
-      if (i % D == 0) {
-        p.part_ml[(slot * G + g) * 2] = M;
-        p.part_ml[(slot * G + g) * 2 + 1] = L;
-      }
-    }
-  }
-  if (nsplit == 1) return;
-
-  // -------------------------------------------------- split merge (last CTA)
-  __threadfence();
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
-  if (tid == 0) {
-    const int ticket = atomicAdd(&p.counters[bh], 1);
-    *s_flag = (ticket == nsplit - 1) ? 1 : 0;
-  }
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
-  if (*s_flag == 0) return;
-  __threadfence();
-  const int64_t slot0 = bh * p.max_splits;
-  for (int i = tid; i < G * D; i += kConsumerWarps * 32) {
-    const int g = i / D;
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2]));
-    float a = 0.f, L = 0.f;
-    for (int s2 = 0; s2 < nsplit; ++s2) {
-      const float ms = __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2]);
-      const float wt = ms == -INFINITY ? 0.f : jenga_dev::fast_exp2(ms - M);
-      a += wt * __ldcg(&p.part_acc[(slot0 + s2) * G * D + i]);
-      L += wt * __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2 + 1]);
-    }
-    outp[i] = jenga_dev::DT<T>::from_f(L > 0.f ? a / L : 0.f);
-  }
-  if (tid == 0) p.counters[bh] = 0;  // re-arm for the next launch / graph replay
+  merge_epilogue<T, G, D>(p, s_acc, s_ml, s_flag, nsplit, split, b, h);
 }
 
-constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
+
 
 int splits_for(int max_blocks, int tpp) {
   const int64_t max_tokens = static_cast<int64_t>(max_blocks) * tpp;
@@ -395,17 +305,8 @@ int launch_typed(const DecodeParams& prm, int batch, cudaStream_t stream) {
   const int merge = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
   const int smem = std::max(ring, merge) + 2 * NS * 8 + 16;
   auto kern = paged_decode_kernel<T, D, G, NS>;
-  // Opt in to >48 KB dynamic shared memory once per device and instantiation.
   static std::atomic<uint64_t> configured{0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << (dev & 63);
-  if (!(configured.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess)
-      return jenga_dev::set_error(JENGA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    configured.fetch_or(bit);
-  }
+  if (int rc = configure_smem(kern, smem, configured)) return rc;
   dim3 grid(prm.max_splits, prm.hkv, batch);
   kern<<<grid, kThreads, smem, stream>>>(prm);
   return jenga_dev::check_launch("paged_decode_kernel");
@@ -507,6 +408,10 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
   prm.part_ml = prm.part_acc + bh * prm.max_splits * G * head_dim;
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((dtype == JENGA_BF16 || dtype == JENGA_F16) && tpp % kTile == 0) {
+    const int rc = launch_decode_tc(prm, dtype, head_dim, static_cast<int>(G), batch, s);
+    if (rc != JENGA_ERR_UNSUPPORTED) return rc;
+  }
   switch (dtype) {
     case JENGA_F32: return dispatch_d<float>(head_dim, static_cast<int>(G), prm, batch, s);
     case JENGA_BF16: return dispatch_d<__nv_bfloat16>(head_dim, static_cast<int>(G), prm, batch, s);

@@ -1,0 +1,150 @@
+// Pieces shared by the two paged-decode kernels (decode.cu: CUDA-core math
+// for fp32 / odd page sizes; decode_tc.cu: tensor-core math for bf16/fp16):
+// launch parameters, the split-KV work assignment and the epilogue that
+// merges the four consumer warps and then the splits of one (request, head).
+#pragma once
+
+#include "common.cuh"
+
+namespace jenga_decode {
+
+constexpr int kTile = 16;  // tokens per pipeline stage
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
+
+struct DecodeParams {
+  const uint8_t* arena;
+  uint64_t start_offset;
+  uint64_t page_stride;
+  const void* q;
+  void* out;
+  const int32_t* table;
+  const int32_t* seq_lens;
+  int kind;
+  int64_t window;
+  int max_blocks;
+  int hq;
+  int hkv;
+  int tpp;
+  int tiles_per_split;
+  int max_splits;
+  float qscale;    // scale*log2e, or scale when soft-capping
+  float cap_log2;  // softcap*log2e (0: off)
+  float inv_cap;   // 1/softcap
+  float* part_acc; // [B][Hkv][max_splits][G][D]
+  float* part_ml;  // [B][Hkv][max_splits][G][2]
+  int* counters;   // [B][Hkv]
+};
+
+// Live ordinals of request b (LayerPolicy::needs_token, layer_policies.cpp:
+// 105-120) cut into splits of whole 16-token tiles.
+struct Work {
+  int n, lo, nsplit, t_begin, t_count;
+};
+
+__device__ __forceinline__ Work assign_work(const DecodeParams& p, int b, int split) {
+  Work w;
+  w.n = p.seq_lens[b];
+  w.lo = 0;
+  if (p.kind == JENGA_KIND_SLIDING_WINDOW && w.n > p.window) w.lo = static_cast<int>(w.n - p.window);
+  const int tile_lo = w.lo / kTile;
+  const int tile_hi = (w.n + kTile - 1) / kTile;
+  const int ntiles = w.n > 0 ? tile_hi - tile_lo : 0;
+  int ns = (ntiles + p.tiles_per_split - 1) / p.tiles_per_split;
+  w.nsplit = max(1, min(ns, p.max_splits));
+  const int per = ntiles / w.nsplit, rem = ntiles % w.nsplit;
+  w.t_begin = tile_lo + split * per + min(split, rem);
+  w.t_count = per + (split < rem ? 1 : 0);
+  return w;
+}
+
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+}
+
+// Called by the 128 consumer threads after each warp w wrote its unnormalised
+// state to s_acc[w][G][D] / s_ml[w][G][{m, l}] (m in log2 units, -inf = no
+// live token).  Writes out[b][h*G+g][:] directly when the request has one
+// split; otherwise stores the CTA partial and the last CTA of (b, h) to
+// finish (atomic ticket) combines all splits and re-arms the ticket.
+template <typename T, int G, int D>
+__device__ __forceinline__ void merge_epilogue(const DecodeParams& p, const float* s_acc, const float* s_ml,
+                                               int* s_flag, int nsplit, int split, int b, int h) {
+  consumers_sync();
+  const int tid = threadIdx.x;
+  const int64_t bh = static_cast<int64_t>(b) * p.hkv + h;
+  T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(b) * p.hq + h * G) * D;
+  for (int i = tid; i < G * D; i += kConsumerWarps * 32) {
+    const int g = i / D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, s_ml[(w * G + g) * 2]);
+    float a = 0.f, L = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      const float mw = s_ml[(w * G + g) * 2];
+      const float wt = mw == -INFINITY ? 0.f : jenga_dev::fast_exp2(mw - M);
+      a += wt * s_acc[(w * G) * D + i];
+      L += wt * s_ml[(w * G + g) * 2 + 1];
+    }
+    if (nsplit == 1) {
+      outp[i] = jenga_dev::DT<T>::from_f(L > 0.f ? a / L : 0.f);
+    } else {
+      const int64_t slot = bh * p.max_splits + split;
+      p.part_acc[slot * G * D + i] = a;
+      if (i % D == 0) {
+        p.part_ml[(slot * G + g) * 2] = M;
+        p.part_ml[(slot * G + g) * 2 + 1] = L;
+      }
+    }
+  }
+  if (nsplit == 1) return;
+
+  __threadfence();
+  consumers_sync();
+  if (tid == 0) {
+    const int ticket = atomicAdd(&p.counters[bh], 1);
+    *s_flag = (ticket == nsplit - 1) ? 1 : 0;
+  }
+  consumers_sync();
+  if (*s_flag == 0) return;
+  __threadfence();
+  const int64_t slot0 = bh * p.max_splits;
+  for (int i = tid; i < G * D; i += kConsumerWarps * 32) {
+    const int g = i / D;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2]));
+    float a = 0.f, L = 0.f;
+    for (int s2 = 0; s2 < nsplit; ++s2) {
+      const float ms = __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2]);
+      const float wt = ms == -INFINITY ? 0.f : jenga_dev::fast_exp2(ms - M);
+      a += wt * __ldcg(&p.part_acc[(slot0 + s2) * G * D + i]);
+      L += wt * __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2 + 1]);
+    }
+    outp[i] = jenga_dev::DT<T>::from_f(L > 0.f ? a / L : 0.f);
+  }
+  if (tid == 0) p.counters[bh] = 0;  // re-arm for the next launch / graph replay
+}
+
+// Opt a kernel in to >48 KB dynamic shared memory once per device.
+template <typename K>
+int configure_smem(K kern, int smem, std::atomic<uint64_t>& configured) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess)
+      return jenga_dev::set_error(JENGA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    configured.fetch_or(bit);
+  }
+  return JENGA_OK;
+}
+
+// Tensor-core path (decode_tc.cu); returns JENGA_ERR_UNSUPPORTED when the
+// shape is not covered so the caller can use the CUDA-core kernel.
+int launch_decode_tc(const DecodeParams& prm, int dtype, int head_dim, int G, int batch, cudaStream_t stream);
+
+}  // namespace jenga_decode

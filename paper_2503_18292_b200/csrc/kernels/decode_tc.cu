@@ -1,0 +1,394 @@
+// Paged decode attention, tensor-core variant (bf16 / fp16 KV, page sizes that
+// are multiples of 16 tokens).  Same contract, work split and epilogue as the
+// CUDA-core kernel in decode.cu; the differences are the data movement and
+// the math:
+//
+//  * K/V tiles move with 2-D TMA tensor loads (cp.async.bulk.tensor -> UTMALDG)
+//    over the whole arena viewed as a [rows][D] matrix, rows = one token of
+//    one (page, layer, K|V, head): row index = (start_offset + global*
+//    page_stride + (h*tpp + off)*D*e) / (D*e).  Boxes of 64 x 16 land in
+//    shared memory with the 128-byte swizzle, so ldmatrix is conflict-free.
+//  * S^T = K . Q^T and O^T += V^T . P^T run on the tensor cores with
+//    mma.sync m16n8k16 (fp32 accumulate): tokens on M (16 per tile), the G
+//    query heads of one KV head on N (padded to 8), head_dim as K for QK and
+//    as M for PV.  P is re-laid from the S accumulator into the PV operand
+//    with movmatrix (8x8 transpose), never touching shared memory.
+//  * online softmax in fp32 registers: per-head tile max via 3 shuffles,
+//    lazy rescale of the O accumulators only when a max moved.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "decode_common.cuh"
+
+namespace jenga_dev {
+bool arena_extent(const void* base, uint64_t* bytes);
+}
+
+namespace {
+
+using namespace jenga_decode;
+
+constexpr int kBoxCols = 64;                // elements per swizzle row (128 B)
+constexpr int kBoxBytes = kTile * 128;      // one 64 x 16 box
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t movm_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+
+template <typename T>
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  } else {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+}
+
+template <typename T, int D, int G, int NS>
+__global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const DecodeParams p,
+                                                                   const __grid_constant__ CUtensorMap tmap) {
+  static_assert(D % kBoxCols == 0, "head_dim must be a multiple of 64");
+  static_assert(G <= 8, "at most 8 query heads per KV head (N = 8)");
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int TILE_BYTES = NBOX * kBoxBytes;  // 16 tokens x D x 2 B
+  constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+  constexpr int KSTEPS = D / 16;
+  constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
+  constexpr int RING = NS * STAGE_BYTES;
+  constexpr int BAR_OFFSET = RING > MERGE_BYTES ? RING : MERGE_BYTES;
+  static_assert(NS % kConsumerWarps == 0, "stage ring must be a multiple of the consumer count");
+
+  extern __shared__ uint8_t smem_raw[];
+  // 128-byte swizzled TMA destinations want 1024-byte aligned boxes.
+  uint8_t* smem = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFFSET);
+  uint64_t* empty = full + NS;
+  int* s_flag = reinterpret_cast<int*>(empty + NS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.z;
+  const int h = blockIdx.y;
+  const int split = blockIdx.x;
+  const Work wk = assign_work(p, b, split);
+  if (split >= wk.nsplit) return;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      jenga_dev::mbar_init(&full[i], 1);
+      jenga_dev::mbar_init(&empty[i], 1);
+    }
+    jenga_dev::fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------ producer (one lane)
+    if (lane == 0) {
+      jenga_dev::prefetch_tmap(&tmap);
+      const uint64_t policy = jenga_dev::l2_policy_evict_first();
+      const int64_t row_bytes = D * 2;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * p.tpp;
+      const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+      const int v_rows = p.hkv * p.tpp;
+      for (int it = 0; it < wk.t_count; ++it) {
+        const int st = it % NS;
+        if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
+        uint8_t* ks = smem + st * STAGE_BYTES;
+        uint8_t* vs = ks + TILE_BYTES;
+        const int tok0 = (wk.t_begin + it) * kTile;
+        const int32_t page = table[tok0 / p.tpp];
+        const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(page) * page_rows + tok0 % p.tpp);
+        jenga_dev::mbar_arrive_expect_tx(&full[st], STAGE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx) {
+          jenga_dev::tma_load_2d(ks + bx * kBoxBytes, &tmap, bx * kBoxCols, row, &full[st], policy);
+          jenga_dev::tma_load_2d(vs + bx * kBoxBytes, &tmap, bx * kBoxCols, row + v_rows, &full[st], policy);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumers
+  const int r4 = lane >> 2;  // fragment row group
+  const int c4 = lane & 3;   // fragment column pair
+  // Q^T as the B operand of S^T = K Q^T: b0 = Q[n][16k + 2c .. +1], b1 = +8
+  uint32_t bq[KSTEPS][2];
+  {
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(p.q) +
+                                                             (static_cast<int64_t>(b) * p.hq + h * G + r4) * D);
+#pragma unroll
+    for (int k = 0; k < KSTEPS; ++k) {
+      bq[k][0] = r4 < G ? __ldg(qrow + (16 * k + 2 * c4) / 2) : 0u;
+      bq[k][1] = r4 < G ? __ldg(qrow + (16 * k + 8 + 2 * c4) / 2) : 0u;
+    }
+  }
+  float o[KSTEPS][4];
+#pragma unroll
+  for (int k = 0; k < KSTEPS; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2*c4, 2*c4+1
+
+  // per-thread ldmatrix geometry
+  const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8;  // K tile row fed by this lane
+  const int k_half = lane >> 4;                           // which 8-wide D half
+  const int v_tok = (lane & 7) + (lane >> 4) * 8;         // V tile token row fed by this lane
+  const int v_half = (lane >> 3) & 1;
+  const int x7 = lane & 7;                                // == row & 7 for both
+
+  for (int it = warp; it < wk.t_count; it += kConsumerWarps) {
+    const int st = it % NS;
+    jenga_dev::mbar_wait(&full[st], (it / NS) & 1);
+    uint8_t* ks = smem + st * STAGE_BYTES;
+    uint8_t* vs = ks + TILE_BYTES;
+    const uint32_t ks_u = jenga_dev::smem_u32(ks), vs_u = jenga_dev::smem_u32(vs);
+    const int tok0 = (wk.t_begin + it) * kTile;
+
+    // ---- S^T = K . Q^T  (16 tokens x 8 heads, fp32)
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < KSTEPS; ++k) {
+      const int chunk = 2 * k + k_half;
+      const uint32_t addr = ks_u + (chunk >> 3) * kBoxBytes + k_row * 128 + (((chunk & 7) ^ x7) << 4);
+      uint32_t a[4];
+      ldsm_x4(a, addr);
+      mma16816<T>(s, a, bq[k][0], bq[k][1]);
+    }
+    // ---- scale, soft-cap, mask (needs_token), online softmax
+    const int ta = tok0 + r4, tb = ta + 8;
+    const bool va = ta >= wk.lo && ta < wk.n, vb = tb >= wk.lo && tb < wk.n;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float x = s[i] * p.qscale;
+      if (p.cap_log2 > 0.f) x = p.cap_log2 * tanhf(x * p.inv_cap);
+      s[i] = x;
+    }
+    s[0] = va ? s[0] : -INFINITY;
+    s[1] = va ? s[1] : -INFINITY;
+    s[2] = vb ? s[2] : -INFINITY;
+    s[3] = vb ? s[3] : -INFINITY;
+    float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, off));
+      t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, off));
+    }
+    const float n0 = fmaxf(m0, t0), n1 = fmaxf(m1, t1);
+    const float a0 = n0 == -INFINITY ? 1.f : jenga_dev::fast_exp2(m0 - n0);
+    const float a1 = n1 == -INFINITY ? 1.f : jenga_dev::fast_exp2(m1 - n1);
+    m0 = n0;
+    m1 = n1;
+    const float p0 = va ? jenga_dev::fast_exp2(s[0] - n0) : 0.f;
+    const float p1 = va ? jenga_dev::fast_exp2(s[1] - n1) : 0.f;
+    const float p2 = vb ? jenga_dev::fast_exp2(s[2] - n0) : 0.f;
+    const float p3 = vb ? jenga_dev::fast_exp2(s[3] - n1) : 0.f;
+    l0 = l0 * a0 + p0 + p2;
+    l1 = l1 * a1 + p1 + p3;
+    if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+#pragma unroll
+      for (int k = 0; k < KSTEPS; ++k) {
+        o[k][0] *= a0;
+        o[k][1] *= a1;
+        o[k][2] *= a0;
+        o[k][3] *= a1;
+      }
+    }
+    // P^T as the B operand of O^T += V^T P^T (k = tokens, n = heads)
+    const uint32_t pb0 = movm_trans(pack2<T>(p0, p1));
+    const uint32_t pb1 = movm_trans(pack2<T>(p2, p3));
+    // masked rows of a boundary tile may hold stale / non-finite bytes:
+    // zero them so 0 * V cannot produce NaN inside the MMA.
+    if (tok0 < wk.lo || tok0 + kTile > wk.n) {
+      for (int r = 0; r < kTile; ++r) {
+        const int t = tok0 + r;
+        if (t >= wk.lo && t < wk.n) continue;
+        for (int c = lane; c < NBOX * 8; c += 32)
+          *reinterpret_cast<uint4*>(vs + (c >> 3) * kBoxBytes + r * 128 + ((c & 7) << 4)) = make_uint4(0, 0, 0, 0);
+      }
+      // order these generic-proxy writes before the TMA refill of this stage
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+    }
+    // ---- O^T += V^T . P^T  (D x 8 heads)
+#pragma unroll
+    for (int k = 0; k < KSTEPS; ++k) {
+      const int chunk = 2 * k + v_half;
+      const uint32_t addr = vs_u + (chunk >> 3) * kBoxBytes + v_tok * 128 + (((chunk & 7) ^ x7) << 4);
+      uint32_t a[4];
+      ldsm_x4_trans(a, addr);
+      mma16816<T>(o[k], a, pb0, pb1);
+    }
+    __syncwarp();
+    if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
+  }
+
+  // -------------------------------------------------- per-warp state -> smem
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  consumers_sync();
+  float* s_acc = reinterpret_cast<float*>(smem);  // [4][G][D]
+  float* s_ml = s_acc + kConsumerWarps * G * D;   // [4][G][2]
+  const int h0 = 2 * c4, h1 = h0 + 1;
+#pragma unroll
+  for (int k = 0; k < KSTEPS; ++k) {
+    const int d = 16 * k + r4;
+    if (h0 < G) {
+      s_acc[(warp * G + h0) * D + d] = o[k][0];
+      s_acc[(warp * G + h0) * D + d + 8] = o[k][2];
+    }
+    if (h1 < G) {
+      s_acc[(warp * G + h1) * D + d] = o[k][1];
+      s_acc[(warp * G + h1) * D + d + 8] = o[k][3];
+    }
+  }
+  if (r4 == 0) {
+    if (h0 < G) {
+      s_ml[(warp * G + h0) * 2] = m0;
+      s_ml[(warp * G + h0) * 2 + 1] = l0;
+    }
+    if (h1 < G) {
+      s_ml[(warp * G + h1) * 2] = m1;
+      s_ml[(warp * G + h1) * 2 + 1] = l1;
+    }
+  }
+  merge_epilogue<T, G, D>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h);
+}
+
+// ------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// One [rows][D] view of the arena per (arena, D, dtype); encoded once.
+int tensor_map(const void* base, int D, int dtype, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<uintptr_t, int, int>, CUtensorMap> cache;
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), D, dtype);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return JENGA_OK;
+  }
+  uint64_t bytes = 0;
+  if (!jenga_dev::arena_extent(base, &bytes)) return JENGA_ERR_UNSUPPORTED;  // not a jenga arena
+  auto fn = encode_fn();
+  if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t row_bytes = static_cast<uint64_t>(D) * 2;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / row_bytes};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile)};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  cache[key] = m;
+  *out = m;
+  return JENGA_OK;
+}
+
+template <typename T, int D, int G>
+int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaStream_t stream) {
+  constexpr int NS = 4;
+  constexpr int STAGE = 2 * kTile * D * 2;
+  constexpr int MERGE = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
+  const int smem = std::max(NS * STAGE, MERGE) + 2 * NS * 8 + 16 + 1024;
+  auto kern = paged_decode_tc_kernel<T, D, G, NS>;
+  static std::atomic<uint64_t> configured{0};
+  if (int rc = configure_smem(kern, smem, configured)) return rc;
+  dim3 grid(prm.max_splits, prm.hkv, batch);
+  kern<<<grid, kThreads, smem, stream>>>(prm, tmap);
+  return jenga_dev::check_launch("paged_decode_tc_kernel");
+}
+
+template <typename T, int D>
+int dispatch_g(int G, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_tc<T, D, 1>(prm, m, batch, s);
+    case 2: return launch_tc<T, D, 2>(prm, m, batch, s);
+    case 4: return launch_tc<T, D, 4>(prm, m, batch, s);
+    case 8: return launch_tc<T, D, 8>(prm, m, batch, s);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+template <typename T>
+int dispatch_d(int D, int G, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+  switch (D) {
+    case 64: return dispatch_g<T, 64>(G, prm, m, batch, s);
+    case 128: return dispatch_g<T, 128>(G, prm, m, batch, s);
+    case 256: return dispatch_g<T, 256>(G, prm, m, batch, s);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+namespace jenga_decode {
+
+int launch_decode_tc(const DecodeParams& prm, int dtype, int head_dim, int G, int batch, cudaStream_t stream) {
+  if (prm.tpp % kTile != 0 || head_dim % kBoxCols != 0 || G > 8) return JENGA_ERR_UNSUPPORTED;
+  if (prm.start_offset % (head_dim * 2) || prm.page_stride % (head_dim * 2)) return JENGA_ERR_UNSUPPORTED;
+  CUtensorMap m;
+  const int rc = tensor_map(prm.arena, head_dim, dtype, &m);
+  if (rc != JENGA_OK) return rc;
+  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, m, batch, stream);
+  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, prm, m, batch, stream);
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+}  // namespace jenga_decode

@@ -1,0 +1,97 @@
+"""Summarise ncu outputs brought back in gpurun_out/ into profiles/.
+
+    python profiles/summarize_ncu.py <tag> [gpurun_out]
+
+Writes profiles/<tag>_launches.md (per-kernel launch count, device time and
+share of the step from the `--metrics gpu__time_duration.sum` launch list),
+profiles/<tag>_ncu_full.md (key --set full metrics per captured launch) and
+profiles/decode_traffic.json (DRAM bytes per decode launch, read by bench.py
+as roofline.traffic).
+"""
+import csv
+import json
+import re
+import subprocess
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__occupancy_limit_shared_mem", "launch__waves_per_multiprocessor",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed_pipe_uniform.sum", "sm__cycles_elapsed.avg.per_second"]
+
+
+def short(name):
+    m = re.search(r"(\w+_kernel)(<[^>]*>)?", name)
+    return (m.group(1) + (m.group(2) or "")) if m else name[:80]
+
+
+def launches(tag, src):
+    path = src / "launches.csv"
+    if not path.exists():
+        return
+    rows = [r for r in csv.DictReader(l for l in open(path) if l.startswith('"'))]
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        k = short(r["Kernel Name"])
+        agg[k][0] += 1
+        v = float(r["Metric Value"].replace(",", ""))
+        agg[k][1] += v / 1e3 if r["Metric Unit"] == "ns" else (v if r["Metric Unit"] == "us" else v * 1e3)
+    total = sum(v[1] for v in agg.values())
+    lines = [f"# {tag}: launch list (ncu --metrics gpu__time_duration.sum --clock-control none)", "",
+             "Cold-cache, serialised launches: compare shares, not absolute step time.", "",
+             "| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+    for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"| `{k}` | {n} | {t:.1f} | {t / n:.1f} | {t / total:.1%} |")
+    (ROOT / "profiles" / f"{tag}_launches.md").write_text("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def full(tag, src):
+    reps = sorted(src.glob("prof_*.ncu-rep"))
+    out = ["# %s: ncu --set full captures" % tag, ""]
+    traffic = None
+    for rep in reps:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(txt.splitlines()))
+        if len(rows) < 3:
+            continue
+        hdr, units = rows[0], rows[1]
+        out.append(f"## {rep.name}")
+        for r in rows[2:]:
+            name = short(r[hdr.index("Kernel Name")])
+            grid = r[hdr.index("Grid Size")]
+            out.append(f"### `{name}` grid {grid}")
+            for k in KEYS:
+                if k in hdr:
+                    out.append(f"- {k} = {r[hdr.index(k)]} {units[hdr.index(k)]}")
+            if "paged_decode" in name and "dram__bytes_read.sum" in hdr:
+                def to_bytes(v, u):
+                    v = float(v.replace(",", ""))
+                    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                rd = to_bytes(r[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_read.sum")])
+                wr = to_bytes(r[hdr.index("dram__bytes_write.sum")], units[hdr.index("dram__bytes_write.sum")])
+                traffic = traffic or []
+                traffic.append({"kernel": name, "grid": grid, "bytes": rd + wr})
+            out.append("")
+    (ROOT / "profiles" / f"{tag}_ncu_full.md").write_text("\n".join(out) + "\n")
+    print("\n".join(out))
+    if traffic:
+        # bench.py sums one full + one SWA layer per pair; report mean per launch
+        per = sum(t["bytes"] for t in traffic) / len(traffic)
+        (ROOT / "profiles" / "decode_traffic.json").write_text(json.dumps(
+            {"source": f"{tag}: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
+             "launches": traffic, "traffic_bytes_per_launch": per}, indent=1))
+
+
+if __name__ == "__main__":
+    tag = sys.argv[1]
+    src = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "gpurun_out"
+    launches(tag, src)
+    full(tag, src)
