@@ -278,7 +278,7 @@ def run_ours(a, rank, world, local_rank):
                          % (eng.arena.nbytes / 1e9)},
         "tokens_per_s": round(B * world * a.steps / (ms * 1e-3), 1),
         "frac_of_hbm_peak": round(value / world / pk["hbm_gbs"], 4),
-        "roofline": {"bound": "hbm", "kernel": "paged_decode_kernel", "achieved": round(dec_gbs, 1),
+        "roofline": {"bound": "hbm", "kernel": "paged_decode_tc_kernel<bf16, D=256, G=2> (TMA + mma.sync)", "achieved": round(dec_gbs, 1),
                      "peak": pk["hbm_gbs"], "peak_source": src, "unit": "GB/s",
                      "frac": round(dec_gbs / pk["hbm_gbs"], 4), "traffic": traffic,
                      "decode_share_of_step": round(dec_ms / (ms_per_step * a.steps), 4),
