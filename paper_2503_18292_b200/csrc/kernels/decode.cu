@@ -103,9 +103,10 @@ __global__ void __launch_bounds__(kThreads) paged_decode_kernel(const DecodePara
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int b = blockIdx.z;
-  const int h = blockIdx.y;
-  const int split = blockIdx.x;
+  // Grid order (head, request, split): see decode_tc.cu.
+  const int b = grid_request(p);
+  const int h = blockIdx.x;
+  const int split = grid_split(p);
 
   const Work wk = assign_work(p, b, split);
   if (split >= wk.nsplit) return;
@@ -291,10 +292,40 @@ __global__ void __launch_bounds__(kThreads) paged_decode_kernel(const DecodePara
 
 
 
-int splits_for(int max_blocks, int tpp) {
+// The workspace is sized for the finest split the launcher may pick.
+constexpr int kMinTilesPerSplit = 8;
+
+int splits_for(int max_blocks, int tpp, int tiles_per_split) {
   const int64_t max_tokens = static_cast<int64_t>(max_blocks) * tpp;
   const int64_t max_tiles = (max_tokens + kTile - 1) / kTile + 1;
-  return static_cast<int>((max_tiles + kTilesPerSplit - 1) / kTilesPerSplit);
+  return static_cast<int>((max_tiles + tiles_per_split - 1) / tiles_per_split);
+}
+
+// Tiles per CTA; JENGA_DECODE_TILES_PER_SPLIT overrides for tuning sweeps.
+int tiles_per_split() {
+  static const int v = [] {
+    const char* e = std::getenv("JENGA_DECODE_TILES_PER_SPLIT");
+    const int x = e ? std::atoi(e) : 0;
+    return x >= kMinTilesPerSplit ? x : kTilesPerSplit;
+  }();
+  return v;
+}
+
+int grid_order() {
+  static const int v = [] {
+    const char* e = std::getenv("JENGA_DECODE_GRID_ORDER");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+// L2 prefetch distance (tiles); JENGA_DECODE_PREFETCH overrides.
+int prefetch_tiles() {
+  static const int v = [] {
+    const char* e = std::getenv("JENGA_DECODE_PREFETCH");
+    return e ? std::max(0, std::atoi(e)) : kDefaultPrefetchTiles;
+  }();
+  return v;
 }
 
 template <typename T, int D, int G>
@@ -307,7 +338,7 @@ int launch_typed(const DecodeParams& prm, int batch, cudaStream_t stream) {
   auto kern = paged_decode_kernel<T, D, G, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  dim3 grid(prm.max_splits, prm.hkv, batch);
+  const dim3 grid = decode_grid(prm, batch);
   kern<<<grid, kThreads, smem, stream>>>(prm);
   return jenga_dev::check_launch("paged_decode_kernel");
 }
@@ -338,7 +369,7 @@ int dispatch_d(int D, int G, const DecodeParams& prm, int batch, cudaStream_t s)
 JENGA_EXPORT size_t jenga_paged_decode_workspace_size(int batch, int num_q_heads, int num_kv_heads, int head_dim,
                                                       int max_blocks, uint32_t tokens_per_page) {
   if (batch <= 0 || num_kv_heads <= 0 || num_q_heads <= 0 || tokens_per_page == 0) return 0;
-  const int64_t ms = splits_for(max_blocks, static_cast<int>(tokens_per_page));
+  const int64_t ms = splits_for(max_blocks, static_cast<int>(tokens_per_page), kMinTilesPerSplit);
   const int64_t bh = static_cast<int64_t>(batch) * num_kv_heads;
   const int64_t G = num_q_heads / num_kv_heads;
   const int64_t counters = ((bh * 4 + 255) / 256) * 256;
@@ -388,8 +419,14 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
   prm.hq = num_q_heads;
   prm.hkv = num_kv_heads;
   prm.tpp = tpp;
-  prm.tiles_per_split = kTilesPerSplit;
-  prm.max_splits = splits_for(max_blocks, tpp);
+  prm.tiles_per_split = tiles_per_split();
+  prm.prefetch_tiles = prefetch_tiles();
+  prm.prefetch_mode = [] {
+    const char* e = std::getenv("JENGA_DECODE_PREFETCH_MODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  prm.grid_order = grid_order();
+  prm.max_splits = splits_for(max_blocks, tpp, tiles_per_split());
   if (softcap > 0.f) {
     prm.qscale = scale;
     prm.cap_log2 = softcap * kLog2e;

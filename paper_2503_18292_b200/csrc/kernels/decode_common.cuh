@@ -13,6 +13,7 @@ constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
+constexpr int kDefaultPrefetchTiles = 0;
 
 struct DecodeParams {
   const uint8_t* arena;
@@ -30,6 +31,9 @@ struct DecodeParams {
   int tpp;
   int tiles_per_split;
   int max_splits;
+  int prefetch_tiles;  // L2 prefetch distance in tiles (0: off)
+  int prefetch_mode;   // 0: one line (translation warm-up), 1: whole tile
+  int grid_order;      // 0: (head, request, split); 1: (head, split, request)
   float qscale;    // scale*log2e, or scale when soft-capping
   float cap_log2;  // softcap*log2e (0: off)
   float inv_cap;   // 1/softcap
@@ -37,6 +41,19 @@ struct DecodeParams {
   float* part_ml;  // [B][Hkv][max_splits][G][2]
   int* counters;   // [B][Hkv]
 };
+
+// Grid = (Hkv, batch, max_splits) when grid_order == 0 (default);
+// (Hkv, max_splits, batch) when 1 (JENGA_DECODE_GRID_ORDER, A/B runs).
+__device__ __forceinline__ int grid_request(const DecodeParams& p) {
+  return p.grid_order == 0 ? blockIdx.y : blockIdx.z;
+}
+__device__ __forceinline__ int grid_split(const DecodeParams& p) {
+  return p.grid_order == 0 ? blockIdx.z : blockIdx.y;
+}
+inline dim3 decode_grid(const DecodeParams& p, int batch, int heads_per_cta = 1) {
+  const int hx = p.hkv / heads_per_cta;
+  return p.grid_order == 0 ? dim3(hx, batch, p.max_splits) : dim3(hx, p.max_splits, batch);
+}
 
 // Live ordinals of request b (LayerPolicy::needs_token, layer_policies.cpp:
 // 105-120) cut into splits of whole 16-token tiles.
@@ -69,32 +86,40 @@ __device__ __forceinline__ void consumers_sync() {
 // live token).  Writes out[b][h*G+g][:] directly when the request has one
 // split; otherwise stores the CTA partial and the last CTA of (b, h) to
 // finish (atomic ticket) combines all splits and re-arms the ticket.
-template <typename T, int G, int D>
+//
+// HG KV heads per CTA: warp w holds local head w % HG of round w / HG, so
+// head hl merges warps {hl, hl + HG, ...}.  The CTA covers heads
+// [h0, h0 + HG); one ticket per (request, head group).
+template <typename T, int G, int D, int HG = 1>
 __device__ __forceinline__ void merge_epilogue(const DecodeParams& p, const float* s_acc, const float* s_ml,
-                                               int* s_flag, int nsplit, int split, int b, int h) {
+                                               int* s_flag, int nsplit, int split, int b, int h0) {
+  constexpr int R = kConsumerWarps / HG;  // warps per head
   consumers_sync();
   const int tid = threadIdx.x;
-  const int64_t bh = static_cast<int64_t>(b) * p.hkv + h;
-  T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(b) * p.hq + h * G) * D;
-  for (int i = tid; i < G * D; i += kConsumerWarps * 32) {
-    const int g = i / D;
+  const int64_t b_h0 = static_cast<int64_t>(b) * p.hkv + h0;
+  T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(b) * p.hq + h0 * G) * D;
+  for (int i = tid; i < HG * G * D; i += kConsumerWarps * 32) {
+    const int hl = i / (G * D);
+    const int j = i - hl * G * D;
+    const int g = j / D;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, s_ml[(w * G + g) * 2]);
+    for (int r = 0; r < R; ++r) M = fmaxf(M, s_ml[((r * HG + hl) * G + g) * 2]);
     float a = 0.f, L = 0.f;
 #pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
+    for (int r = 0; r < R; ++r) {
+      const int w = r * HG + hl;
       const float mw = s_ml[(w * G + g) * 2];
       const float wt = mw == -INFINITY ? 0.f : jenga_dev::fast_exp2(mw - M);
-      a += wt * s_acc[(w * G) * D + i];
+      a += wt * s_acc[(w * G) * D + j];
       L += wt * s_ml[(w * G + g) * 2 + 1];
     }
     if (nsplit == 1) {
       outp[i] = jenga_dev::DT<T>::from_f(L > 0.f ? a / L : 0.f);
     } else {
-      const int64_t slot = bh * p.max_splits + split;
-      p.part_acc[slot * G * D + i] = a;
-      if (i % D == 0) {
+      const int64_t slot = (b_h0 + hl) * p.max_splits + split;
+      p.part_acc[slot * G * D + j] = a;
+      if (j % D == 0) {
         p.part_ml[(slot * G + g) * 2] = M;
         p.part_ml[(slot * G + g) * 2 + 1] = L;
       }
@@ -105,27 +130,29 @@ __device__ __forceinline__ void merge_epilogue(const DecodeParams& p, const floa
   __threadfence();
   consumers_sync();
   if (tid == 0) {
-    const int ticket = atomicAdd(&p.counters[bh], 1);
+    const int ticket = atomicAdd(&p.counters[b_h0], 1);
     *s_flag = (ticket == nsplit - 1) ? 1 : 0;
   }
   consumers_sync();
   if (*s_flag == 0) return;
   __threadfence();
-  const int64_t slot0 = bh * p.max_splits;
-  for (int i = tid; i < G * D; i += kConsumerWarps * 32) {
-    const int g = i / D;
+  for (int i = tid; i < HG * G * D; i += kConsumerWarps * 32) {
+    const int hl = i / (G * D);
+    const int j = i - hl * G * D;
+    const int g = j / D;
+    const int64_t slot0 = (b_h0 + hl) * p.max_splits;
     float M = -INFINITY;
     for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2]));
     float a = 0.f, L = 0.f;
     for (int s2 = 0; s2 < nsplit; ++s2) {
       const float ms = __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2]);
       const float wt = ms == -INFINITY ? 0.f : jenga_dev::fast_exp2(ms - M);
-      a += wt * __ldcg(&p.part_acc[(slot0 + s2) * G * D + i]);
+      a += wt * __ldcg(&p.part_acc[(slot0 + s2) * G * D + j]);
       L += wt * __ldcg(&p.part_ml[((slot0 + s2) * G + g) * 2 + 1]);
     }
     outp[i] = jenga_dev::DT<T>::from_f(L > 0.f ? a / L : 0.f);
   }
-  if (tid == 0) p.counters[bh] = 0;  // re-arm for the next launch / graph replay
+  if (tid == 0) p.counters[b_h0] = 0;  // re-arm for the next launch / graph replay
 }
 
 // Opt a kernel in to >48 KB dynamic shared memory once per device.

@@ -8,6 +8,13 @@
 //    one (page, layer, K|V, head): row index = (start_offset + global*
 //    page_stride + (h*tpp + off)*D*e) / (D*e).  Boxes of 64 x 16 land in
 //    shared memory with the 128-byte swizzle, so ldmatrix is conflict-free.
+//  * One CTA serves HG KV heads of a request: a pipeline stage holds the same
+//    16-token tile of all HG heads, which are adjacent in the page-layer slice
+//    ([K|V][Hkv][tpp][D]), so each stage is one contiguous HG x 8 KiB run of K
+//    and one of V.  Long contiguous runs keep DRAM row locality high under the
+//    page-layer layout, where one layer is only a 128 KiB slice of every
+//    2.75 MiB page (measured: the busiest DRAM channels idle ~18% with 8 KiB
+//    runs).
 //  * S^T = K . Q^T and O^T += V^T . P^T run on the tensor cores with
 //    mma.sync m16n8k16 (fp32 accumulate): tokens on M (16 per tile), the G
 //    query heads of one KV head on N (padded to 8), head_dim as K for QK and
@@ -32,8 +39,8 @@ namespace {
 
 using namespace jenga_decode;
 
-constexpr int kBoxCols = 64;                // elements per swizzle row (128 B)
-constexpr int kBoxBytes = kTile * 128;      // one 64 x 16 box
+constexpr int kBoxCols = 64;            // elements per swizzle row (128 B)
+constexpr int kBoxBytes = kTile * 128;  // one 64 x 16 box
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
@@ -81,19 +88,34 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
-template <typename T, int D, int G, int NS>
-__global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const DecodeParams p,
-                                                                   const __grid_constant__ CUtensorMap tmap) {
+// Shared-memory budget per CTA for the stage ring: 1 CTA/SM when a CTA owns
+// 4 heads, 2 when it owns 2, 3 when it owns 1 (~192 KiB in flight per SM).
+template <int HG>
+constexpr int ring_budget() {
+  return HG >= 4 ? 196608 : (HG == 2 ? 98304 : 65536);
+}
+
+template <int D, int HG>
+constexpr int stages() {
+  constexpr int stage = 2 * HG * kTile * D * 2;
+  constexpr int ns = ring_budget<HG>() / stage;
+  return ns < 2 ? 2 : (ns > 12 ? 12 : ns);
+}
+
+template <typename T, int D, int G, int HG, int NS>
+__global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
+    paged_decode_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
   static_assert(D % kBoxCols == 0, "head_dim must be a multiple of 64");
   static_assert(G <= 8, "at most 8 query heads per KV head (N = 8)");
+  static_assert(kConsumerWarps % HG == 0, "heads per CTA must divide the consumer warps");
   constexpr int NBOX = D / kBoxCols;
-  constexpr int TILE_BYTES = NBOX * kBoxBytes;  // 16 tokens x D x 2 B
-  constexpr int STAGE_BYTES = 2 * TILE_BYTES;
+  constexpr int TILE_BYTES = NBOX * kBoxBytes;  // 16 tokens x D x 2 B, one head
+  constexpr int STAGE_BYTES = 2 * HG * TILE_BYTES;
   constexpr int KSTEPS = D / 16;
+  constexpr int ROUNDS = kConsumerWarps / HG;   // warps per head
   constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
   constexpr int RING = NS * STAGE_BYTES;
   constexpr int BAR_OFFSET = RING > MERGE_BYTES ? RING : MERGE_BYTES;
-  static_assert(NS % kConsumerWarps == 0, "stage ring must be a multiple of the consumer count");
 
   extern __shared__ uint8_t smem_raw[];
   // 128-byte swizzled TMA destinations want 1024-byte aligned boxes.
@@ -104,16 +126,16 @@ __global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const Deco
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int b = blockIdx.z;
-  const int h = blockIdx.y;
-  const int split = blockIdx.x;
+  const int b = grid_request(p);
+  const int h0 = blockIdx.x * HG;  // first KV head of this CTA
+  const int split = grid_split(p);
   const Work wk = assign_work(p, b, split);
   if (split >= wk.nsplit) return;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       jenga_dev::mbar_init(&full[i], 1);
-      jenga_dev::mbar_init(&empty[i], 1);
+      jenga_dev::mbar_init(&empty[i], HG);  // every head's warp releases the stage
     }
     jenga_dev::fence_mbar_init();
   }
@@ -127,29 +149,40 @@ __global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const Deco
       jenga_dev::prefetch_tmap(&tmap);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
       const int64_t row_bytes = D * 2;
-      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * p.tpp;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h0) * p.tpp;
       const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
       const int v_rows = p.hkv * p.tpp;
       for (int it = 0; it < wk.t_count; ++it) {
         const int st = it % NS;
         if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
         uint8_t* ks = smem + st * STAGE_BYTES;
-        uint8_t* vs = ks + TILE_BYTES;
+        uint8_t* vs = ks + HG * TILE_BYTES;
         const int tok0 = (wk.t_begin + it) * kTile;
         const int32_t page = table[tok0 / p.tpp];
         const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(page) * page_rows + tok0 % p.tpp);
         jenga_dev::mbar_arrive_expect_tx(&full[st], STAGE_BYTES);
+        // K of heads h0..h0+HG-1 in address order, then V: two contiguous runs.
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx) {
-          jenga_dev::tma_load_2d(ks + bx * kBoxBytes, &tmap, bx * kBoxCols, row, &full[st], policy);
-          jenga_dev::tma_load_2d(vs + bx * kBoxBytes, &tmap, bx * kBoxCols, row + v_rows, &full[st], policy);
-        }
+        for (int hl = 0; hl < HG; ++hl)
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx)
+            jenga_dev::tma_load_2d(ks + hl * TILE_BYTES + bx * kBoxBytes, &tmap, bx * kBoxCols, row + hl * p.tpp,
+                                   &full[st], policy);
+#pragma unroll
+        for (int hl = 0; hl < HG; ++hl)
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx)
+            jenga_dev::tma_load_2d(vs + hl * TILE_BYTES + bx * kBoxBytes, &tmap, bx * kBoxCols,
+                                   row + v_rows + hl * p.tpp, &full[st], policy);
       }
     }
     return;
   }
 
   // -------------------------------------------------- consumers
+  const int hl = warp % HG;      // local head of this warp
+  const int round = warp / HG;   // which of the ROUNDS stage streams
+  const int h = h0 + hl;
   const int r4 = lane >> 2;  // fragment row group
   const int c4 = lane & 3;   // fragment column pair
   // Q^T as the B operand of S^T = K Q^T: b0 = Q[n][16k + 2c .. +1], b1 = +8
@@ -175,11 +208,11 @@ __global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const Deco
   const int v_half = (lane >> 3) & 1;
   const int x7 = lane & 7;                                // == row & 7 for both
 
-  for (int it = warp; it < wk.t_count; it += kConsumerWarps) {
+  for (int it = round; it < wk.t_count; it += ROUNDS) {
     const int st = it % NS;
     jenga_dev::mbar_wait(&full[st], (it / NS) & 1);
-    uint8_t* ks = smem + st * STAGE_BYTES;
-    uint8_t* vs = ks + TILE_BYTES;
+    uint8_t* ks = smem + st * STAGE_BYTES + hl * TILE_BYTES;
+    uint8_t* vs = smem + st * STAGE_BYTES + (HG + hl) * TILE_BYTES;
     const uint32_t ks_u = jenga_dev::smem_u32(ks), vs_u = jenga_dev::smem_u32(vs);
     const int tok0 = (wk.t_begin + it) * kTile;
 
@@ -236,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const Deco
     const uint32_t pb0 = movm_trans(pack2<T>(p0, p1));
     const uint32_t pb1 = movm_trans(pack2<T>(p2, p3));
     // masked rows of a boundary tile may hold stale / non-finite bytes:
-    // zero them so 0 * V cannot produce NaN inside the MMA.
+    // zero this head's rows so 0 * V cannot produce NaN inside the MMA.
     if (tok0 < wk.lo || tok0 + kTile > wk.n) {
       for (int r = 0; r < kTile; ++r) {
         const int t = tok0 + r;
@@ -270,30 +303,30 @@ __global__ void __launch_bounds__(kThreads, 3) paged_decode_tc_kernel(const Deco
   consumers_sync();
   float* s_acc = reinterpret_cast<float*>(smem);  // [4][G][D]
   float* s_ml = s_acc + kConsumerWarps * G * D;   // [4][G][2]
-  const int h0 = 2 * c4, h1 = h0 + 1;
+  const int q0 = 2 * c4, q1 = q0 + 1;             // query heads held by this lane
 #pragma unroll
   for (int k = 0; k < KSTEPS; ++k) {
     const int d = 16 * k + r4;
-    if (h0 < G) {
-      s_acc[(warp * G + h0) * D + d] = o[k][0];
-      s_acc[(warp * G + h0) * D + d + 8] = o[k][2];
+    if (q0 < G) {
+      s_acc[(warp * G + q0) * D + d] = o[k][0];
+      s_acc[(warp * G + q0) * D + d + 8] = o[k][2];
     }
-    if (h1 < G) {
-      s_acc[(warp * G + h1) * D + d] = o[k][1];
-      s_acc[(warp * G + h1) * D + d + 8] = o[k][3];
+    if (q1 < G) {
+      s_acc[(warp * G + q1) * D + d] = o[k][1];
+      s_acc[(warp * G + q1) * D + d + 8] = o[k][3];
     }
   }
   if (r4 == 0) {
-    if (h0 < G) {
-      s_ml[(warp * G + h0) * 2] = m0;
-      s_ml[(warp * G + h0) * 2 + 1] = l0;
+    if (q0 < G) {
+      s_ml[(warp * G + q0) * 2] = m0;
+      s_ml[(warp * G + q0) * 2 + 1] = l0;
     }
-    if (h1 < G) {
-      s_ml[(warp * G + h1) * 2] = m1;
-      s_ml[(warp * G + h1) * 2 + 1] = l1;
+    if (q1 < G) {
+      s_ml[(warp * G + q1) * 2] = m1;
+      s_ml[(warp * G + q1) * 2 + 1] = l1;
     }
   }
-  merge_epilogue<T, G, D>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h);
+  merge_epilogue<T, G, D, HG>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h0);
 }
 
 // ------------------------------------------------------------ host side
@@ -341,39 +374,60 @@ int tensor_map(const void* base, int D, int dtype, CUtensorMap* out) {
   return JENGA_OK;
 }
 
-template <typename T, int D, int G>
+template <typename T, int D, int G, int HG>
 int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaStream_t stream) {
-  constexpr int NS = 4;
-  constexpr int STAGE = 2 * kTile * D * 2;
+  constexpr int NS = stages<D, HG>();
+  constexpr int STAGE = 2 * HG * kTile * D * 2;
   constexpr int MERGE = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
   const int smem = std::max(NS * STAGE, MERGE) + 2 * NS * 8 + 16 + 1024;
-  auto kern = paged_decode_tc_kernel<T, D, G, NS>;
+  auto kern = paged_decode_tc_kernel<T, D, G, HG, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  dim3 grid(prm.max_splits, prm.hkv, batch);
+  const dim3 grid = decode_grid(prm, batch, HG);
   kern<<<grid, kThreads, smem, stream>>>(prm, tmap);
   return jenga_dev::check_launch("paged_decode_tc_kernel");
 }
 
+template <typename T, int D, int G>
+int dispatch_hg(int hg, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+  switch (hg) {
+    case 1: return launch_tc<T, D, G, 1>(prm, m, batch, s);
+    case 2: return launch_tc<T, D, G, 2>(prm, m, batch, s);
+    case 4: return launch_tc<T, D, G, 4>(prm, m, batch, s);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
 template <typename T, int D>
-int dispatch_g(int G, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+int dispatch_g(int G, int hg, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
   switch (G) {
-    case 1: return launch_tc<T, D, 1>(prm, m, batch, s);
-    case 2: return launch_tc<T, D, 2>(prm, m, batch, s);
-    case 4: return launch_tc<T, D, 4>(prm, m, batch, s);
-    case 8: return launch_tc<T, D, 8>(prm, m, batch, s);
+    case 1: return dispatch_hg<T, D, 1>(hg, prm, m, batch, s);
+    case 2: return dispatch_hg<T, D, 2>(hg, prm, m, batch, s);
+    case 4: return dispatch_hg<T, D, 4>(hg, prm, m, batch, s);
+    case 8: return dispatch_hg<T, D, 8>(hg, prm, m, batch, s);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
 
 template <typename T>
-int dispatch_d(int D, int G, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+int dispatch_d(int D, int G, int hg, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
   switch (D) {
-    case 64: return dispatch_g<T, 64>(G, prm, m, batch, s);
-    case 128: return dispatch_g<T, 128>(G, prm, m, batch, s);
-    case 256: return dispatch_g<T, 256>(G, prm, m, batch, s);
+    case 64: return dispatch_g<T, 64>(G, hg, prm, m, batch, s);
+    case 128: return dispatch_g<T, 128>(G, hg, prm, m, batch, s);
+    case 256: return dispatch_g<T, 256>(G, hg, prm, m, batch, s);
   }
   return JENGA_ERR_UNSUPPORTED;
+}
+
+// KV heads per CTA: 4 when possible (JENGA_DECODE_HEADS_PER_CTA overrides).
+int heads_per_cta(int hkv) {
+  static const int forced = [] {
+    const char* e = std::getenv("JENGA_DECODE_HEADS_PER_CTA");
+    return e ? std::atoi(e) : 0;
+  }();
+  for (int hg : {forced, 4, 2, 1})
+    if ((hg == 1 || hg == 2 || hg == 4) && hkv % hg == 0) return hg;
+  return 1;
 }
 
 }  // namespace
@@ -386,8 +440,9 @@ int launch_decode_tc(const DecodeParams& prm, int dtype, int head_dim, int G, in
   CUtensorMap m;
   const int rc = tensor_map(prm.arena, head_dim, dtype, &m);
   if (rc != JENGA_OK) return rc;
-  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, m, batch, stream);
-  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, prm, m, batch, stream);
+  const int hg = heads_per_cta(prm.hkv);
+  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, hg, prm, m, batch, stream);
+  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, hg, prm, m, batch, stream);
   return JENGA_ERR_UNSUPPORTED;
 }
 
