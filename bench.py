@@ -112,6 +112,7 @@ def run_ours(a, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2503_18292_b200 import ops
+    from paper_2503_18292_b200.distributed import gather_rows, max_over_ranks
     from paper_2503_18292_b200.engine import DecodeEngine
     from paper_2503_18292_b200.geometry import gemma2_9b
 
@@ -126,7 +127,8 @@ def run_ours(a, rank, world, local_rank):
     # exact arena sizing: full group grows to max_tokens; SWA keeps <= W + tpp
     spl_pages = B * (math.ceil(max_tokens / a.tpp) + 1) + B * (math.ceil(4096 / a.tpp) + 2) + 16
     eng = DecodeEngine(geom, spl_pages, B, max_tokens, dev)
-    ids = [rank * 100000 + i for i in range(B)]
+    from paper_2503_18292_b200.distributed import shard_requests
+    ids = shard_requests(list(range(B * world)), rank, world)  # this GPU's requests; pool is private
     eng.add_requests(ids)
     # fill the arena with finite bf16 KV (contents are never re-derived: values only)
     t0 = time.time()
@@ -199,14 +201,16 @@ def run_ours(a, rank, world, local_rank):
     clocks = clk.stop()
     ms = start.elapsed_time(end)
     dec_ms = sum(e0.elapsed_time(e1) for st in evs for e0, e1 in st)
+    kv_bytes_local = kv_bytes
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)           # timed on the device, max over ranks
+        t = torch.tensor([kv_bytes], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)                     # whole-job bytes
+        kv_bytes = int(t.item())
     ms_per_step = ms / a.steps
     # algorithmic bytes of the decode kernel: live K/V + q read + out write
     qo = 2 * nl * B * H * D * 2 * a.steps
-    dec_gbs = (kv_bytes + qo) / (dec_ms * 1e-3) / 1e9
+    dec_gbs = (kv_bytes_local + qo) / (dec_ms * 1e-3) / 1e9
 
     # ---------------- e2e: host buffers through the public API each step
     e2e = None
@@ -243,9 +247,7 @@ def run_ours(a, rank, world, local_rank):
         torch.cuda.synchronize()
         e_ms = s0.elapsed_time(s1)
         if world > 1:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            e_ms = max_over_ranks(e_ms, dev)
         e_val = e_bytes * world / (e_ms * 1e-3) / 1e9
         e2e = {"value": round(e_val, 1), "unit": "GB/s", "h2d_bytes_per_step": int(q.nbytes + kn.nbytes + vn.nbytes),
                "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": round(e_ms / a.steps, 3),
@@ -254,12 +256,11 @@ def run_ours(a, rank, world, local_rank):
     # ---------------- verification gather (NCCL, outside the timed region)
     finite = bool(torch.isfinite(out.float()).all().item())
     if world > 1:
-        gathered = [torch.empty_like(out[-1]) for _ in range(world)]
-        dist.all_gather(gathered, out[-1].contiguous())
-        finite = finite and all(bool(torch.isfinite(x.float()).all().item()) for x in gathered)
+        gathered = gather_rows(out[-1])        # NCCL all-gather of the last layer's outputs
+        finite = finite and bool(torch.isfinite(gathered.float()).all().item())
 
     pk, src = peaks()
-    value = kv_bytes * world / (ms * 1e-3) / 1e9
+    value = kv_bytes / (ms * 1e-3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "decode_traffic.json"
     if tf.exists():

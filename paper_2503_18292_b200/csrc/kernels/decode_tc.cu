@@ -95,11 +95,15 @@ constexpr int ring_budget() {
   return HG >= 4 ? 196608 : (HG == 2 ? 98304 : 65536);
 }
 
+// Ring depth: a multiple of the rounds (kConsumerWarps / HG) so each slot is
+// always consumed by the same warps — a warp that skipped a use of a slot
+// could otherwise wait on a parity two phases ahead and pass early.
 template <int D, int HG>
 constexpr int stages() {
+  constexpr int rounds = kConsumerWarps / HG;
   constexpr int stage = 2 * HG * kTile * D * 2;
-  constexpr int ns = ring_budget<HG>() / stage;
-  return ns < 2 ? 2 : (ns > 12 ? 12 : ns);
+  constexpr int ns = (ring_budget<HG>() / stage) / rounds * rounds;
+  return ns < rounds ? rounds : (ns > 12 ? 12 : ns);
 }
 
 template <typename T, int D, int G, int HG, int NS>
@@ -419,13 +423,16 @@ int dispatch_d(int D, int G, int hg, const DecodeParams& prm, const CUtensorMap&
   return JENGA_ERR_UNSUPPORTED;
 }
 
-// KV heads per CTA: 4 when possible (JENGA_DECODE_HEADS_PER_CTA overrides).
+// KV heads per CTA: 1 by default — three 1-head CTAs per SM overlap each
+// other's prologue/epilogue and measured fastest on the Gemma shard
+// (profiles/r01_sweeps.md); JENGA_DECODE_HEADS_PER_CTA=2|4 selects the
+// multi-head variants.
 int heads_per_cta(int hkv) {
   static const int forced = [] {
     const char* e = std::getenv("JENGA_DECODE_HEADS_PER_CTA");
     return e ? std::atoi(e) : 0;
   }();
-  for (int hg : {forced, 4, 2, 1})
+  for (int hg : {forced, 1})
     if ((hg == 1 || hg == 2 || hg == 4) && hkv % hg == 0) return hg;
   return 1;
 }
