@@ -42,7 +42,8 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--batch-per-gpu", type=int, default=32)
+    p.add_argument("--workload", default="gemma2-9b", choices=["gemma2-9b", "jamba-style", "llama-3.2-11b-vision"])
+    p.add_argument("--batch-per-gpu", type=int, default=0, help="0: the workload's default")
     p.add_argument("--ctx", type=int, default=8192)
     p.add_argument("--tpp", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -59,7 +60,7 @@ def peaks():
 
 
 def workload_desc(a):
-    return (f"gemma2-9b decode: {a.batch_per_gpu} req/GPU x {a.ctx} ctx, {2 * a.layers_per_group} layers "
+    return (f"gemma2-9b decode: {a.batch_per_gpu or 32} req/GPU x {a.ctx} ctx, {2 * a.layers_per_group} layers "
             f"({a.layers_per_group} full + {a.layers_per_group} SWA-4096), Hq=16 Hkv=8 D=256, tpp={a.tpp}")
 
 
@@ -106,111 +107,196 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# --------------------------------------------------------------------- workloads
+class Workload:
+    """One BASELINE.json config as a decode loop: layer schedule in model
+    order, prompt construction and algorithmic byte accounting."""
+
+    def __init__(self, a):
+        from paper_2503_18292_b200.geometry import gemma2_9b, jamba_style, llama32_11b_vision
+        self.name = a.workload
+        self.ctx = a.ctx
+        self.image_tokens = 0
+        if a.workload == "gemma2-9b":
+            self.geom = gemma2_9b(a.tpp)
+            for gg in self.geom.groups:
+                gg.num_layers = a.layers_per_group
+            self.B = a.batch_per_gpu or 32
+            L = a.layers_per_group
+            self.layers = [(g, l) for l in range(L) for g in (0, 1)]  # alternating full / SWA
+            self.desc = (f"gemma2-9b decode: {self.B} req/GPU x {a.ctx} ctx, {2 * L} layers ({L} full + {L} "
+                         f"SWA-4096), Hq=16 Hkv=8 D=256, tpp={a.tpp}")
+        elif a.workload == "jamba-style":
+            self.geom = jamba_style(a.tpp)
+            self.B = a.batch_per_gpu or 64
+            self.layers = []
+            for i in range(4):  # one attention layer per 8 (Jamba), 28 Mamba layers
+                self.layers.append((0, i))
+                self.layers += [(1, 7 * i + j) for j in range(7)]
+            self.desc = (f"jamba-style hybrid decode: {self.B} req/GPU x {a.ctx} ctx, 4 attention layers (Hq=32 Hkv=8 "
+                         f"D=128 bf16, tpp={a.tpp}) + 28 Mamba layers with fp32 last-token state pages "
+                         f"(622,592 B/layer) in the same LCM pool; state gathered and scattered per layer")
+        elif a.workload == "llama-3.2-11b-vision":
+            self.geom = llama32_11b_vision(a.tpp)
+            self.B = a.batch_per_gpu or 64
+            self.image_tokens = 6404  # one image = 4 tiles x 1601 tokens
+            self.layers = []
+            for i in range(8):  # a cross-attention layer after every 4 self-attention layers
+                self.layers += [(0, 4 * i + j) for j in range(4)]
+                self.layers.append((1, i))
+            self.desc = (f"llama-3.2-11b-vision decode: {self.B} req/GPU x {a.ctx} text ctx + {self.image_tokens} "
+                         f"image tokens, 32 self-attention + 8 cross-attention layers, Hq=32 Hkv=8 D=128 bf16, "
+                         f"tpp={a.tpp}")
+        else:
+            raise SystemExit(f"unknown workload {a.workload}")
+        self.spec = self.geom.spec()
+
+    def max_tokens(self, steps):
+        return max(self.ctx + self.image_tokens + steps + 16, 64)
+
+    def arena_large_pages(self, steps):
+        from paper_2503_18292_b200 import AddressMap
+        from paper_2503_18292_b200.jenga import LayerKind
+        addr = AddressMap(self.spec)
+        total = 0
+        for g, gg in enumerate(self.geom.groups):
+            tpp = self.spec.groups[g].tokens_per_page
+            if gg.kind == LayerKind.kMamba:
+                smalls = self.B
+            elif gg.kind == LayerKind.kCrossAttention:
+                smalls = self.B * (math.ceil(self.image_tokens / tpp) + 1)
+            elif gg.kind == LayerKind.kSlidingWindow:
+                smalls = self.B * (math.ceil(gg.window / tpp) + 2)
+            else:
+                smalls = self.B * (math.ceil((self.ctx + steps + 16) / tpp) + 1)
+            total += math.ceil(smalls / addr.slots_per_large(g)) + self.B  # request-aware units
+        return total + 8
+
+    def prompt(self, eng, ids, rank):
+        """Interleaved prompt: images first (cross groups store them), then text;
+        seeded request order per 16-position chunk so pages interleave."""
+        rng = np.random.default_rng(1234 + rank)
+        B = len(ids)
+        order = np.arange(B)
+        n_img = self.image_tokens
+        for pos in range(n_img + self.ctx - 1):
+            if pos % 16 == 0:
+                order = rng.permutation(B)
+            img = [1] * B if pos < n_img else None
+            done = eng.append([ids[i] for i in order], is_image=img)
+            assert done == B
+
+
 # --------------------------------------------------------------------- our arm
 def run_ours(a, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     from paper_2503_18292_b200 import ops
-    from paper_2503_18292_b200.distributed import gather_rows, max_over_ranks
+    from paper_2503_18292_b200.distributed import gather_rows, max_over_ranks, shard_requests, sum_over_ranks
     from paper_2503_18292_b200.engine import DecodeEngine
-    from paper_2503_18292_b200.geometry import gemma2_9b
+    from paper_2503_18292_b200.jenga import LayerKind
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device(f"cuda:{local_rank}")
-    geom = gemma2_9b(a.tpp)
-    for gg in geom.groups:
-        gg.num_layers = a.layers_per_group
-    B = a.batch_per_gpu
+    local_dev = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device(f"cuda:{local_dev}")
+    wl = Workload(a)
+    B = wl.B
     total_steps = a.warmup + a.steps + (0 if a.no_e2e else a.warmup + a.steps) + 2
-    max_tokens = a.ctx + total_steps + 16
-    # exact arena sizing: full group grows to max_tokens; SWA keeps <= W + tpp
-    spl_pages = B * (math.ceil(max_tokens / a.tpp) + 1) + B * (math.ceil(4096 / a.tpp) + 2) + 16
-    eng = DecodeEngine(geom, spl_pages, B, max_tokens, dev)
-    from paper_2503_18292_b200.distributed import shard_requests
-    ids = shard_requests(list(range(B * world)), rank, world)  # this GPU's requests; pool is private
+    eng = DecodeEngine(wl.geom, wl.arena_large_pages(total_steps), B, wl.max_tokens(total_steps), dev)
+    ids = shard_requests(list(range(B * world)), rank, world)  # this GPU's requests; its pool is private
     eng.add_requests(ids)
-    # fill the arena with finite bf16 KV (contents are never re-derived: values only)
     t0 = time.time()
-    av = eng.arena.tensor().view(torch.bfloat16)
+    av = eng.arena.tensor().view(torch.bfloat16)  # finite random KV / state bytes (values only)
     chunk = 1 << 30
     for s in range(0, av.numel(), chunk):
         av[s:s + chunk].normal_()
-    # prefill page lists to ctx-1 tokens, interleaved (seeded order per 16-position chunk)
-    rng = np.random.default_rng(1234 + rank)
-    order = np.arange(B)
-    for pos in range(a.ctx - 1):
-        if pos % 16 == 0:
-            order = rng.permutation(B)
-        done = eng.append([ids[i] for i in order])
-        assert done == B
+    wl.prompt(eng, ids, rank)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
 
-    H, D, Hkv = 16, 256, 8
-    nl = 2 * a.layers_per_group
+    attn = [(i, g, l) for i, (g, l) in enumerate(wl.layers) if eng.tables[g].geom.is_attention]
+    mamba = [(i, g, l) for i, (g, l) in enumerate(wl.layers) if eng.tables[g].geom.kind == LayerKind.kMamba]
     gen = torch.Generator(device=dev).manual_seed(1 + rank)
-    q = torch.randn((nl, B, H, D), generator=gen, device=dev).to(torch.bfloat16)
-    kn = torch.randn((nl, B, Hkv, D), generator=gen, device=dev).to(torch.bfloat16)
-    vn = torch.randn((nl, B, Hkv, D), generator=gen, device=dev).to(torch.bfloat16)
+    g0 = eng.tables[attn[0][1]].geom
+    H, Hkv, D = g0.num_q_heads, g0.num_kv_heads, g0.head_dim
+    na = len(attn)
+    q = torch.randn((na, B, H, D), generator=gen, device=dev).to(g0.dtype)
+    kn = torch.randn((na, B, Hkv, D), generator=gen, device=dev).to(g0.dtype)
+    vn = torch.randn((na, B, Hkv, D), generator=gen, device=dev).to(g0.dtype)
     out = torch.empty_like(q)
-    layers = [(g, l) for l in range(a.layers_per_group) for g in (0, 1)]  # alternating full / SWA
+    state = None
+    if mamba:
+        state = torch.empty((B, eng.view(mamba[0][1], 0).exec_page_size), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-
     bptl = 2 * Hkv * D * 2
+    slot = {i: j for j, (i, _, _) in enumerate(attn)}
 
     def step(ev=None):
         eng.append()
         eng.sync_tables()
-        for i, (g, l) in enumerate(layers):
-            eng.write_kv(g, l, kn[i], vn[i])
+        pg = {}
+        for i, (g, l) in enumerate(wl.layers):
+            kind = eng.tables[g].geom.kind
+            if kind == LayerKind.kMamba:
+                if g not in pg:
+                    pg[g] = eng.mamba_page_globals(g)
+                v = eng.view(g, l)
+                ops.mamba_state_gather(eng.arena, v, pg[g], state)   # last-token state -> dense
+                ops.mamba_state_scatter(eng.arena, v, pg[g], state)  # (SSM update out of scope)
+                continue
+            j = slot[i]
+            if kind != LayerKind.kCrossAttention:  # cross KV (image tokens) is static during decode
+                eng.write_kv(g, l, kn[j], vn[j])
             if ev is not None:
-                ev[i][0].record(stream)
-            eng.decode(g, l, q[i], out[i])
+                ev[j][0].record(stream)
+            eng.decode(g, l, q[j], out[j])
             if ev is not None:
-                ev[i][1].record(stream)
+                ev[j][1].record(stream)
 
-    def live_bytes():
-        full = eng.live_tokens(0).sum()
-        win = eng.live_tokens(1).sum()
-        return int((full + win) * a.layers_per_group * bptl), int((full + win) * a.layers_per_group)
+    def step_bytes():
+        """(KV bytes read by decode, Mamba state bytes moved) for this step."""
+        kv = 0
+        for _, g, _ in attn:
+            kv += int(eng.live_tokens(g).sum()) * bptl
+        st = 0
+        for _, g, l in mamba:
+            st += 2 * B * eng.view(g, l).exec_page_size
+        return kv, st
 
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in layers]
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in attn]
            for _ in range(a.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kv_bytes = 0
-    kv_tokens = 0
-    clk = ClockSampler(local_rank)
+    kv_bytes = st_bytes = 0
+    clk = ClockSampler(local_dev)
     clk.start()
     launches0 = ops.kernel_launch_count()
     torch.cuda.synchronize()
     start.record(stream)
     for s in range(a.steps):
         step(evs[s])
-        b, t = live_bytes()
-        kv_bytes += b
-        kv_tokens += t
+        kb, sb = step_bytes()
+        kv_bytes += kb
+        st_bytes += sb
     end.record(stream)
     torch.cuda.synchronize()
     launches = ops.kernel_launch_count() - launches0
     clocks = clk.stop()
     ms = start.elapsed_time(end)
     dec_ms = sum(e0.elapsed_time(e1) for st in evs for e0, e1 in st)
-    kv_bytes_local = kv_bytes
+    kv_local = kv_bytes
+    moved = kv_bytes + st_bytes
     if world > 1:
-        ms = max_over_ranks(ms, dev)           # timed on the device, max over ranks
-        t = torch.tensor([kv_bytes], device=dev, dtype=torch.float64)
-        dist.all_reduce(t)                     # whole-job bytes
-        kv_bytes = int(t.item())
+        ms = max_over_ranks(ms, dev)                   # timed on the device, max over ranks
+        moved = int(sum_over_ranks(moved, dev))        # whole-job bytes
     ms_per_step = ms / a.steps
-    # algorithmic bytes of the decode kernel: live K/V + q read + out write
-    qo = 2 * nl * B * H * D * 2 * a.steps
-    dec_gbs = (kv_bytes_local + qo) / (dec_ms * 1e-3) / 1e9
+    qo = 2 * na * B * H * D * 2 * a.steps              # q read + out write of the decode launches
+    dec_gbs = (kv_local + qo) / (dec_ms * 1e-3) / 1e9
 
     # ---------------- e2e: host buffers through the public API each step
     e2e = None
@@ -236,21 +322,21 @@ def run_ours(a, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
         e_bytes = 0
-        t0 = time.perf_counter()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(a.steps):
             e2e_step()
-            e_bytes += live_bytes()[0]
+            e_bytes += sum(step_bytes())
         s1.record(stream)
         torch.cuda.synchronize()
         e_ms = s0.elapsed_time(s1)
         if world > 1:
             e_ms = max_over_ranks(e_ms, dev)
-        e_val = e_bytes * world / (e_ms * 1e-3) / 1e9
-        e2e = {"value": round(e_val, 1), "unit": "GB/s", "h2d_bytes_per_step": int(q.nbytes + kn.nbytes + vn.nbytes),
-               "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": round(e_ms / a.steps, 3),
+            e_bytes = int(sum_over_ranks(e_bytes, dev))
+        e2e = {"value": round(e_bytes / (e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
+               "h2d_bytes_per_step": int(q.nbytes + kn.nbytes + vn.nbytes), "d2h_bytes_per_step": int(out.nbytes),
+               "ms_per_step": round(e_ms / a.steps, 3),
                "tokens_per_s": round(B * world * a.steps / (e_ms * 1e-3), 1)}
 
     # ---------------- verification gather (NCCL, outside the timed region)
@@ -260,33 +346,37 @@ def run_ours(a, rank, world, local_rank):
         finite = finite and bool(torch.isfinite(gathered.float()).all().item())
 
     pk, src = peaks()
-    value = kv_bytes / (ms * 1e-3) / 1e9
+    value = moved / (ms * 1e-3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "decode_traffic.json"
-    if tf.exists():
+    if tf.exists() and a.workload == "gemma2-9b":
         try:
             traffic = json.loads(tf.read_text()).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
+    kname = f"paged_decode_tc_kernel<bf16, D={D}, G={H // Hkv}> (TMA + mma.sync)"
     res = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random N(0,1) bf16 KV/q; page lists from the "
                                                     "native Jenga allocator, seeded interleaved request order)",
-        "config": {"workload": workload_desc(a), "global_batch": B * world, "seq_len": a.ctx,
+        "config": {"workload": wl.desc, "global_batch": B * world, "seq_len": a.ctx,
                    "parallelism": f"dp{world} (request shards, independent Jenga pool per GPU)",
-                   "l2": "inputs larger than L2 (KV arena %.1f GB/GPU vs 126 MB L2); no flush needed"
+                   "l2": "inputs larger than L2 (arena %.1f GB/GPU vs 126 MB L2); no flush needed"
                          % (eng.arena.nbytes / 1e9)},
         "tokens_per_s": round(B * world * a.steps / (ms * 1e-3), 1),
         "frac_of_hbm_peak": round(value / world / pk["hbm_gbs"], 4),
-        "roofline": {"bound": "hbm", "kernel": "paged_decode_tc_kernel<bf16, D=256, G=2> (TMA + mma.sync)", "achieved": round(dec_gbs, 1),
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(dec_gbs, 1),
                      "peak": pk["hbm_gbs"], "peak_source": src, "unit": "GB/s",
                      "frac": round(dec_gbs / pk["hbm_gbs"], 4), "traffic": traffic,
                      "decode_share_of_step": round(dec_ms / (ms_per_step * a.steps), 4),
-                     "algorithmic_bytes_per_step": int((kv_bytes + qo) / a.steps)},
+                     "algorithmic_bytes_per_step": int((kv_local + qo) / a.steps),
+                     "algorithmic_bytes_per_launch": int((kv_local + qo) / a.steps / na)},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "setup_s": round(setup_s, 1), "outputs_finite": finite,
     }
+    if st_bytes:
+        res["mamba_state_bytes_per_step"] = int(st_bytes / a.steps)
     return res
 
 
@@ -388,7 +478,7 @@ def run_reference(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(el / max(a.steps, 1) * 1e3, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic", "config": {"workload": workload_desc(a) + " — CPU sample: " + res0["sample"],
-                                            "global_batch": a.batch_per_gpu * a.gpus, "seq_len": a.ctx,
+                                            "global_batch": (a.batch_per_gpu or 32) * a.gpus, "seq_len": a.ctx,
                                             "parallelism": "host cores"},
             "cpu_baseline": cb, "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
@@ -409,9 +499,13 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        backend = os.environ.get("JENGA_BENCH_BACKEND", "nccl")  # gloo only for 1-GPU rehearsals
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            dist.init_process_group(backend)
     res = run_ours(a, rank, world, local_rank)
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.workload == "gemma2-9b":
         try:
             res["cpu_baseline"] = cpu_sample(a, steps=1)
         except Exception as e:  # the baseline must not sink the GPU line

@@ -25,16 +25,28 @@ def shard_requests(global_ids: Sequence[int], rank: int, world: int) -> List[int
 def gather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather equal-shaped per-rank tensors into [world * rows, ...] in rank order."""
     world = dist.get_world_size(group)
-    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    if local.device.type == "cuda":
+    if local.device.type == "cuda" and dist.get_backend(group) == "nccl":
+        out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
-    else:
-        parts = list(out.chunk(world))
-        dist.all_gather(parts, local.contiguous(), group=group)
-    return out
+        return out
+    host = local.detach().cpu().contiguous()
+    out = torch.empty((world * host.shape[0],) + tuple(host.shape[1:]), dtype=host.dtype)
+    dist.all_gather(list(out.chunk(world)), host, group=group)
+    return out.to(local.device)
+
+
+def _backend_device(device, group=None):
+    return device if dist.get_backend(group) == "nccl" else "cpu"
 
 
 def max_over_ranks(value: float, device, group=None) -> float:
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64, device=_backend_device(device, group))
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, device, group=None) -> float:
+    t = torch.tensor([value], dtype=torch.float64, device=_backend_device(device, group))
+    dist.all_reduce(t, group=group)
     return float(t.item())
