@@ -20,6 +20,14 @@ int set(int code, const char* msg);
 
 namespace jenga_dev {
 int set_error(int code, const std::string& msg) { return jenga_host_err::set(code, msg.c_str()); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("JENGA_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
 }  // namespace jenga_dev
 
 struct jenga_arena {

@@ -18,6 +18,10 @@ __global__ void __launch_bounds__(256) reshape_and_cache_kernel(
     uint32_t tpp, const uint8_t* __restrict__ key, const uint8_t* __restrict__ value,
     int64_t token_stride_bytes, const int64_t* __restrict__ slots, int n_tokens) {
   const int chunks_per_row = row_bytes >> 4;
+  // PDL: let the decode kernel that follows get resident now; wait for our own
+  // prerequisites (the previous layer's decode) before touching the arena.
+  jenga_dev::pdl_launch_dependents();
+  jenga_dev::pdl_wait();
   const int64_t total = static_cast<int64_t>(n_tokens) * hkv * 2 * chunks_per_row;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -103,10 +107,10 @@ JENGA_EXPORT int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view
   if (n_tokens == 0) return JENGA_OK;
   const int64_t total = static_cast<int64_t>(n_tokens) * num_kv_heads * 2 * (row_bytes / 16);
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  reshape_and_cache_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<uint8_t*>(arena_base), view.start_offset, view.page_stride, num_kv_heads, row_bytes,
-      tokens_per_page, static_cast<const uint8_t*>(key), static_cast<const uint8_t*>(value),
-      kv_token_stride * e, slot_mapping, n_tokens);
+  launch_maybe_pdl(reshape_and_cache_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                   static_cast<uint8_t*>(arena_base), view.start_offset, view.page_stride, num_kv_heads, row_bytes,
+                   tokens_per_page, static_cast<const uint8_t*>(key), static_cast<const uint8_t*>(value),
+                   kv_token_stride * e, slot_mapping, n_tokens);
   return check_launch("reshape_and_cache_kernel");
 }
 

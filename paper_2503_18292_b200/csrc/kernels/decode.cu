@@ -319,15 +319,6 @@ int grid_order() {
   return v;
 }
 
-// L2 prefetch distance (tiles); JENGA_DECODE_PREFETCH overrides.
-int prefetch_tiles() {
-  static const int v = [] {
-    const char* e = std::getenv("JENGA_DECODE_PREFETCH");
-    return e ? std::max(0, std::atoi(e)) : kDefaultPrefetchTiles;
-  }();
-  return v;
-}
-
 template <typename T, int D, int G>
 int launch_typed(const DecodeParams& prm, int batch, cudaStream_t stream) {
   constexpr int NS = 4;
@@ -372,7 +363,7 @@ JENGA_EXPORT size_t jenga_paged_decode_workspace_size(int batch, int num_q_heads
   const int64_t ms = splits_for(max_blocks, static_cast<int>(tokens_per_page), kMinTilesPerSplit);
   const int64_t bh = static_cast<int64_t>(batch) * num_kv_heads;
   const int64_t G = num_q_heads / num_kv_heads;
-  const int64_t counters = ((bh * 4 + 255) / 256) * 256;
+  const int64_t counters = ((bh * 4 + 16 + 255) / 256) * 256;
   return static_cast<size_t>(counters + bh * ms * G * head_dim * 4 + bh * ms * G * 2 * 4);
 }
 
@@ -420,12 +411,8 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
   prm.hkv = num_kv_heads;
   prm.tpp = tpp;
   prm.tiles_per_split = tiles_per_split();
-  prm.prefetch_tiles = prefetch_tiles();
-  prm.prefetch_mode = [] {
-    const char* e = std::getenv("JENGA_DECODE_PREFETCH_MODE");
-    return e ? std::atoi(e) : 0;
-  }();
   prm.grid_order = grid_order();
+  prm.batch = batch;
   prm.max_splits = splits_for(max_blocks, tpp, tiles_per_split());
   if (softcap > 0.f) {
     prm.qscale = scale;
@@ -439,8 +426,9 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
   const int64_t bh = static_cast<int64_t>(batch) * num_kv_heads;
   const int64_t G = num_q_heads / num_kv_heads;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const int64_t counters = ((bh * 4 + 255) / 256) * 256;
+  const int64_t counters = ((bh * 4 + 16 + 255) / 256) * 256;
   prm.counters = reinterpret_cast<int*>(ws);
+  prm.work = prm.counters + bh;  // two ints after the split tickets
   prm.part_acc = reinterpret_cast<float*>(ws + counters);
   prm.part_ml = prm.part_acc + bh * prm.max_splits * G * head_dim;
 

@@ -13,7 +13,6 @@ constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
-constexpr int kDefaultPrefetchTiles = 0;
 
 struct DecodeParams {
   const uint8_t* arena;
@@ -31,9 +30,9 @@ struct DecodeParams {
   int tpp;
   int tiles_per_split;
   int max_splits;
-  int prefetch_tiles;  // L2 prefetch distance in tiles (0: off)
-  int prefetch_mode;   // 0: one line (translation warm-up), 1: whole tile
   int grid_order;      // 0: (head, request, split); 1: (head, split, request)
+  int batch;
+  int* work;           // persistent kernel: [0] next work item, [1] CTAs finished
   float qscale;    // scale*log2e, or scale when soft-capping
   float cap_log2;  // softcap*log2e (0: off)
   float inv_cap;   // 1/softcap

@@ -106,17 +106,198 @@ constexpr int stages() {
   return ns < rounds ? rounds : (ns > 12 ? 12 : ns);
 }
 
+// ------------------------------------------------------------ per-warp math
+// One consumer warp's running state for one KV head: Q^T fragments (the B
+// operand of S^T = K Q^T), the O^T accumulators and the online-softmax
+// statistics of the two query heads this lane's fragments hold.
+template <int D>
+struct HeadState {
+  static constexpr int K = D / 16;
+  uint32_t bq[K][2];
+  float o[K][4];
+  float m0, m1, l0, l1;  // query heads 2*c4, 2*c4+1
+};
+
+template <typename T, int D, int G>
+__device__ __forceinline__ void head_begin(HeadState<D>& st, const DecodeParams& p, int b, int h, int lane) {
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(p.q) +
+                                                           (static_cast<int64_t>(b) * p.hq + h * G + r4) * D);
+#pragma unroll
+  for (int k = 0; k < HeadState<D>::K; ++k) {
+    st.bq[k][0] = r4 < G ? __ldg(qrow + (16 * k + 2 * c4) / 2) : 0u;
+    st.bq[k][1] = r4 < G ? __ldg(qrow + (16 * k + 8 + 2 * c4) / 2) : 0u;
+    st.o[k][0] = st.o[k][1] = st.o[k][2] = st.o[k][3] = 0.f;
+  }
+  st.m0 = st.m1 = -INFINITY;
+  st.l0 = st.l1 = 0.f;
+}
+
+// One 16-token tile of one head: ks/vs are the head's K and V tiles (NBOX
+// swizzled 64x16 boxes each) in shared memory.
+template <typename T, int D>
+__device__ __forceinline__ void head_tile(HeadState<D>& st, uint8_t* ks, uint8_t* vs, int tok0, int lo, int n,
+                                          const DecodeParams& p, int lane) {
+  constexpr int KS = HeadState<D>::K;
+  constexpr int NBOX = D / kBoxCols;
+  const int r4 = lane >> 2;
+  const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8;  // K tile row fed by this lane
+  const int k_half = lane >> 4;                           // which 8-wide D half
+  const int v_tok = (lane & 7) + (lane >> 4) * 8;         // V tile token row fed by this lane
+  const int v_half = (lane >> 3) & 1;
+  const int x7 = lane & 7;                                // == row & 7 for both
+  const uint32_t ks_u = jenga_dev::smem_u32(ks), vs_u = jenga_dev::smem_u32(vs);
+
+  // ---- S^T = K . Q^T  (16 tokens x 8 heads, fp32)
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int chunk = 2 * k + k_half;
+    uint32_t a[4];
+    ldsm_x4(a, ks_u + (chunk >> 3) * kBoxBytes + k_row * 128 + (((chunk & 7) ^ x7) << 4));
+    mma16816<T>(s, a, st.bq[k][0], st.bq[k][1]);
+  }
+  // ---- scale, soft-cap, mask (needs_token), online softmax
+  const int ta = tok0 + r4, tb = ta + 8;
+  const bool va = ta >= lo && ta < n, vb = tb >= lo && tb < n;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float x = s[i] * p.qscale;
+    if (p.cap_log2 > 0.f) x = p.cap_log2 * tanhf(x * p.inv_cap);
+    s[i] = x;
+  }
+  s[0] = va ? s[0] : -INFINITY;
+  s[1] = va ? s[1] : -INFINITY;
+  s[2] = vb ? s[2] : -INFINITY;
+  s[3] = vb ? s[3] : -INFINITY;
+  float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, off));
+    t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, off));
+  }
+  const float n0 = fmaxf(st.m0, t0), n1 = fmaxf(st.m1, t1);
+  const float a0 = n0 == -INFINITY ? 1.f : jenga_dev::fast_exp2(st.m0 - n0);
+  const float a1 = n1 == -INFINITY ? 1.f : jenga_dev::fast_exp2(st.m1 - n1);
+  st.m0 = n0;
+  st.m1 = n1;
+  const float p0 = va ? jenga_dev::fast_exp2(s[0] - n0) : 0.f;
+  const float p1 = va ? jenga_dev::fast_exp2(s[1] - n1) : 0.f;
+  const float p2 = vb ? jenga_dev::fast_exp2(s[2] - n0) : 0.f;
+  const float p3 = vb ? jenga_dev::fast_exp2(s[3] - n1) : 0.f;
+  st.l0 = st.l0 * a0 + p0 + p2;
+  st.l1 = st.l1 * a1 + p1 + p3;
+  if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      st.o[k][0] *= a0;
+      st.o[k][1] *= a1;
+      st.o[k][2] *= a0;
+      st.o[k][3] *= a1;
+    }
+  }
+  // P^T as the B operand of O^T += V^T P^T (k = tokens, n = heads)
+  const uint32_t pb0 = movm_trans(pack2<T>(p0, p1));
+  const uint32_t pb1 = movm_trans(pack2<T>(p2, p3));
+  // masked rows of a boundary tile may hold stale / non-finite bytes:
+  // zero this head's rows so 0 * V cannot produce NaN inside the MMA.
+  if (tok0 < lo || tok0 + kTile > n) {
+    for (int r = 0; r < kTile; ++r) {
+      const int t = tok0 + r;
+      if (t >= lo && t < n) continue;
+      for (int c = lane; c < NBOX * 8; c += 32)
+        *reinterpret_cast<uint4*>(vs + (c >> 3) * kBoxBytes + r * 128 + ((c & 7) << 4)) = make_uint4(0, 0, 0, 0);
+    }
+    // order these generic-proxy writes before the TMA refill of this stage
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+  }
+  // ---- O^T += V^T . P^T  (D x 8 heads)
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int chunk = 2 * k + v_half;
+    uint32_t a[4];
+    ldsm_x4_trans(a, vs_u + (chunk >> 3) * kBoxBytes + v_tok * 128 + (((chunk & 7) ^ x7) << 4));
+    mma16816<T>(st.o[k], a, pb0, pb1);
+  }
+}
+
+// Reduce the per-lane l partials and write this warp's unnormalised state to
+// the merge area s_acc[warp][G][D] / s_ml[warp][G][2].
+template <int D, int G>
+__device__ __forceinline__ void head_store(HeadState<D>& st, float* s_acc, float* s_ml, int warp, int lane) {
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, off);
+    st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, off);
+  }
+  const int r4 = lane >> 2, c4 = lane & 3;
+  const int q0 = 2 * c4, q1 = q0 + 1;
+#pragma unroll
+  for (int k = 0; k < HeadState<D>::K; ++k) {
+    const int d = 16 * k + r4;
+    if (q0 < G) {
+      s_acc[(warp * G + q0) * D + d] = st.o[k][0];
+      s_acc[(warp * G + q0) * D + d + 8] = st.o[k][2];
+    }
+    if (q1 < G) {
+      s_acc[(warp * G + q1) * D + d] = st.o[k][1];
+      s_acc[(warp * G + q1) * D + d + 8] = st.o[k][3];
+    }
+  }
+  if (r4 == 0) {
+    if (q0 < G) {
+      s_ml[(warp * G + q0) * 2] = st.m0;
+      s_ml[(warp * G + q0) * 2 + 1] = st.l0;
+    }
+    if (q1 < G) {
+      s_ml[(warp * G + q1) * 2] = st.m1;
+      s_ml[(warp * G + q1) * 2 + 1] = st.l1;
+    }
+  }
+}
+
+// TMA loads of one tile (16 tokens) of HG heads into a stage:
+// K of heads h0..h0+HG-1 in address order, then V — two contiguous runs.
+template <int D, int HG>
+__device__ __forceinline__ void load_stage(const CUtensorMap* tmap, uint8_t* stage, uint64_t* bar, int32_t row,
+                                           int tpp, int v_rows, uint64_t policy) {
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int TILE_BYTES = NBOX * kBoxBytes;
+  jenga_dev::mbar_arrive_expect_tx(bar, 2 * HG * TILE_BYTES);
+#pragma unroll
+  for (int hl = 0; hl < HG; ++hl)
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      jenga_dev::tma_load_2d(stage + hl * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols, row + hl * tpp, bar,
+                             policy);
+#pragma unroll
+  for (int hl = 0; hl < HG; ++hl)
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      jenga_dev::tma_load_2d(stage + (HG + hl) * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols,
+                             row + v_rows + hl * tpp, bar, policy);
+}
+
+// Arena row of the first K row of (page of token tok0, head h0).
+__device__ __forceinline__ int32_t tile_row(const DecodeParams& p, const int32_t* table, int h0, int tok0,
+                                            int64_t row_bytes) {
+  const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h0) * p.tpp;
+  const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+  return static_cast<int32_t>(base_row + static_cast<int64_t>(table[tok0 / p.tpp]) * page_rows + tok0 % p.tpp);
+}
+
+// ------------------------------------------------------------ grid kernel
+// One CTA per (KV-head group, request, split).
 template <typename T, int D, int G, int HG, int NS>
 __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
     paged_decode_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
   static_assert(D % kBoxCols == 0, "head_dim must be a multiple of 64");
   static_assert(G <= 8, "at most 8 query heads per KV head (N = 8)");
   static_assert(kConsumerWarps % HG == 0, "heads per CTA must divide the consumer warps");
-  constexpr int NBOX = D / kBoxCols;
-  constexpr int TILE_BYTES = NBOX * kBoxBytes;  // 16 tokens x D x 2 B, one head
+  constexpr int TILE_BYTES = (D / kBoxCols) * kBoxBytes;  // 16 tokens x D x 2 B, one head
   constexpr int STAGE_BYTES = 2 * HG * TILE_BYTES;
-  constexpr int KSTEPS = D / 16;
-  constexpr int ROUNDS = kConsumerWarps / HG;   // warps per head
+  constexpr int ROUNDS = kConsumerWarps / HG;            // warps per head
   constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
   constexpr int RING = NS * STAGE_BYTES;
   constexpr int BAR_OFFSET = RING > MERGE_BYTES ? RING : MERGE_BYTES;
@@ -144,193 +325,219 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
     jenga_dev::fence_mbar_init();
   }
   __syncthreads();
+  // PDL: the next kernel in the stream may become resident now.  Block
+  // tables / seq_lens come from a non-PDL kernel and are complete; q, the
+  // newest token's K/V (reshape_and_cache) and the reused workspace are only
+  // touched after pdl_wait().
+  jenga_dev::pdl_launch_dependents();
 
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
   if (warp == kConsumerWarps) {
-    // ------------------------------------------------ producer (one lane)
-    if (lane == 0) {
+    if (lane == 0) {  // producer: one elected lane
       jenga_dev::prefetch_tmap(&tmap);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int64_t row_bytes = D * 2;
-      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h0) * p.tpp;
-      const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
       const int v_rows = p.hkv * p.tpp;
+      bool waited = false;
       for (int it = 0; it < wk.t_count; ++it) {
         const int st = it % NS;
         if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
-        uint8_t* ks = smem + st * STAGE_BYTES;
-        uint8_t* vs = ks + HG * TILE_BYTES;
         const int tok0 = (wk.t_begin + it) * kTile;
-        const int32_t page = table[tok0 / p.tpp];
-        const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(page) * page_rows + tok0 % p.tpp);
-        jenga_dev::mbar_arrive_expect_tx(&full[st], STAGE_BYTES);
-        // K of heads h0..h0+HG-1 in address order, then V: two contiguous runs.
-#pragma unroll
-        for (int hl = 0; hl < HG; ++hl)
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            jenga_dev::tma_load_2d(ks + hl * TILE_BYTES + bx * kBoxBytes, &tmap, bx * kBoxCols, row + hl * p.tpp,
-                                   &full[st], policy);
-#pragma unroll
-        for (int hl = 0; hl < HG; ++hl)
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            jenga_dev::tma_load_2d(vs + hl * TILE_BYTES + bx * kBoxBytes, &tmap, bx * kBoxCols,
-                                   row + v_rows + hl * p.tpp, &full[st], policy);
+        if (!waited && tok0 + kTile >= wk.n) {  // the tile holding the newest token
+          jenga_dev::pdl_wait();
+          waited = true;
+        }
+        load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], tile_row(p, table, h0, tok0, D * 2), p.tpp,
+                          v_rows, policy);
       }
     }
     return;
   }
 
-  // -------------------------------------------------- consumers
   const int hl = warp % HG;      // local head of this warp
   const int round = warp / HG;   // which of the ROUNDS stage streams
-  const int h = h0 + hl;
-  const int r4 = lane >> 2;  // fragment row group
-  const int c4 = lane & 3;   // fragment column pair
-  // Q^T as the B operand of S^T = K Q^T: b0 = Q[n][16k + 2c .. +1], b1 = +8
-  uint32_t bq[KSTEPS][2];
-  {
-    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(static_cast<const T*>(p.q) +
-                                                             (static_cast<int64_t>(b) * p.hq + h * G + r4) * D);
-#pragma unroll
-    for (int k = 0; k < KSTEPS; ++k) {
-      bq[k][0] = r4 < G ? __ldg(qrow + (16 * k + 2 * c4) / 2) : 0u;
-      bq[k][1] = r4 < G ? __ldg(qrow + (16 * k + 8 + 2 * c4) / 2) : 0u;
-    }
-  }
-  float o[KSTEPS][4];
-#pragma unroll
-  for (int k = 0; k < KSTEPS; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // heads 2*c4, 2*c4+1
-
-  // per-thread ldmatrix geometry
-  const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8;  // K tile row fed by this lane
-  const int k_half = lane >> 4;                           // which 8-wide D half
-  const int v_tok = (lane & 7) + (lane >> 4) * 8;         // V tile token row fed by this lane
-  const int v_half = (lane >> 3) & 1;
-  const int x7 = lane & 7;                                // == row & 7 for both
-
+  HeadState<D> hs;
+  jenga_dev::pdl_wait();  // q and the workspace belong to the previous kernels until here
+  head_begin<T, D, G>(hs, p, b, h0 + hl, lane);
   for (int it = round; it < wk.t_count; it += ROUNDS) {
     const int st = it % NS;
     jenga_dev::mbar_wait(&full[st], (it / NS) & 1);
-    uint8_t* ks = smem + st * STAGE_BYTES + hl * TILE_BYTES;
-    uint8_t* vs = smem + st * STAGE_BYTES + (HG + hl) * TILE_BYTES;
-    const uint32_t ks_u = jenga_dev::smem_u32(ks), vs_u = jenga_dev::smem_u32(vs);
-    const int tok0 = (wk.t_begin + it) * kTile;
-
-    // ---- S^T = K . Q^T  (16 tokens x 8 heads, fp32)
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int k = 0; k < KSTEPS; ++k) {
-      const int chunk = 2 * k + k_half;
-      const uint32_t addr = ks_u + (chunk >> 3) * kBoxBytes + k_row * 128 + (((chunk & 7) ^ x7) << 4);
-      uint32_t a[4];
-      ldsm_x4(a, addr);
-      mma16816<T>(s, a, bq[k][0], bq[k][1]);
-    }
-    // ---- scale, soft-cap, mask (needs_token), online softmax
-    const int ta = tok0 + r4, tb = ta + 8;
-    const bool va = ta >= wk.lo && ta < wk.n, vb = tb >= wk.lo && tb < wk.n;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float x = s[i] * p.qscale;
-      if (p.cap_log2 > 0.f) x = p.cap_log2 * tanhf(x * p.inv_cap);
-      s[i] = x;
-    }
-    s[0] = va ? s[0] : -INFINITY;
-    s[1] = va ? s[1] : -INFINITY;
-    s[2] = vb ? s[2] : -INFINITY;
-    s[3] = vb ? s[3] : -INFINITY;
-    float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, off));
-      t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, off));
-    }
-    const float n0 = fmaxf(m0, t0), n1 = fmaxf(m1, t1);
-    const float a0 = n0 == -INFINITY ? 1.f : jenga_dev::fast_exp2(m0 - n0);
-    const float a1 = n1 == -INFINITY ? 1.f : jenga_dev::fast_exp2(m1 - n1);
-    m0 = n0;
-    m1 = n1;
-    const float p0 = va ? jenga_dev::fast_exp2(s[0] - n0) : 0.f;
-    const float p1 = va ? jenga_dev::fast_exp2(s[1] - n1) : 0.f;
-    const float p2 = vb ? jenga_dev::fast_exp2(s[2] - n0) : 0.f;
-    const float p3 = vb ? jenga_dev::fast_exp2(s[3] - n1) : 0.f;
-    l0 = l0 * a0 + p0 + p2;
-    l1 = l1 * a1 + p1 + p3;
-    if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
-#pragma unroll
-      for (int k = 0; k < KSTEPS; ++k) {
-        o[k][0] *= a0;
-        o[k][1] *= a1;
-        o[k][2] *= a0;
-        o[k][3] *= a1;
-      }
-    }
-    // P^T as the B operand of O^T += V^T P^T (k = tokens, n = heads)
-    const uint32_t pb0 = movm_trans(pack2<T>(p0, p1));
-    const uint32_t pb1 = movm_trans(pack2<T>(p2, p3));
-    // masked rows of a boundary tile may hold stale / non-finite bytes:
-    // zero this head's rows so 0 * V cannot produce NaN inside the MMA.
-    if (tok0 < wk.lo || tok0 + kTile > wk.n) {
-      for (int r = 0; r < kTile; ++r) {
-        const int t = tok0 + r;
-        if (t >= wk.lo && t < wk.n) continue;
-        for (int c = lane; c < NBOX * 8; c += 32)
-          *reinterpret_cast<uint4*>(vs + (c >> 3) * kBoxBytes + r * 128 + ((c & 7) << 4)) = make_uint4(0, 0, 0, 0);
-      }
-      // order these generic-proxy writes before the TMA refill of this stage
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-    }
-    // ---- O^T += V^T . P^T  (D x 8 heads)
-#pragma unroll
-    for (int k = 0; k < KSTEPS; ++k) {
-      const int chunk = 2 * k + v_half;
-      const uint32_t addr = vs_u + (chunk >> 3) * kBoxBytes + v_tok * 128 + (((chunk & 7) ^ x7) << 4);
-      uint32_t a[4];
-      ldsm_x4_trans(a, addr);
-      mma16816<T>(o[k], a, pb0, pb1);
-    }
+    uint8_t* stage = smem + st * STAGE_BYTES;
+    head_tile<T, D>(hs, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, (wk.t_begin + it) * kTile, wk.lo,
+                    wk.n, p, lane);
     __syncwarp();
     if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
   }
-
-  // -------------------------------------------------- per-warp state -> smem
-#pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
-  }
   consumers_sync();
-  float* s_acc = reinterpret_cast<float*>(smem);  // [4][G][D]
+  float* s_acc = reinterpret_cast<float*>(smem);  // [4][G][D] (the ring is drained)
   float* s_ml = s_acc + kConsumerWarps * G * D;   // [4][G][2]
-  const int q0 = 2 * c4, q1 = q0 + 1;             // query heads held by this lane
-#pragma unroll
-  for (int k = 0; k < KSTEPS; ++k) {
-    const int d = 16 * k + r4;
-    if (q0 < G) {
-      s_acc[(warp * G + q0) * D + d] = o[k][0];
-      s_acc[(warp * G + q0) * D + d + 8] = o[k][2];
-    }
-    if (q1 < G) {
-      s_acc[(warp * G + q1) * D + d] = o[k][1];
-      s_acc[(warp * G + q1) * D + d + 8] = o[k][3];
-    }
-  }
-  if (r4 == 0) {
-    if (q0 < G) {
-      s_ml[(warp * G + q0) * 2] = m0;
-      s_ml[(warp * G + q0) * 2 + 1] = l0;
-    }
-    if (q1 < G) {
-      s_ml[(warp * G + q1) * 2] = m1;
-      s_ml[(warp * G + q1) * 2 + 1] = l1;
-    }
-  }
+  head_store<D, G>(hs, s_acc, s_ml, warp, lane);
   merge_epilogue<T, G, D, HG>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h0);
+}
+
+// ------------------------------------------------------------ persistent kernel
+// gridDim.x CTAs (a few per SM) pull work items (request, head group, split)
+// from a global atomic queue.  The producer keeps streaming tiles across item
+// boundaries, so the TMA ring never drains between items and there is no
+// wave-quantisation tail; the consumers merge each item while the next one's
+// tiles are already landing.  Items are enumerated request by request from a
+// per-CTA prefix over the requests' split counts (needs batch <= kMaxPersistB).
+constexpr int kMaxPersistB = 2048;
+constexpr int kItemSlots = 4;
+
+struct ItemDesc {
+  int b, h0, split, n, lo, nsplit, t_begin, t_count, seq0, stop;
+};
+
+template <typename T, int D, int G, int HG, int NS>
+__global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
+    paged_decode_tc_persistent(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int TILE_BYTES = (D / kBoxCols) * kBoxBytes;
+  constexpr int STAGE_BYTES = 2 * HG * TILE_BYTES;
+  constexpr int ROUNDS = kConsumerWarps / HG;
+  constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
+  constexpr int RING = NS * STAGE_BYTES;
+  static_assert(NS % ROUNDS == 0, "slots must map to fixed consumer warps");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  float* s_acc = reinterpret_cast<float*>(smem + RING);     // separate from the ring:
+  float* s_ml = s_acc + kConsumerWarps * G * D;             // the producer keeps filling it
+  ItemDesc* items = reinterpret_cast<ItemDesc*>(smem + RING + MERGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(items + kItemSlots);
+  uint64_t* empty = full + NS;
+  uint64_t* item_full = empty + NS;
+  uint64_t* item_empty = item_full + kItemSlots;
+  int* s_flag = reinterpret_cast<int*>(item_empty + kItemSlots);
+  int* s_prefix = s_flag + 4;  // [batch + 1] item prefix over requests
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int groups = p.hkv / HG;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      jenga_dev::mbar_init(&full[i], 1);
+      jenga_dev::mbar_init(&empty[i], HG);
+    }
+    for (int i = 0; i < kItemSlots; ++i) {
+      jenga_dev::mbar_init(&item_full[i], 1);
+      jenga_dev::mbar_init(&item_empty[i], kConsumerWarps);
+    }
+    jenga_dev::fence_mbar_init();
+  }
+  if (warp == 0) {  // items per request -> exclusive prefix (one warp scan)
+    const int per = (p.batch + 31) / 32;
+    int local = 0;
+    for (int i = 0; i < per; ++i) {
+      const int bb = lane * per + i;
+      if (bb < p.batch) local += assign_work(p, bb, 0).nsplit * groups;
+    }
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    int run = incl - local;
+    for (int i = 0; i < per; ++i) {
+      const int bb = lane * per + i;
+      if (bb < p.batch) {
+        s_prefix[bb] = run;
+        run += assign_work(p, bb, 0).nsplit * groups;
+      }
+    }
+    if (lane == 31) s_prefix[p.batch] = incl;
+  }
+  __syncthreads();
+  const int total = s_prefix[p.batch];
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {  // producer: fetch items, stream their tiles
+      jenga_dev::prefetch_tmap(&tmap);
+      const uint64_t policy = jenga_dev::l2_policy_evict_first();
+      const int v_rows = p.hkv * p.tpp;
+      int seq = 0;
+      for (int ic = 0;; ++ic) {
+        const int j = ic % kItemSlots;
+        if (ic >= kItemSlots) jenga_dev::mbar_wait(&item_empty[j], ((ic / kItemSlots) & 1) ^ 1);
+        const int item = atomicAdd(&p.work[0], 1);
+        ItemDesc d{};
+        if (item >= total) {
+          d.stop = 1;
+          items[j] = d;
+          jenga_dev::mbar_arrive(&item_full[j]);
+          break;
+        }
+        int lo_b = 0, hi_b = p.batch - 1;  // last request with prefix <= item
+        while (lo_b < hi_b) {
+          const int mid = (lo_b + hi_b + 1) >> 1;
+          if (s_prefix[mid] <= item) lo_b = mid;
+          else hi_b = mid - 1;
+        }
+        const int r = item - s_prefix[lo_b];
+        d.b = lo_b;
+        d.split = r / groups;
+        d.h0 = (r % groups) * HG;
+        const Work wk = assign_work(p, d.b, d.split);
+        d.n = wk.n;
+        d.lo = wk.lo;
+        d.nsplit = wk.nsplit;
+        d.t_begin = wk.t_begin;
+        d.t_count = wk.t_count;
+        d.seq0 = seq;
+        items[j] = d;
+        jenga_dev::mbar_arrive(&item_full[j]);  // release: the descriptor is visible to its waiters
+        const int32_t* table = p.table + static_cast<int64_t>(d.b) * p.max_blocks;
+        for (int it = 0; it < d.t_count; ++it, ++seq) {
+          const int st = seq % NS;
+          if (seq >= NS) jenga_dev::mbar_wait(&empty[st], ((seq / NS) & 1) ^ 1);
+          const int tok0 = (d.t_begin + it) * kTile;
+          load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], tile_row(p, table, d.h0, tok0, D * 2), p.tpp,
+                            v_rows, policy);
+        }
+      }
+    }
+  } else {
+    const int hl = warp % HG;
+    const int round = warp / HG;
+    HeadState<D> hs;
+    for (int ic = 0;; ++ic) {
+      const int j = ic % kItemSlots;
+      jenga_dev::mbar_wait(&item_full[j], (ic / kItemSlots) & 1);
+      const ItemDesc d = items[j];
+      __syncwarp();
+      if (lane == 0) jenga_dev::mbar_arrive(&item_empty[j]);
+      if (d.stop) break;
+      head_begin<T, D, G>(hs, p, d.b, d.h0 + hl, lane);
+      // this warp owns the global tiles seq with seq % ROUNDS == round (NS % ROUNDS == 0,
+      // so every use of a slot is consumed by the same warps)
+      int it = (round - d.seq0 % ROUNDS + ROUNDS) % ROUNDS;
+      for (; it < d.t_count; it += ROUNDS) {
+        const int seq = d.seq0 + it;
+        const int st = seq % NS;
+        jenga_dev::mbar_wait(&full[st], (seq / NS) & 1);
+        uint8_t* stage = smem + st * STAGE_BYTES;
+        head_tile<T, D>(hs, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, (d.t_begin + it) * kTile, d.lo,
+                        d.n, p, lane);
+        __syncwarp();
+        if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
+      }
+      consumers_sync();  // the previous item's merge has finished reading s_acc
+      head_store<D, G>(hs, s_acc, s_ml, warp, lane);
+      merge_epilogue<T, G, D, HG>(p, s_acc, s_ml, s_flag, d.nsplit, d.split, d.b, d.h0);
+    }
+  }
+  // the last CTA out re-arms the queue for the next launch / graph replay
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&p.work[1], 1) == static_cast<int>(gridDim.x) - 1) {
+      p.work[0] = 0;
+      p.work[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------ host side
@@ -378,17 +585,55 @@ int tensor_map(const void* base, int D, int dtype, CUtensorMap* out) {
   return JENGA_OK;
 }
 
+int num_sms() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// Persistent scheduling only with JENGA_DECODE_PERSISTENT=1: measured slower
+// than three grid CTAs per SM on the bench shapes (profiles/r01_sweeps.md).
+bool use_persistent(int batch) {
+  static const int v = [] {
+    const char* e = std::getenv("JENGA_DECODE_PERSISTENT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0 && batch <= kMaxPersistB;
+}
+
 template <typename T, int D, int G, int HG>
 int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaStream_t stream) {
-  constexpr int NS = stages<D, HG>();
   constexpr int STAGE = 2 * HG * kTile * D * 2;
   constexpr int MERGE = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
+  constexpr int CTAS_PER_SM = HG >= 4 ? 1 : (HG == 2 ? 2 : 3);
+  if (use_persistent(batch)) {
+    // ring budget net of the separate merge area, a multiple of the rounds
+    constexpr int ROUNDS = kConsumerWarps / HG;
+    constexpr int BUDGET = ring_budget<HG>() - MERGE;
+    constexpr int NSR = (BUDGET / STAGE) / ROUNDS * ROUNDS;
+    constexpr int NS = NSR < ROUNDS ? ROUNDS : (NSR > 12 ? 12 : NSR);
+    const int smem = NS * STAGE + MERGE + kItemSlots * static_cast<int>(sizeof(ItemDesc)) +
+                     (2 * NS + 2 * kItemSlots) * 8 + 16 + (batch + 1) * 4 + 1024;
+    auto kern = paged_decode_tc_persistent<T, D, G, HG, NS>;
+    static std::atomic<uint64_t> configured{0};
+    if (int rc = configure_smem(kern, smem, configured)) return rc;
+    int per_sm = 0;  // resident CTAs per SM at this shared-memory size
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    kern<<<num_sms() * std::min(per_sm, CTAS_PER_SM), kThreads, smem, stream>>>(prm, tmap);
+    return jenga_dev::check_launch("paged_decode_tc_persistent");
+  }
+  constexpr int NS = stages<D, HG>();
   const int smem = std::max(NS * STAGE, MERGE) + 2 * NS * 8 + 16 + 1024;
   auto kern = paged_decode_tc_kernel<T, D, G, HG, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
   const dim3 grid = decode_grid(prm, batch, HG);
-  kern<<<grid, kThreads, smem, stream>>>(prm, tmap);
+  jenga_dev::launch_maybe_pdl(kern, grid, dim3(kThreads), smem, stream, prm, tmap);
   return jenga_dev::check_launch("paged_decode_tc_kernel");
 }
 

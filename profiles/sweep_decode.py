@@ -43,7 +43,8 @@ def one(batch=32, ctx=8192, iters=20):
     out = torch.empty_like(q)
     res = {"tiles_per_split": os.environ.get("JENGA_DECODE_TILES_PER_SPLIT", "default"), "layers": nl, "layer": layer,
            "prefetch": os.environ.get("JENGA_DECODE_PREFETCH", "0"),
-           "grid_order": os.environ.get("JENGA_DECODE_GRID_ORDER", "0"), "tpp": tpp, "hg": os.environ.get("JENGA_DECODE_HEADS_PER_CTA", "auto")}
+           "grid_order": os.environ.get("JENGA_DECODE_GRID_ORDER", "0"), "tpp": tpp, "hg": os.environ.get("JENGA_DECODE_HEADS_PER_CTA", "auto"),
+           "persistent": os.environ.get("JENGA_DECODE_PERSISTENT", "1")}
     bptl = 8192
     for g, name in ((0, "full"), (1, "swa")):
         live = int(eng.live_tokens(g).sum())
@@ -77,8 +78,9 @@ if __name__ == "__main__":
     if "--one" in sys.argv:
         one()
     else:
-        grid = [("1", "32"), ("2", "32"), ("4", "32"), ("4", "16"), ("4", "64"), ("2", "16")]
-        for hg, tps in grid:
+        grid = [("0", "1", "32"), ("1", "1", "32"), ("1", "1", "16"), ("1", "4", "16"), ("1", "4", "8"),
+                ("1", "2", "16"), ("1", "1", "64")]
+        for pers, hg, tps in grid:
             env = dict(os.environ, SWEEP_TPP="16", SWEEP_LAYERS="21", SWEEP_LAYER="0", JENGA_DECODE_HEADS_PER_CTA=hg,
-                       JENGA_DECODE_TILES_PER_SPLIT=tps)
+                       JENGA_DECODE_TILES_PER_SPLIT=tps, JENGA_DECODE_PERSISTENT=pers)
             subprocess.run([sys.executable, __file__, "--one"], env=env, check=False)
