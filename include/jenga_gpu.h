@@ -204,6 +204,29 @@ int jenga_pages_store(jenga_pages* pl, uint64_t request, int g, uint64_t pos,
                       uint64_t now_step);
 int jenga_pages_release(jenga_pages* pl, uint64_t request, int allow_cache,
                         uint64_t now_step);
+/* Admission with prefix caching (reference SimEngine::admit + KvAllocator::
+ * lookup_and_pin + adopt_lookup_result, simulator.cpp:435-452, 391-433,
+ * kv_allocator.cpp:241-303): install the prompt (n tokens; is_image and
+ * image_ordinals may be NULL), pin the longest cached prefix and splice its
+ * pages into the page lists.  *hit = prompt positions already resident. */
+int jenga_pages_admit(jenga_pages* pl, uint64_t request, const uint64_t* tokens,
+                      const uint8_t* is_image, const uint64_t* image_ordinals, uint64_t n,
+                      uint64_t now_step, uint64_t* hit);
+/* Chunked prefill of up to `budget` prompt positions (simulator.cpp:504-547).
+ * *consumed = positions stored; JENGA_ERR_OOM when an allocation failed. */
+int jenga_pages_prefill(jenga_pages* pl, uint64_t request, uint64_t budget, uint64_t now_step,
+                        uint64_t* consumed);
+/* Mamba restore after a prefix hit: the pinned checkpoint page of group g
+ * (*has=0 when none is pending).  The caller copies it into the working page
+ * (jenga_page_copy) and then calls jenga_pages_finish_restore, which returns
+ * the checkpoint to the cache — the reference instead leaks the pinned page
+ * (simulator.cpp:409-414). */
+int jenga_pages_restore_pending(const jenga_pages* pl, uint64_t request, int g, int* has,
+                                jenga_small_page* checkpoint);
+int jenga_pages_finish_restore(jenga_pages* pl, uint64_t request, int g, uint64_t now_step);
+int jenga_pages_set_fix_mamba_restore(jenga_pages* pl, int on);
+/* PrefixCache::entries (prefix_cache.hpp:71) */
+int jenga_kv_cache_entries(const jenga_kv* kv, int g, uint64_t* n);
 int jenga_pages_seq_len(const jenga_pages* pl, uint64_t request, uint64_t* len);
 /* Per-group state of one request. */
 int jenga_pages_group_state(const jenga_pages* pl, uint64_t request, int g,

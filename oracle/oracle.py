@@ -178,7 +178,9 @@ class RefLib:
             "ref_kv_fragmentation": [_p, _int, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)],
             "ref_kv_has_associated_empty": [_p, _int, _u64, C.POINTER(_int)],
             "ref_kv_check_invariants": [_p],
-            "ref_sim_create": [_p, _u64, _u64, _int, _int, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
+            "ref_sim_create": [_p, _u64, _u64, _int, _int, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
+            "ref_gen_multi_article": [_u32, _u32, _u64, _u64, _u64, _u64, _u64, _p, _p, _p, _p, _p, _int,
+                                      C.POINTER(_int)],
             "ref_sim_step": [_p, C.POINTER(_u32)],
             "ref_sim_done": [_p],
             "ref_sim_request": [_p, _u64, C.POINTER(_int), C.POINTER(_u64), C.POINTER(_u64)],
@@ -428,6 +430,24 @@ class RefPageLists:
         return o.value
 
 
+def multi_article_trace(ref: RefLib, articles=4, questions=3, article_tokens=4000, question_tokens=50,
+                        output_tokens=20, spacing=200, seed=0):
+    """The reference trace generator (trace.cpp:144-169) as request dicts."""
+    cap = articles * questions
+    ids = np.zeros(cap, np.uint64)
+    arr = np.zeros(cap, np.uint64)
+    outs = np.zeros(cap, np.uint64)
+    grp = np.zeros(cap, np.int32)
+    seg = np.zeros((cap, 2), np.uint64)
+    n = _int()
+    ref.check(ref.lib.ref_gen_multi_article(articles, questions, article_tokens, question_tokens, output_tokens,
+                                            spacing, seed, ids.ctypes.data_as(_p), arr.ctypes.data_as(_p),
+                                            outs.ctypes.data_as(_p), grp.ctypes.data_as(_p),
+                                            seg.ctypes.data_as(_p), cap, C.byref(n)))
+    return [{"id": int(ids[i]), "arrival": int(arr[i]), "output": int(outs[i]), "prefix_group": int(grp[i]),
+             "segments": [[0, int(seg[i, 0])], [0, int(seg[i, 1])]]} for i in range(n.value)]
+
+
 class RefSim:
     """The reference SimEngine (stepped), page lists read back via the shim."""
 
@@ -439,12 +459,13 @@ class RefSim:
         segc = np.array([len(r["segments"]) for r in requests], dtype=np.int32)
         segi = np.array([int(s[0]) for r in requests for s in r["segments"]] or [0], dtype=np.int32)
         segt = np.array([int(s[1]) for r in requests for s in r["segments"]] or [0], dtype=np.uint64)
-        self._keep = (ids, arr, outs, segc, segi, segt)
+        grp = np.array([r.get("prefix_group", -1) for r in requests], dtype=np.int32)
+        self._keep = (ids, arr, outs, segc, segi, segt, grp)
         self.h = _p()
         self.ref.check(self.L.ref_sim_create(spec.h, budget, chunk, 1 if prefix_caching else 0, len(ids),
                                              ids.ctypes.data_as(_p), arr.ctypes.data_as(_p), outs.ctypes.data_as(_p),
                                              segc.ctypes.data_as(_p), segi.ctypes.data_as(_p),
-                                             segt.ctypes.data_as(_p), C.byref(self.h)))
+                                             segt.ctypes.data_as(_p), grp.ctypes.data_as(_p), C.byref(self.h)))
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -33,6 +33,7 @@
 #include "jenga/memory_layout.hpp"
 #include "jenga/model_config.hpp"
 #include "jenga/simulator.hpp"
+#include "jenga/trace.hpp"
 #undef private
 
 #define EXPORT extern "C" __attribute__((visibility("default")))
@@ -267,7 +268,8 @@ EXPORT int ref_kv_check_invariants(void* kv) {
 // seg_count[r] segments for request r.
 EXPORT int ref_sim_create(void* s, uint64_t budget, uint64_t chunk, int prefix_caching, int n_req,
                           const uint64_t* ids, const uint64_t* arrival, const uint64_t* output_tokens,
-                          const int* seg_count, const int* seg_is_image, const uint64_t* seg_tokens, void** out) {
+                          const int* seg_count, const int* seg_is_image, const uint64_t* seg_tokens,
+                          const int* prefix_group, void** out) {
   return guarded([&] {
     EngineConfig cfg;
     cfg.memory_budget = budget;
@@ -280,10 +282,38 @@ EXPORT int ref_sim_create(void* s, uint64_t budget, uint64_t chunk, int prefix_c
       q.id = ids[r];
       q.arrival_step = arrival[r];
       q.output_tokens = output_tokens[r];
+      if (prefix_group && prefix_group[r] >= 0) q.prefix_group = "article-" + std::to_string(prefix_group[r]);
       for (int i = 0; i < seg_count[r]; ++i, ++k) q.segments.push_back(Segment{seg_is_image[k] != 0, seg_tokens[k]});
       tr.requests.push_back(q);
     }
     *out = new SimEngine(static_cast<Spec*>(s)->spec, cfg, tr);
+  });
+}
+// The reference multi-article prefix trace (trace.cpp:144-169), flattened:
+// per request id, arrival, output, prefix group index, and 2 text segments.
+EXPORT int ref_gen_multi_article(uint32_t articles, uint32_t questions, uint64_t article_tokens,
+                                 uint64_t question_tokens, uint64_t output_tokens, uint64_t spacing, uint64_t seed,
+                                 uint64_t* ids, uint64_t* arrival, uint64_t* out_tokens, int* group,
+                                 uint64_t* seg_tokens /* [n][2] */, int cap, int* n) {
+  return guarded([&] {
+    MultiArticleParams p;
+    p.num_articles = articles;
+    p.questions_per_article = questions;
+    p.article_tokens = article_tokens;
+    p.question_tokens = question_tokens;
+    p.output_tokens = output_tokens;
+    p.round_spacing_steps = spacing;
+    const Trace t = gen_multi_article_prefix(p, seed);
+    *n = static_cast<int>(t.requests.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+      const auto& r = t.requests[i];
+      ids[i] = r.id;
+      arrival[i] = r.arrival_step;
+      out_tokens[i] = r.output_tokens;
+      group[i] = std::stoi(r.prefix_group->substr(8));
+      seg_tokens[2 * i] = r.segments[0].tokens;
+      seg_tokens[2 * i + 1] = r.segments[1].tokens;
+    }
   });
 }
 EXPORT void ref_sim_destroy(void* e) { delete static_cast<SimEngine*>(e); }

@@ -122,6 +122,12 @@ _SIGS = {
     "jenga_pages_append_batch": (_int, [_p, _pu64, _int, _pu64, C.POINTER(C.c_uint8), _u64, _pint]),
     "jenga_pages_store": (_int, [_p, _u64, _int, _u64, _u64]),
     "jenga_pages_release": (_int, [_p, _u64, _int, _u64]),
+    "jenga_pages_admit": (_int, [_p, _u64, _pu64, C.POINTER(C.c_uint8), _pu64, _u64, _u64, _pu64]),
+    "jenga_pages_prefill": (_int, [_p, _u64, _u64, _u64, _pu64]),
+    "jenga_pages_restore_pending": (_int, [_p, _u64, _int, _pint, C.POINTER(SmallPage)]),
+    "jenga_pages_finish_restore": (_int, [_p, _u64, _int, _u64]),
+    "jenga_pages_set_fix_mamba_restore": (_int, [_p, _int]),
+    "jenga_kv_cache_entries": (_int, [_p, _int, _pu64]),
     "jenga_pages_seq_len": (_int, [_p, _u64, _pu64]),
     "jenga_pages_group_state": (_int, [_p, _u64, _int, _pu64, _pu64, _pu64, _pu64, _pint, C.POINTER(SmallPage)]),
     "jenga_pages_blocks": (_int, [_p, _u64, _int, C.POINTER(SmallPage), C.POINTER(C.c_uint8), _u64, _pu64]),

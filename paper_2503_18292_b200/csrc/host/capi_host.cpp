@@ -441,6 +441,59 @@ JENGA_EXPORT int jenga_pages_release(jenga_pages* pl, uint64_t request, int allo
   return guarded([&] { pl->pl->release(request, allow_cache != 0, now); });
 }
 
+JENGA_EXPORT int jenga_pages_admit(jenga_pages* pl, uint64_t request, const uint64_t* tokens,
+                                   const uint8_t* is_image, const uint64_t* image_ordinals, uint64_t n,
+                                   uint64_t now, uint64_t* hit) {
+  ARG_CHECK(pl != nullptr && (n == 0 || tokens != nullptr));
+  return guarded([&] {
+    std::vector<uint64_t> t(tokens, tokens + n);
+    std::vector<uint8_t> img = is_image ? std::vector<uint8_t>(is_image, is_image + n) : std::vector<uint8_t>();
+    std::vector<uint64_t> ord =
+        image_ordinals ? std::vector<uint64_t>(image_ordinals, image_ordinals + n) : std::vector<uint64_t>();
+    const uint64_t h = pl->pl->admit(request, t, img, ord, now);
+    if (hit) *hit = h;
+  });
+}
+
+JENGA_EXPORT int jenga_pages_prefill(jenga_pages* pl, uint64_t request, uint64_t budget, uint64_t now,
+                                     uint64_t* consumed) {
+  ARG_CHECK(pl != nullptr);
+  bool oom = false;
+  int rc = guarded([&] {
+    const uint64_t c = pl->pl->prefill(request, budget, now, &oom);
+    if (consumed) *consumed = c;
+  });
+  if (rc == JENGA_OK && oom) return fail(JENGA_ERR_OOM, "out of KV memory during prefill (preempt the request)");
+  return rc;
+}
+
+JENGA_EXPORT int jenga_pages_restore_pending(const jenga_pages* pl, uint64_t request, int g, int* has,
+                                             jenga_small_page* checkpoint) {
+  ARG_CHECK(pl != nullptr && has != nullptr && g >= 0);
+  return guarded([&] {
+    const auto& r = pl->pl->request(request);
+    *has = (static_cast<size_t>(g) < r.restore.size() && r.restore[g].has_value()) ? 1 : 0;
+    if (*has && checkpoint) *checkpoint = to_c(*r.restore[g]);
+  });
+}
+
+JENGA_EXPORT int jenga_pages_finish_restore(jenga_pages* pl, uint64_t request, int g, uint64_t now) {
+  ARG_CHECK(pl != nullptr && g >= 0);
+  return guarded([&] { pl->pl->finish_restore(request, static_cast<size_t>(g), now); });
+}
+
+JENGA_EXPORT int jenga_pages_set_fix_mamba_restore(jenga_pages* pl, int on) {
+  ARG_CHECK(pl != nullptr);
+  pl->pl->fix_mamba_restore = on != 0;
+  return JENGA_OK;
+}
+
+JENGA_EXPORT int jenga_kv_cache_entries(const jenga_kv* kv, int g, uint64_t* n) {
+  ARG_CHECK(kv != nullptr && n != nullptr);
+  GROUP_CHECK(kv, g);
+  return guarded([&] { *n = kv->kv->cache().entries(g); });
+}
+
 JENGA_EXPORT int jenga_pages_seq_len(const jenga_pages* pl, uint64_t request, uint64_t* len) {
   ARG_CHECK(pl != nullptr && len != nullptr);
   return guarded([&] { *len = pl->pl->request(request).tokens.size(); });

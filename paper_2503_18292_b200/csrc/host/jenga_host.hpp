@@ -274,6 +274,40 @@ class PrefixCache {
   std::vector<std::unordered_map<uint64_t, std::vector<Entry>>> by_group_;
 };
 
+// ---------------------------------------------------------------- prefix sets
+// Sorted disjoint inclusive ranges of valid prefix lengths (reference
+// range_set.hpp:14-39 semantics).
+class PrefixRangeSet {
+ public:
+  void append(uint64_t v) { append_range(v, v); }
+  void append_range(uint64_t lo, uint64_t hi);
+  bool contains(uint64_t v) const;
+  uint64_t max_value() const { return r_.empty() ? 0 : r_.back().second; }
+  static PrefixRangeSet intersect(const PrefixRangeSet& a, const PrefixRangeSet& b);
+  const std::vector<std::pair<uint64_t, uint64_t>>& ranges() const { return r_; }
+
+ private:
+  std::vector<std::pair<uint64_t, uint64_t>> r_;
+};
+
+// reference layer_policies.cpp:9-77
+std::vector<uint64_t> required_tokens(const LayerGroupSpec& g, uint64_t p, bool* defined);
+PrefixRangeSet possible_prefixes(const LayerGroupSpec& g, const std::vector<bool>& is_hit);
+// reference prefix_cache.cpp:25-57
+PrefixRangeSet stored_to_global_prefixes(const PrefixRangeSet& valid, const std::vector<uint64_t>& stored_positions,
+                                         uint64_t sequence_length);
+uint64_t find_longest_common_prefix(const std::vector<PrefixRangeSet>& per_group);
+
+struct GroupLookupInput {
+  std::vector<uint64_t> stored_positions;
+  std::vector<BlockContent> blocks;
+  std::vector<uint64_t> block_end_ordinal;
+};
+struct LookupResult {
+  uint64_t hit_length = 0;
+  std::vector<std::vector<std::pair<uint64_t, SmallPageId>>> pinned;  // per group (block, page)
+};
+
 // ---------------------------------------------------------------- engine
 struct AllocResult {
   SmallPageId page;
@@ -298,6 +332,9 @@ class KvAllocator {
   void free(size_t g, SmallPageId page, const std::optional<BlockContent>& cached);
   void pin(size_t g, SmallPageId page, uint64_t request);
   std::optional<LargePageId> evict_lru_large_page();
+  // reference kv_allocator.cpp:241-303
+  LookupResult lookup_and_pin(const std::vector<GroupLookupInput>& inputs, uint64_t sequence_length,
+                              uint64_t request);
   void set_request_aware(bool on) { request_aware_ = on; }
   uint64_t budget_bytes() const { return budget_; }
   const uint64_t* alloc_step_counts() const { return step_counts_; }
@@ -377,6 +414,12 @@ class PageLists {
     std::vector<uint64_t> image_ordinal;  // per position (image tokens only)
     std::vector<GroupRuntime> groups;
     bool needs_release = false;  // set by a failed (OOM) append
+    uint64_t prompt_len = 0;     // admit(): prefill target
+    uint64_t consumed = 0;       // admit(): prompt positions prefilled (hits included)
+    // Mamba checkpoint pages pinned by a prefix hit, per group: the state to
+    // copy into the working page before decoding resumes (the reference pins
+    // them and never adopts them, simulator.cpp:409-414).
+    std::vector<std::optional<SmallPageId>> restore;
   };
 
   void add_request(uint64_t id);
@@ -391,8 +434,25 @@ class PageLists {
   const Request& request(uint64_t id) const;
   bool group_stores_position(size_t g, const Request& r, uint64_t pos) const;
 
+  // Admission (reference simulator.cpp:435-452): install the prompt and, with
+  // prefix caching, pin and adopt the longest cached prefix.  Returns the hit
+  // length (prompt positions already resident).
+  uint64_t admit(uint64_t id, const std::vector<uint64_t>& tokens, const std::vector<uint8_t>& is_image,
+                 const std::vector<uint64_t>& image_ordinals, uint64_t now);
+  // Chunked prefill of up to `budget` positions (reference simulator.cpp:
+  // 504-547, vision-embedding groups excluded).  Returns positions consumed;
+  // *oom set when an allocation failed.
+  uint64_t prefill(uint64_t id, uint64_t budget, uint64_t now, bool* oom);
+  // reference simulator.cpp:347-358
+  void refresh_mamba_checkpoints(uint64_t id, uint64_t now);
+  // The Mamba restore fix: forget (and free) a pinned checkpoint page once
+  // the caller has copied it into the working page.
+  void finish_restore(uint64_t id, size_t g, uint64_t now);
+  bool fix_mamba_restore = true;  // false: keep the reference's pinned-page leak
+
  private:
   Request& req(uint64_t id);
+  std::vector<GroupLookupInput> build_lookup_inputs(const Request& r) const;
   void append_chain(Request& r, size_t g);
   void free_block(Request& r, size_t g, uint64_t b, bool allow_cache, uint64_t now);
 

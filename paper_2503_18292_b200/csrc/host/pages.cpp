@@ -1,6 +1,8 @@
 // Per-request page lists: the producer of every block table.  Semantics are
 // those of the reference simulator's GroupRuntime bookkeeping (cited per
 // method); scheduling, metrics and preemption policy stay with the caller.
+#include <algorithm>
+
 #include "jenga_host.hpp"
 
 namespace jenga {
@@ -16,6 +18,7 @@ void PageLists::add_request(uint64_t id) {
   Request r;
   r.id = id;
   r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  r.restore.assign(kv_->num_groups(), std::nullopt);
   requests_.push_back(std::move(r));
 }
 
@@ -143,6 +146,7 @@ void PageLists::free_block(Request& r, size_t g, uint64_t b, bool allow_cache, u
 // are driven separately by the caller (jenga_pages_store).
 bool PageLists::append(uint64_t id, uint64_t token, bool is_image, uint64_t image_ordinal,
                        uint64_t now) {
+  refresh_mamba_checkpoints(id, now);  // decode_one, simulator.cpp:551
   Request& r = req(id);
   JENGA_CHECK(!r.needs_release, "append after OOM: release (preempt) the request first");
   r.tokens.push_back(token);
@@ -165,10 +169,139 @@ bool PageLists::append(uint64_t id, uint64_t token, bool is_image, uint64_t imag
   return true;
 }
 
+// reference simulator.cpp:360-389
+std::vector<GroupLookupInput> PageLists::build_lookup_inputs(const Request& r) const {
+  std::vector<GroupLookupInput> inputs(kv_->num_groups());
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    GroupLookupInput& in = inputs[g];
+    const LayerGroupSpec& grp = kv_->group(g);
+    for (uint64_t pos = 1; pos <= r.prompt_len; ++pos)
+      if (group_stores_position(g, r, pos)) in.stored_positions.push_back(pos);
+    if (grp.kind == LayerKind::kVisionEmbedding) continue;  // never cached
+    const uint64_t t = grp.kind == LayerKind::kMamba ? grp.checkpoint_interval_tokens : grp.tokens_per_page;
+    const uint64_t full_blocks = in.stored_positions.size() / t;
+    uint64_t parent = block_chain_salt(grp.name);
+    for (uint64_t b = 0; b < full_blocks; ++b) {
+      BlockContent c;
+      c.parent_key = parent;
+      c.tokens.reserve(t);
+      for (uint64_t i = 0; i < t; ++i) c.tokens.push_back(r.tokens[in.stored_positions[b * t + i] - 1]);
+      c.key = chain_block_key(c.parent_key, c.tokens);
+      parent = c.key;
+      in.blocks.push_back(std::move(c));
+      in.block_end_ordinal.push_back((b + 1) * t);
+    }
+  }
+  return inputs;
+}
+
+// reference simulator.cpp:435-452 (admit) + 391-433 (adopt_lookup_result)
+uint64_t PageLists::admit(uint64_t id, const std::vector<uint64_t>& tokens, const std::vector<uint8_t>& is_image,
+                          const std::vector<uint64_t>& image_ordinals, uint64_t now) {
+  (void)now;
+  Request& r = req(id);
+  JENGA_CHECK(is_image.empty() || is_image.size() == tokens.size(), "is_image length mismatch");
+  r.tokens = tokens;
+  r.is_image = is_image.empty() ? std::vector<uint8_t>(tokens.size(), 0) : is_image;
+  r.image_ordinal = image_ordinals.size() == tokens.size() ? image_ordinals : std::vector<uint64_t>(tokens.size(), 0);
+  r.prompt_len = tokens.size();
+  r.consumed = 0;
+  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  r.restore.assign(kv_->num_groups(), std::nullopt);
+  r.needs_release = false;
+  if (!prefix_caching_) return 0;
+  const auto inputs = build_lookup_inputs(r);
+  const LookupResult res = kv_->lookup_and_pin(inputs, r.prompt_len, id);
+  const uint64_t hit = res.hit_length;
+  if (hit == 0) return 0;
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    GroupRuntime& rt = r.groups[g];
+    const GroupLookupInput& in = inputs[g];
+    const LayerGroupSpec& grp = kv_->group(g);
+    const uint64_t m = static_cast<uint64_t>(
+        std::upper_bound(in.stored_positions.begin(), in.stored_positions.end(), hit) - in.stored_positions.begin());
+    if (grp.kind == LayerKind::kVisionEmbedding) continue;
+    rt.stored = m;
+    rt.stored_positions.assign(in.stored_positions.begin(), in.stored_positions.begin() + m);
+    if (grp.kind == LayerKind::kMamba) {
+      const uint64_t k = grp.checkpoint_interval_tokens;
+      JENGA_CHECK(m % k == 0, "mamba hit not on a checkpoint boundary");
+      rt.checkpoints = m / k;
+      rt.chain.assign(in.blocks.begin(), in.blocks.begin() + rt.checkpoints);
+      // The checkpoint page lookup_and_pin pinned: the state to restore.
+      if (fix_mamba_restore && !res.pinned[g].empty()) r.restore[g] = res.pinned[g].back().second;
+      continue;
+    }
+    const uint64_t t = grp.tokens_per_page;
+    const uint64_t covering = (m + t - 1) / t;
+    rt.blocks.assign(covering, Block{});
+    rt.chain.assign(in.blocks.begin(), in.blocks.begin() + std::min<uint64_t>(covering, in.blocks.size()));
+    for (const auto& [b, page] : res.pinned[g]) {
+      JENGA_CHECK(b < covering, "pinned block beyond hit prefix");
+      rt.blocks[b] = Block{page, true};
+      rt.live_blocks++;
+      rt.held_tokens += std::min(m, (b + 1) * t) - b * t;
+    }
+    while (rt.freed_blocks < rt.blocks.size() && !rt.blocks[rt.freed_blocks].live) rt.freed_blocks++;
+  }
+  r.consumed = hit;
+  return hit;
+}
+
+// reference simulator.cpp:504-547 (text path)
+uint64_t PageLists::prefill(uint64_t id, uint64_t budget, uint64_t now, bool* oom) {
+  Request& r = req(id);
+  if (oom) *oom = false;
+  uint64_t done = 0;
+  while (done < budget && r.consumed < r.prompt_len) {
+    const uint64_t pos = r.consumed + 1;
+    for (size_t g = 0; g < kv_->num_groups(); ++g) {
+      if (kv_->group(g).kind == LayerKind::kVisionEmbedding) continue;
+      if (!group_stores_position(g, r, pos)) continue;
+      const GroupRuntime& rt = r.groups[g];
+      if (!rt.stored_positions.empty() && pos <= rt.stored_positions.back()) continue;  // pinned block
+      if (!store_position(id, g, pos, now)) {
+        r.needs_release = true;
+        if (oom) *oom = true;
+        return done;
+      }
+    }
+    r.consumed++;
+    done++;
+  }
+  refresh_mamba_checkpoints(id, now);
+  return done;
+}
+
+// reference simulator.cpp:347-358
+void PageLists::refresh_mamba_checkpoints(uint64_t id, uint64_t now) {
+  if (!prefix_caching_) return;
+  Request& r = req(id);
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    if (kv_->group(g).kind != LayerKind::kMamba) continue;
+    GroupRuntime& rt = r.groups[g];
+    if (rt.checkpoints == 0 || rt.chain.size() < rt.checkpoints) continue;
+    auto page = kv_->cache().find(g, rt.chain[rt.checkpoints - 1]);
+    if (page.has_value()) kv_->type_allocator(g).touch(*page, now);
+  }
+}
+
+void PageLists::finish_restore(uint64_t id, size_t g, uint64_t now) {
+  Request& r = req(id);
+  JENGA_CHECK(g < r.restore.size() && r.restore[g].has_value(), "no pending Mamba restore");
+  GroupRuntime& rt = r.groups[g];
+  JENGA_CHECK(rt.checkpoints >= 1 && rt.chain.size() >= rt.checkpoints, "restore without a checkpoint chain");
+  const SmallPageId page = *r.restore[g];
+  kv_->type_allocator(g).touch(page, now);
+  kv_->free(g, page, rt.chain[rt.checkpoints - 1]);  // back to the cache as the same checkpoint
+  r.restore[g].reset();
+}
+
 // reference simulator.cpp:314-327
 void PageLists::release(uint64_t id, bool allow_cache, uint64_t now) {
   Request& r = req(id);
   for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    if (g < r.restore.size() && r.restore[g].has_value()) finish_restore(id, g, now);
     GroupRuntime& rt = r.groups[g];
     for (uint64_t b = 0; b < rt.blocks.size(); ++b)
       if (rt.blocks[b].live) free_block(r, g, b, allow_cache && prefix_caching_, now);

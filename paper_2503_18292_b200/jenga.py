@@ -343,6 +343,11 @@ class KvAllocator:
         check(lib.jenga_kv_group_counts(self.h, g, C.byref(u), C.byref(e), C.byref(m), C.byref(o)))
         return {"used": u.value, "evictable": e.value, "empty": m.value, "owned_units": o.value}
 
+    def cache_entries(self, g: int) -> int:
+        n = C.c_uint64()
+        check(lib.jenga_kv_cache_entries(self.h, g, C.byref(n)))
+        return n.value
+
     def pool_free_pages(self) -> int:
         n = C.c_uint32()
         check(lib.jenga_kv_pool_free_pages(self.h, C.byref(n)))
@@ -411,6 +416,39 @@ class PageLists:
 
     def release(self, request: int, allow_cache: bool = False, now: int = 0) -> None:
         check(lib.jenga_pages_release(self.h, request, 1 if allow_cache else 0, now))
+
+    def admit(self, request: int, tokens, is_image=None, image_ordinals=None, now: int = 0) -> int:
+        """Install the prompt; with prefix caching pin + adopt the longest cached
+        prefix (reference admit / lookup_and_pin / adopt_lookup_result). Returns the hit."""
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint64))
+        img = None if is_image is None else np.ascontiguousarray(np.asarray(is_image, dtype=np.uint8))
+        ordn = None if image_ordinals is None else np.ascontiguousarray(np.asarray(image_ordinals, dtype=np.uint64))
+        hit = C.c_uint64()
+        check(lib.jenga_pages_admit(self.h, request, t.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                    None if img is None else img.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    None if ordn is None else ordn.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                    len(t), now, C.byref(hit)))
+        return hit.value
+
+    def prefill(self, request: int, budget: int, now: int = 0):
+        """Store up to `budget` prompt positions. Returns (consumed, oom)."""
+        c = C.c_uint64()
+        rc = lib.jenga_pages_prefill(self.h, request, budget, now, C.byref(c))
+        if rc == _lib.JENGA_ERR_OOM:
+            return c.value, True
+        check(rc)
+        return c.value, False
+
+    def restore_pending(self, request: int, g: int):
+        has, page = C.c_int(), _lib.SmallPage()
+        check(lib.jenga_pages_restore_pending(self.h, request, g, C.byref(has), C.byref(page)))
+        return SmallPageId(page.large, page.slot) if has.value else None
+
+    def finish_restore(self, request: int, g: int, now: int = 0) -> None:
+        check(lib.jenga_pages_finish_restore(self.h, request, g, now))
+
+    def set_fix_mamba_restore(self, on: bool) -> None:
+        check(lib.jenga_pages_set_fix_mamba_restore(self.h, 1 if on else 0))
 
     def seq_len(self, request: int) -> int:
         n = C.c_uint64()

@@ -26,7 +26,7 @@ ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
 from oracle import ref_lib  # noqa: E402
-from oracle.oracle import RefSim  # noqa: E402
+from oracle.oracle import RefKv, RefSim  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 REF_CONFIGS = Path("/root/reference/proj/configs")
@@ -229,13 +229,71 @@ def sim_pages(ref):
     return out
 
 
+PREFIX_MODELS = {
+    "window": spec_json("win", [
+        {"name": "self", "kind": "full", "num_layers": 2, "bytes_per_token_per_layer": 64, "tokens_per_page": 4},
+        {"name": "window", "kind": "sliding_window", "num_layers": 3, "bytes_per_token_per_layer": 64,
+         "window_tokens": 24, "tokens_per_page": 4}]),
+    "hybrid": spec_json("hyb", [
+        {"name": "attn", "kind": "full", "num_layers": 2, "bytes_per_token_per_layer": 64, "tokens_per_page": 2},
+        {"name": "ssm", "kind": "mamba", "num_layers": 3, "bytes_per_token_per_layer": 256,
+         "checkpoint_interval_tokens": 16}]),
+}
+
+
+def sim_prefix(ref):
+    """Reference SimEngine with prefix caching on its multi-article trace
+    (trace.cpp:144-169): later rounds hit the cached article prefixes."""
+    from oracle.oracle import multi_article_trace
+    out = []
+    for model, budget, chunk, params in (
+            ("window", 8 << 20, 48, dict(articles=3, questions=3, article_tokens=90, question_tokens=9,
+                                         output_tokens=6, spacing=12, seed=3)),
+            ("window", 96 * 1024, 32, dict(articles=3, questions=4, article_tokens=60, question_tokens=7,
+                                           output_tokens=5, spacing=9, seed=4)),
+            ("hybrid", 8 << 20, 40, dict(articles=2, questions=3, article_tokens=64, question_tokens=8,
+                                         output_tokens=5, spacing=10, seed=5))):
+        reqs = multi_article_trace(ref, **params)
+        s = ref.spec(PREFIX_MODELS[model])
+        sim = RefSim(s, budget, chunk, True, reqs)
+        ng = len(json.loads(PREFIX_MODELS[model])["groups"])
+        snaps = []
+        step = 0
+        ref_error = None
+        while not sim.done() and step < 400:
+            try:
+                sim.step()
+            except Exception as e:  # the reference's Mamba prefix-hit leak (SURVEY §4b)
+                ref_error = str(e)
+                break
+            step += 1
+            snap = {"step": step, "requests": []}
+            for r in reqs:
+                rq = sim.request(r["id"])
+                groups = []
+                for g in range(ng):
+                    st = sim.group_state(r["id"], g)
+                    groups.append({"pages": st["pages"].tolist(), "live": st["live"].astype(int).tolist(),
+                                   "stored": st["stored"], "freed": st["freed"],
+                                   "working": None if st["working"] is None else [int(x) for x in st["working"]]})
+                snap["requests"].append({"id": r["id"], "phase": rq["phase"], "consumed": rq["consumed"],
+                                         "groups": groups})
+            snaps.append(snap)
+        kv = RefKv(s, budget, handle=sim.L.ref_sim_allocator(sim.h))
+        final = [kv.counts(g) for g in range(ng)]
+        out.append({"model": model, "spec": json.loads(PREFIX_MODELS[model]), "budget": budget, "chunk": chunk,
+                    "requests": reqs, "snapshots": snaps, "final_counts": final, "done": sim.done(),
+                    "reference_error": ref_error})
+    return out
+
+
 def main():
     ref = ref_lib()
     if ref is None:
         raise SystemExit("reference library unavailable: build oracle/_ref first (oracle/build_oracle.py)")
     for name, fn in (("fig6.json", fig6), ("configs.json", configs), ("random_geometries.json", random_geometries),
                      ("alloc_sequences.json", alloc_sequences), ("policies.json", policies),
-                     ("sim_pages.json", sim_pages)):
+                     ("sim_pages.json", sim_pages), ("sim_prefix.json", sim_prefix)):
         data = fn(ref)
         with open(OUT / name, "w") as f:
             json.dump(data, f, separators=(",", ":"))
