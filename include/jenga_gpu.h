@@ -225,6 +225,12 @@ int jenga_pages_restore_pending(const jenga_pages* pl, uint64_t request, int g, 
                                 jenga_small_page* checkpoint);
 int jenga_pages_finish_restore(jenga_pages* pl, uint64_t request, int g, uint64_t now_step);
 int jenga_pages_set_fix_mamba_restore(jenga_pages* pl, int on);
+/* Defer sliding-window frees across a prefill chunk (the reference's
+ * suppress_window_free, simulator.cpp:466-500): while on, stored positions
+ * never free out-of-window blocks; apply performs the pending frees once the
+ * chunk's attention has run. */
+int jenga_pages_set_defer_window_free(jenga_pages* pl, uint64_t request, int on);
+int jenga_pages_apply_window_free(jenga_pages* pl, uint64_t request, uint64_t now_step);
 /* PrefixCache::entries (prefix_cache.hpp:71) */
 int jenga_kv_cache_entries(const jenga_kv* kv, int g, uint64_t* n);
 int jenga_pages_seq_len(const jenga_pages* pl, uint64_t request, uint64_t* len);
@@ -303,6 +309,19 @@ int jenga_paged_decode(void* arena_base, jenga_layer_view view, int kind, int dt
                        int num_kv_heads, int head_dim, uint32_t tokens_per_page,
                        float scale, float softcap, void* workspace, size_t workspace_bytes,
                        void* stream);
+
+/* Chunked-prefill paged attention (bf16/fp16, tokens_per_page % 16 == 0):
+ * request b's queries are q[cu_q[b] .. cu_q[b+1]) — its newest ordinals
+ * (0-based positions seq_lens[b]-C_b .. seq_lens[b]-1), whose K/V were already
+ * written with jenga_reshape_and_cache.  Causal (+ window for SWA); cross
+ * attention attends all seq_lens[b] image keys.  q/out [total_tokens][Hq][D];
+ * max_chunk = max C_b.  arena_base must come from jenga_arena_create. */
+int jenga_paged_prefill(void* arena_base, jenga_layer_view view, int kind, int dtype,
+                        uint64_t window, const void* q, void* out, const int32_t* cu_q,
+                        int total_tokens, int max_chunk, const int32_t* block_table,
+                        const int32_t* seq_lens, int batch, int max_blocks, int num_q_heads,
+                        int num_kv_heads, int head_dim, uint32_t tokens_per_page, float scale,
+                        float softcap, void* stream);
 
 /* Mamba last-token state (one working page per request, tpp=1):
  * gather dense[B][exec_page_size] <- arena slice; scatter the reverse

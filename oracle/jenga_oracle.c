@@ -292,6 +292,62 @@ int orc_paged_decode(const uint8_t* arena, uint64_t start_offset, uint64_t page_
   return a.rc;
 }
 
+/* Chunked prefill attention (reference prefill_some, simulator.cpp:504-547,
+ * stores the chunk's positions): request b owns query
+ * tokens [cu_q[b], cu_q[b+1]) which are its newest C_b ordinals, i.e. 0-based
+ * positions n_b - C_b .. n_b - 1 with n_b = seq_lens[b].  Query position i
+ * attends key j iff j <= i (causal) and, for sliding windows, j + W > i
+ * (needs_token at length i+1, layer_policies.cpp:105-120); cross attention
+ * attends all n_b keys.  q/out [T][Hq][D], out fp64. */
+int orc_paged_prefill(const uint8_t* arena, uint64_t start_offset, uint64_t page_stride, int kind, int dtype,
+                      int64_t window, const uint8_t* q, double* out, const int32_t* cu_q, const int32_t* table,
+                      const int32_t* seq_lens, int batch, int max_blocks, int hq, int hkv, int d, int tpp,
+                      double scale, double softcap) {
+  if (hkv <= 0 || hq % hkv || tpp <= 0) return ORC_ERR_CONFIG;
+  const int e = dtype_size(dtype), G = hq / hkv;
+  const int64_t row = (int64_t)d * e;
+  for (int b = 0; b < batch; ++b) {
+    const int n = seq_lens[b], c = cu_q[b + 1] - cu_q[b];
+    if (c > n && kind != ORC_CROSS) return ORC_ERR_INVARIANT;
+    double* s = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int t = 0; t < c; ++t) {
+      const int i = n - c + t;  /* 0-based position of this query */
+      int lo = 0, hi = i;       /* inclusive key range */
+      if (kind == ORC_CROSS) hi = n - 1;
+      if (kind == ORC_SWA && i + 1 > window) lo = (int)(i + 1 - window);
+      for (int qh = 0; qh < hq; ++qh) {
+        const int h = qh / G;
+        const uint8_t* qp = q + ((int64_t)(cu_q[b] + t) * hq + qh) * row;
+        double* op = out + ((int64_t)(cu_q[b] + t) * hq + qh) * d;
+        for (int x = 0; x < d; ++x) op[x] = 0.0;
+        double m = -INFINITY;
+        for (int j = lo; j <= hi; ++j) {
+          const int32_t page = table[(int64_t)b * max_blocks + j / tpp];
+          if (page < 0) { free(s); return ORC_ERR_INVARIANT; }
+          const uint8_t* kp = arena + start_offset + (int64_t)page * page_stride + slice_row(0, h, hkv, tpp, j % tpp) * row;
+          double dot = 0.0;
+          for (int x = 0; x < d; ++x) dot += ld_elem(qp + x * e, dtype) * ld_elem(kp + x * e, dtype);
+          dot *= scale;
+          if (softcap > 0.0) dot = softcap * tanh(dot / softcap);
+          s[j] = dot;
+          if (dot > m) m = dot;
+        }
+        double l = 0.0;
+        for (int j = lo; j <= hi; ++j) {
+          const double p = exp(s[j] - m);
+          l += p;
+          const int32_t page = table[(int64_t)b * max_blocks + j / tpp];
+          const uint8_t* vp = arena + start_offset + (int64_t)page * page_stride + slice_row(1, h, hkv, tpp, j % tpp) * row;
+          for (int x = 0; x < d; ++x) op[x] += p * ld_elem(vp + x * e, dtype);
+        }
+        if (l > 0) for (int x = 0; x < d; ++x) op[x] /= l;
+      }
+    }
+    free(s);
+  }
+  return ORC_OK;
+}
+
 /* Mamba last-token state (simulator.cpp:222-244: one working page per
  * request; the layer's slice is exec_page_size bytes at start+global*stride). */
 int orc_mamba_gather(const uint8_t* arena, uint64_t start_offset, uint64_t page_stride, uint64_t exec_bytes,

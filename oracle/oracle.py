@@ -42,6 +42,8 @@ class COracle:
         L.orc_reshape_and_cache.argtypes = [_p, _u64, _u64, _int, _int, _int, _int, _p, _p, _i64, _p, _int]
         L.orc_paged_decode.argtypes = [_p, _u64, _u64, _int, _int, _i64, _p, _p, _p, _p, _int, _int, _int, _int,
                                        _int, _int, _dbl, _dbl, _int]
+        L.orc_paged_prefill.argtypes = [_p, _u64, _u64, _int, _int, _i64, _p, _p, _p, _p, _p, _int, _int, _int,
+                                        _int, _int, _int, _dbl, _dbl]
         L.orc_mamba_gather.argtypes = [_p, _u64, _u64, _u64, _p, _int, _p]
         L.orc_mamba_scatter.argtypes = [_p, _u64, _u64, _u64, _p, _int, _p]
         L.orc_page_copy.argtypes = [_p, _u64, _p, _p, _int]
@@ -114,6 +116,18 @@ class COracle:
                                            q.ctypes.data_as(_p), out.ctypes.data_as(_p), tp, sp, batch,
                                            table.shape[1], hq, hkv, d, tpp, float(scale), float(softcap),
                                            int(nthreads)))
+        return out
+
+    def paged_prefill(self, arena: np.ndarray, view, kind, dtype, window, q: np.ndarray, cu_q, table, seq_lens, hq,
+                      hkv, d, tpp, scale, softcap=0.0) -> np.ndarray:
+        cu, cp = _np(cu_q, np.int32)
+        table, tp = _np(table, np.int32)
+        seq_lens, sp = _np(seq_lens, np.int32)
+        q = np.ascontiguousarray(q)
+        out = np.zeros((int(cu[-1]), hq, d), dtype=np.float64)
+        self._ok(self.lib.orc_paged_prefill(arena.ctypes.data_as(_p), view[0], view[1], kind, dtype, int(window),
+                                            q.ctypes.data_as(_p), out.ctypes.data_as(_p), cp, tp, sp, table.shape[0],
+                                            table.shape[1], hq, hkv, d, tpp, float(scale), float(softcap)))
         return out
 
     def mamba_gather(self, arena, view, page_globals, batch):

@@ -127,6 +127,8 @@ _SIGS = {
     "jenga_pages_restore_pending": (_int, [_p, _u64, _int, _pint, C.POINTER(SmallPage)]),
     "jenga_pages_finish_restore": (_int, [_p, _u64, _int, _u64]),
     "jenga_pages_set_fix_mamba_restore": (_int, [_p, _int]),
+    "jenga_pages_set_defer_window_free": (_int, [_p, _u64, _int]),
+    "jenga_pages_apply_window_free": (_int, [_p, _u64, _u64]),
     "jenga_kv_cache_entries": (_int, [_p, _int, _pu64]),
     "jenga_pages_seq_len": (_int, [_p, _u64, _pu64]),
     "jenga_pages_group_state": (_int, [_p, _u64, _int, _pu64, _pu64, _pu64, _pu64, _pint, C.POINTER(SmallPage)]),
@@ -142,6 +144,8 @@ _SIGS = {
     "jenga_paged_decode_workspace_size": (C.c_size_t, [_int, _int, _int, _int, _int, _u32]),
     "jenga_paged_decode": (_int, [_p, LayerViewC, _int, _int, _u64, _p, _p, _p, _p, _int, _int, _int, _int, _int,
                                   _u32, C.c_float, C.c_float, _p, C.c_size_t, _p]),
+    "jenga_paged_prefill": (_int, [_p, LayerViewC, _int, _int, _u64, _p, _p, _p, _int, _int, _p, _p, _int, _int,
+                                   _int, _int, _int, _u32, C.c_float, C.c_float, _p]),
     "jenga_mamba_state_gather": (_int, [_p, LayerViewC, _p, _int, _p, _p]),
     "jenga_mamba_state_scatter": (_int, [_p, LayerViewC, _p, _int, _p, _p]),
     "jenga_page_copy": (_int, [_p, _u64, _p, _p, _int, _p]),

@@ -488,6 +488,16 @@ JENGA_EXPORT int jenga_pages_set_fix_mamba_restore(jenga_pages* pl, int on) {
   return JENGA_OK;
 }
 
+JENGA_EXPORT int jenga_pages_set_defer_window_free(jenga_pages* pl, uint64_t request, int on) {
+  ARG_CHECK(pl != nullptr);
+  return guarded([&] { pl->pl->set_defer_window_free(request, on != 0); });
+}
+
+JENGA_EXPORT int jenga_pages_apply_window_free(jenga_pages* pl, uint64_t request, uint64_t now) {
+  ARG_CHECK(pl != nullptr);
+  return guarded([&] { pl->pl->apply_window_free(request, now); });
+}
+
 JENGA_EXPORT int jenga_kv_cache_entries(const jenga_kv* kv, int g, uint64_t* n) {
   ARG_CHECK(kv != nullptr && n != nullptr);
   GROUP_CHECK(kv, g);

@@ -420,6 +420,10 @@ class PageLists {
     // copy into the working page before decoding resumes (the reference pins
     // them and never adopts them, simulator.cpp:409-414).
     std::vector<std::optional<SmallPageId>> restore;
+    // Defer sliding-window frees while a prefill chunk's attention still
+    // needs keys that left the window (the reference's suppress_window_free,
+    // simulator.cpp:466-500); apply_window_free() performs them.
+    bool defer_window_free = false;
   };
 
   void add_request(uint64_t id);
@@ -448,6 +452,9 @@ class PageLists {
   // The Mamba restore fix: forget (and free) a pinned checkpoint page once
   // the caller has copied it into the working page.
   void finish_restore(uint64_t id, size_t g, uint64_t now);
+  void set_defer_window_free(uint64_t id, bool on) { req(id).defer_window_free = on; }
+  // reference finish_prefill's deferred frees (simulator.cpp:484-500)
+  void apply_window_free(uint64_t id, uint64_t now);
   bool fix_mamba_restore = true;  // false: keep the reference's pinned-page leak
 
  private:

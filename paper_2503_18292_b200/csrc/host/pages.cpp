@@ -113,7 +113,7 @@ bool PageLists::store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now
   const uint64_t ordinal_value = grp.stores_image_tokens() ? r.image_ordinal[pos - 1] : pos;
   ta.set_prefix_length(rt.blocks[bidx].page, ordinal_value);
 
-  if (grp.kind == LayerKind::kSlidingWindow) {
+  if (grp.kind == LayerKind::kSlidingWindow && !r.defer_window_free) {
     const uint64_t w = grp.window_tokens;
     if (rt.stored > w) {
       const uint64_t exited = rt.stored - w;
@@ -283,6 +283,19 @@ void PageLists::refresh_mamba_checkpoints(uint64_t id, uint64_t now) {
     if (rt.checkpoints == 0 || rt.chain.size() < rt.checkpoints) continue;
     auto page = kv_->cache().find(g, rt.chain[rt.checkpoints - 1]);
     if (page.has_value()) kv_->type_allocator(g).touch(*page, now);
+  }
+}
+
+void PageLists::apply_window_free(uint64_t id, uint64_t now) {
+  Request& r = req(id);
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    const LayerGroupSpec& grp = kv_->group(g);
+    if (grp.kind != LayerKind::kSlidingWindow) continue;
+    GroupRuntime& rt = r.groups[g];
+    if (rt.stored <= grp.window_tokens) continue;
+    const uint64_t t = grp.tokens_per_page;
+    const uint64_t exited = rt.stored - grp.window_tokens;
+    while (rt.freed_blocks * t + t <= exited) free_block(r, g, rt.freed_blocks, true, now);
   }
 }
 

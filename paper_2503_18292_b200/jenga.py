@@ -450,6 +450,12 @@ class PageLists:
     def set_fix_mamba_restore(self, on: bool) -> None:
         check(lib.jenga_pages_set_fix_mamba_restore(self.h, 1 if on else 0))
 
+    def set_defer_window_free(self, request: int, on: bool) -> None:
+        check(lib.jenga_pages_set_defer_window_free(self.h, request, 1 if on else 0))
+
+    def apply_window_free(self, request: int, now: int = 0) -> None:
+        check(lib.jenga_pages_apply_window_free(self.h, request, now))
+
     def seq_len(self, request: int) -> int:
         n = C.c_uint64()
         check(lib.jenga_pages_seq_len(self.h, request, C.byref(n)))

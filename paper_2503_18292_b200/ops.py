@@ -136,6 +136,25 @@ def paged_decode(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out:
     return out
 
 
+def paged_prefill(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out: torch.Tensor, cu_q: torch.Tensor,
+                  max_chunk: int, block_table: torch.Tensor, seq_lens: torch.Tensor, num_kv_heads: int,
+                  tokens_per_page: int, scale: float, window: int = 0, softcap: float = 0.0) -> torch.Tensor:
+    """Chunked-prefill attention: q/out [T, Hq, D] (bf16/fp16), cu_q int32 [B+1]."""
+    T, hq, d = q.shape
+    _need(out, q.dtype, "out")
+    _need(cu_q, torch.int32, "cu_q")
+    _need(block_table, torch.int32, "block_table")
+    _need(seq_lens, torch.int32, "seq_lens")
+    if not q.is_contiguous():
+        raise ValueError("q must be contiguous")
+    B = cu_q.numel() - 1
+    check(lib.jenga_paged_prefill(arena.base, view.c(), int(kind), DTYPE_CODE[q.dtype], int(window), _ptr(q),
+                                  _ptr(out), _ptr(cu_q), T, int(max_chunk), _ptr(block_table), _ptr(seq_lens), B,
+                                  block_table.shape[-1], hq, num_kv_heads, d, tokens_per_page, float(scale),
+                                  float(softcap), _stream()))
+    return out
+
+
 def mamba_state_gather(arena: Arena, view: LayerView, page_globals: torch.Tensor, dense: torch.Tensor) -> None:
     _need(page_globals, torch.int64, "page_globals")
     check(lib.jenga_mamba_state_gather(arena.base, view.c(), _ptr(page_globals), page_globals.numel(),

@@ -15,7 +15,8 @@ ORC_DTYPE = {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}
 TOL = {torch.float32: 1e-5, torch.bfloat16: 1e-2, torch.float16: 5e-3}
 
 
-def make_engine(geom: ModelGeometry, lens, seed=0, headroom_pages=8, poison=True, image_flags=None):
+def make_engine(geom: ModelGeometry, lens, seed=0, headroom_pages=8, poison=True, image_flags=None,
+                defer_window=False):
     """Append tokens (interleaved, seeded order per 16-position chunk) until
     each request reaches lens[r]; returns the engine with tables synced."""
     spec = geom.spec()
@@ -35,6 +36,9 @@ def make_engine(geom: ModelGeometry, lens, seed=0, headroom_pages=8, poison=True
         eng.arena.tensor().fill_(0xFF)  # NaN in every float format: masked rows must never leak
     ids = list(range(100, 100 + len(lens)))
     eng.add_requests(ids)
+    if defer_window:  # prefill chunks: keep out-of-window blocks until attention ran
+        for r in ids:
+            eng.pages.set_defer_window_free(r, True)
     rng = np.random.default_rng(seed)
     cur = [0] * len(lens)
     pos = 0
@@ -56,15 +60,18 @@ def make_engine(geom: ModelGeometry, lens, seed=0, headroom_pages=8, poison=True
     return eng, ids
 
 
-def fill_group_kv(eng: DecodeEngine, g: int, layers, seed=0):
-    """Write random K/V for every stored ordinal of group g through the product
-    slot_mapping + reshape_and_cache kernels.  Returns (req, ord, K, V, slots)."""
+def fill_group_kv(eng: DecodeEngine, g: int, layers, seed=0, all_live=False):
+    """Write random K/V for every live stored ordinal of group g through the
+    product slot_mapping + reshape_and_cache kernels (SWA: the window only,
+    unless all_live).  Returns (req, ord, K, V, slots)."""
     t = eng.tables[g]
     gg = t.geom
     B = len(eng.requests)
     n = t.h_n_stored[:B].numpy().astype(np.int64)
     lo = np.zeros(B, dtype=np.int64)
-    if gg.window:
+    if all_live:
+        lo = t.h_first_live[:B].numpy().astype(np.int64) * eng.spec.groups[g].tokens_per_page
+    elif gg.window:
         lo = np.maximum(0, n - gg.window)
     req = np.concatenate([np.full(n[b] - lo[b], b, dtype=np.int32) for b in range(B)]) if n.sum() else \
         np.zeros(0, np.int32)

@@ -212,3 +212,26 @@ def test_interleaved_workload_matches_reference_allocator(ref):
             assert [lv for _, lv in blocks] == live.tolist()
     kv.check_invariants()
     rkv.check_invariants()
+
+
+def test_deferred_window_free_then_apply():
+    """After the chunk's attention the deferred SWA frees leave exactly the
+    pages decode keeps (reference finish_prefill, simulator.cpp:484-500)."""
+    from paper_2503_18292_b200 import LayerGroupSpec
+    spec = ModelSpec("w", [LayerGroupSpec("win", LayerKind.kSlidingWindow, 1, 64, tokens_per_page=4,
+                                          window_tokens=10)])
+    a = KvAllocator(spec, 1 << 20)
+    pa = PageLists(a)
+    b = KvAllocator(spec, 1 << 20)
+    pb = PageLists(b)
+    for pl in (pa, pb):
+        pl.add_request(1)
+    pa.set_defer_window_free(1, True)
+    for _ in range(37):
+        pa.append(1)
+        pb.append(1)
+    assert sum(lv for _, lv in pa.blocks(1, 0)) == 10 and pa.group_state(1, 0)["freed_blocks"] == 0
+    pa.apply_window_free(1)
+    pa.set_defer_window_free(1, False)
+    assert [lv for _, lv in pa.blocks(1, 0)] == [lv for _, lv in pb.blocks(1, 0)]
+    a.check_invariants()
