@@ -30,6 +30,13 @@ namespace jenga_dev {
 bool arena_extent(const void* base, uint64_t* bytes);
 }
 
+namespace jenga_decode {
+int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_stride, void* out, const int32_t* cu_q,
+                       const int32_t* table, const int32_t* seq_lens, int kind, int64_t window, int max_blocks,
+                       int hq, int hkv, int tpp, int q_blocks_128, float qscale, float cap_log2, float inv_cap,
+                       int dtype, int head_dim, int batch, int total_tokens, const void* q, cudaStream_t s);
+}
+
 namespace {
 
 using namespace jenga_decode;
@@ -442,6 +449,11 @@ JENGA_EXPORT int jenga_paged_prefill(void* arena_base, jenga_layer_view view, in
     prm.qscale = scale * kLog2e;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int rc = jenga_decode::launch_prefill_tc5(arena_base, prm.start_offset, prm.page_stride, out, cu_q,
+                                                  block_table, seq_lens, kind, prm.window, max_blocks, num_q_heads,
+                                                  num_kv_heads, prm.tpp, prm.q_blocks, prm.qscale, prm.cap_log2,
+                                                  prm.inv_cap, dtype, head_dim, batch, total_tokens, q, s);
+  if (rc != JENGA_ERR_UNSUPPORTED) return rc;
   if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, batch, total_tokens, q, s);
   return dispatch_d<__half>(head_dim, G, prm, dtype, batch, total_tokens, q, s);
 }

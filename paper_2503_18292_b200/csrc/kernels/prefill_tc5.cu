@@ -1,0 +1,533 @@
+// Chunked-prefill paged attention on the 5th-generation tensor cores
+// (tcgen05.mma + TMEM), bf16/fp16.  Same contract as prefill.cu (which keeps
+// the mma.sync path for comparison, JENGA_PREFILL_TC5=0).
+//
+// One CTA = (128 query rows, KV head, request); rows are (token, query head)
+// pairs r = t*G + g as in prefill.cu.  Six warps:
+//   warps 0-3  softmax / correction / epilogue: thread r owns query row r,
+//              i.e. TMEM lane r of the S and O accumulators (32x32b loads);
+//              scores are masked with the reference liveness rule
+//              (layer_policies.cpp:105-120), exponentiated against a lazily
+//              updated row max (O is rescaled in TMEM only when the max grows
+//              by more than 2^8), and P is written to shared memory in the
+//              128-byte-swizzled K-major layout the MMA reads.
+//   warp 4     TMA producer: the Q block once (3-D box), then KT-token K/V
+//              tiles of the paged arena (2-D boxes, one per page piece).
+//   warp 5     MMA issuer (one elected thread) and TMEM owner:
+//                S[j%2]  = Q . K_j^T   M=128, N=KT, K=D   (A, B K-major)
+//                O      += P_j . V_j    M=128, N=D,  K=KT  (B MN-major)
+//              software-pipelined: S_{j+1} is issued before O += P_j V_j;
+//              tcgen05.commit releases K/V stages and P buffers.
+// TMEM: O in columns [0, D), S double buffer after it (512 allocated).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "decode_common.cuh"
+
+namespace jenga_dev {
+bool arena_extent(const void* base, uint64_t* bytes);
+}
+
+namespace {
+
+using namespace jenga_decode;
+
+constexpr int kRows = 128;
+constexpr int kSoftWarps = 4;
+constexpr int kProducerWarp = 4;
+constexpr int kMmaWarp = 5;
+constexpr int kT5Threads = 6 * 32;
+constexpr int kBoxCols = 64;
+constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescales
+
+struct Prefill5Params {
+  const uint8_t* arena;
+  uint64_t start_offset, page_stride;
+  void* out;
+  const int32_t* cu_q;
+  const int32_t* table;
+  const int32_t* seq_lens;
+  int kind;
+  int64_t window;
+  int max_blocks, hq, hkv, tpp, q_blocks;
+  float qscale, cap_log2, inv_cap;
+};
+
+// ---------------------------------------------------------------- tcgen05
+__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  // sm100 shared-memory matrix descriptor, 128-byte swizzle (layout type 2),
+  // version 1; addresses / offsets in 16-byte units.
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // version
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: f32 accumulate, bf16 (1) or f16 (0)
+// inputs, A K-major, B K-major (b_mn = 0) or MN-major (1), M x N.
+template <typename T>
+__device__ __forceinline__ uint32_t idesc_f16(int m, int n, int b_mn) {
+  const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(b_mn) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   jenga_dev::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(addr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  } else {
+    __half2 v = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int32_t c0, int32_t c1, int32_t c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(jenga_dev::smem_u32(bar))
+      : "memory");
+}
+
+// D = head_dim, G = query heads per KV head, KT = KV tokens per tile.
+template <typename T, int D, int G, int KT, int NS>
+__global__ void __launch_bounds__(kT5Threads, 1)
+    paged_prefill_tc5_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap kv_map,
+                             const __grid_constant__ CUtensorMap q_map) {
+  constexpr int NBOX = D / kBoxCols;          // 64-column chunks of head_dim
+  constexpr int QB = kRows / G;               // tokens per query block
+  constexpr int Q_CHUNK = kRows * 128;        // one 64-col chunk of Q (K-major atom column)
+  constexpr int KV_CHUNK = KT * 128;          // one 64-col chunk of a K or V tile
+  constexpr int KV_BYTES = NBOX * KV_CHUNK;   // K (or V) of one tile, one head
+  constexpr int STAGE = 2 * KV_BYTES;
+  constexpr int P_BYTES = kRows * 128;        // P buffer: 128 rows x 128-byte line
+  constexpr int PIECES = KT / kTile;          // 16-row TMA boxes per tile chunk
+  constexpr uint32_t TMEM_COLS = D + 2 * KT <= 256 ? 256 : 512;  // power of two >= O + S columns
+  constexpr int S_COL = D;                    // S double buffer after O
+  static_assert(KT == 32 || KT == 64, "KV tile is 32 or 64 tokens");
+  static_assert(D + 2 * KT <= 512, "TMEM budget");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* qs = smem;
+  uint8_t* ring = qs + NBOX * Q_CHUNK;
+  uint8_t* pbuf = ring + NS * STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + 2 * P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + NS;
+  uint64_t* s_full = kv_empty + NS;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* p_empty = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
+  const int t0 = qb * QB;
+  if (t0 >= c_len) return;
+  const int n = p.seq_lens[b];
+  const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
+  const int pos0 = n - c_len + t0;
+  const int pos1 = n - c_len + min(t0 + QB, c_len) - 1;
+  int key_lo = 0;
+  const int key_hi = cross ? n - 1 : pos1;
+  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
+  const int tile_lo = key_lo / KT;
+  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    jenga_dev::mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      jenga_dev::mbar_init(&kv_full[i], 1);
+      jenga_dev::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      jenga_dev::mbar_init(&s_full[i], 1);
+      jenga_dev::mbar_init(&s_empty[i], kSoftWarps);
+      jenga_dev::mbar_init(&p_full[i], kSoftWarps);
+      jenga_dev::mbar_init(&p_empty[i], 1);
+    }
+    jenga_dev::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     jenga_dev::smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
+
+  if (warp == kProducerWarp) {
+    if (lane == 0) {
+      jenga_dev::prefetch_tmap(&kv_map);
+      jenga_dev::prefetch_tmap(&q_map);
+      jenga_dev::mbar_arrive_expect_tx(q_full, NBOX * Q_CHUNK);
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx) tma_load_3d(qs + bx * Q_CHUNK, &q_map, bx * kBoxCols, h * G, p.cu_q[b] + t0, q_full);
+      const uint64_t policy = jenga_dev::l2_policy_evict_first();
+      const int64_t row_bytes = D * 2;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * p.tpp;
+      const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+      const int v_rows = p.hkv * p.tpp;
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j % NS;
+        if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+        uint8_t* ks = ring + st * STAGE;
+        jenga_dev::mbar_arrive_expect_tx(&kv_full[st], STAGE);
+        for (int pc = 0; pc < PIECES; ++pc) {
+          const int tok = (tile_lo + j) * KT + pc * kTile;
+          const int32_t page = table[min(tok / p.tpp, p.max_blocks - 1)];
+          const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows +
+                                                   tok % p.tpp);
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx) {
+            jenga_dev::tma_load_2d(ks + bx * KV_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols, row, &kv_full[st],
+                                   policy);
+            jenga_dev::tma_load_2d(ks + KV_BYTES + bx * KV_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols,
+                                   row + v_rows, &kv_full[st], policy);
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      const uint32_t id_s = idesc_f16<T>(kRows, KT, 0);
+      const uint32_t id_o = idesc_f16<T>(kRows, D, 1);
+      const uint32_t qs_u = jenga_dev::smem_u32(qs);
+      auto issue_pv = [&](int jj) {
+        const int sb = jj & 1;
+        jenga_dev::mbar_wait(&p_full[sb], (jj >> 1) & 1);
+        tc_fence_after();
+        const uint32_t p_u = jenga_dev::smem_u32(pbuf + sb * P_BYTES);
+        const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < KT / 16; ++k) {
+          const uint64_t da = umma_desc(p_u + k * 32, 16, 1024);                 // P [128][KT] K-major
+          const uint64_t db = umma_desc(v_u + k * 16 * 128, KV_CHUNK, 1024);     // V [KT][D] MN-major
+          umma(tmem, da, db, id_o, (jj > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&p_empty[sb]);          // P buffer free, O updated
+        umma_commit(&kv_empty[jj % NS]);    // K/V stage free
+      };
+      jenga_dev::mbar_wait(q_full, 0);
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j % NS, sb = j & 1;
+        jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
+        if (j >= 2) jenga_dev::mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint64_t da = umma_desc(qs_u + (k >> 2) * Q_CHUNK + (k & 3) * 32, 16, 1024);   // Q [128][D]
+          const uint64_t db = umma_desc(k_u + (k >> 2) * KV_CHUNK + (k & 3) * 32, 16, 1024);   // K [KT][D]
+          umma(tmem + S_COL + sb * KT, da, db, id_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[sb]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      if (ntiles > 0) issue_pv(ntiles - 1);
+    }
+  } else {
+    // ------------------------------------------ softmax / correction warps
+    const int r = threadIdx.x;  // query row == TMEM lane
+    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+    const int tok = t0 + r / G;
+    const bool row_ok = tok < c_len;
+    const int ipos = n - c_len + tok;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int sb = j & 1;
+      const int ktok0 = (tile_lo + j) * KT;
+      jenga_dev::mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s[KT];
+#pragma unroll
+      for (int c = 0; c < KT; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + lane_addr + S_COL + sb * KT + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c + i] = v[i];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) jenga_dev::mbar_arrive(&s_empty[sb]);
+      float mt = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        const int key = ktok0 + i;
+        bool ok = row_ok && key >= key_lo && key <= (cross ? n - 1 : ipos);
+        if (p.kind == JENGA_KIND_SLIDING_WINDOW) ok = ok && key + p.window > ipos;
+        float x = s[i] * p.qscale;
+        if (p.cap_log2 > 0.f) x = p.cap_log2 * tanhf(x * p.inv_cap);
+        s[i] = ok ? x : -INFINITY;
+        mt = fmaxf(mt, s[i]);
+      }
+      // Grow the reference max only when it moved by > 2^8 (P stays <= 256);
+      // tcgen05.ld/st are warp-collective, so the warp rescales together.
+      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+        const float m_new = fmaxf(m_used, mt);
+        if (j >= 1) {  // O holds P_0..P_{j-1} V: wait for the last PV, rescale rows
+          const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
+          jenga_dev::mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + c, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= alpha;
+            tmem_st32(tmem + lane_addr + c, v);
+          }
+          tc_fence_before();
+          l *= alpha;
+        }
+        m_used = m_new;
+      }
+      uint32_t pk[KT / 2];
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < KT; i += 2) {
+        const float a = s[i] == -INFINITY ? 0.f : jenga_dev::fast_exp2(s[i] - m_used);
+        const float bb = s[i + 1] == -INFINITY ? 0.f : jenga_dev::fast_exp2(s[i + 1] - m_used);
+        rs += a + bb;
+        pk[i / 2] = pack2<T>(a, bb);
+      }
+      l += rs;
+      if (j >= 2) jenga_dev::mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);  // P buffer free (PV_{j-2} done)
+      // P row r -> 128-byte line r of the K-major SW128 P buffer
+      uint8_t* prow = pbuf + sb * P_BYTES + r * 128;
+#pragma unroll
+      for (int c = 0; c < KT / 8; ++c)
+        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      // masked keys of a boundary tile may hold non-finite V bytes (0*NaN = NaN
+      // in the MMA): zero those V rows; 128 threads cover KT rows x NBOX chunks
+      if (ktok0 < key_lo || ktok0 + KT - 1 > key_hi) {
+        uint8_t* vs = ring + (j % NS) * STAGE + KV_BYTES;
+        for (int idx = r; idx < KT * NBOX; idx += kRows) {
+          const int vrow = idx % KT, chunk = idx / KT;
+          const int key = ktok0 + vrow;
+          if (key >= key_lo && key <= key_hi) continue;
+          uint4* line = reinterpret_cast<uint4*>(vs + chunk * KV_CHUNK + vrow * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) jenga_dev::mbar_arrive(&p_full[sb]);
+    }
+    // ---- epilogue: O / l -> out
+    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      float v[32];
+      if (ntiles > 0) {
+        tmem_ld32(tmem + lane_addr + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
+                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
+                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
+                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+template <typename T, int D, int G>
+int launch_tc5(const Prefill5Params& prm, int dtype, int batch, int total_tokens, const void* q, cudaStream_t s) {
+  constexpr int KT = D >= 256 ? 32 : 64;
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int NS = D >= 256 ? 3 : 2;
+  const int smem = NBOX * kRows * 128 + NS * 2 * NBOX * KT * 128 + 2 * kRows * 128 + (1 + 2 * NS + 8) * 8 + 16 + 1024;
+  auto fn = encode_fn();
+  if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  uint64_t bytes = 0;
+  if (!jenga_dev::arena_extent(prm.arena, &bytes))
+    return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_prefill: arena_base must come from jenga_arena_create");
+  const CUtensorMapDataType dt =
+      dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap kv_map, q_map;
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / (D * 2)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+    cuuint32_t box[2] = {kBoxCols, kTile};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&kv_map, dt, 2, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
+  }
+  {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(prm.hq),
+                          static_cast<cuuint64_t>(total_tokens)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(prm.hq) * D * 2};
+    cuuint32_t box[3] = {kBoxCols, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(kRows / G)};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (fn(&q_map, dt, 3, const_cast<void*>(q), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: Q tensor map encode failed");
+  }
+  auto kern = paged_prefill_tc5_kernel<T, D, G, KT, NS>;
+  static std::atomic<uint64_t> configured{0};
+  if (int rc = configure_smem(kern, smem, configured)) return rc;
+  dim3 grid(prm.q_blocks, prm.hkv, batch);
+  kern<<<grid, kT5Threads, smem, s>>>(prm, kv_map, q_map);
+  return jenga_dev::check_launch("paged_prefill_tc5_kernel");
+}
+
+template <typename T, int D>
+int dispatch_g(int G, const Prefill5Params& prm, int dtype, int batch, int total, const void* q, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_tc5<T, D, 1>(prm, dtype, batch, total, q, s);
+    case 2: return launch_tc5<T, D, 2>(prm, dtype, batch, total, q, s);
+    case 4: return launch_tc5<T, D, 4>(prm, dtype, batch, total, q, s);
+    case 8: return launch_tc5<T, D, 8>(prm, dtype, batch, total, q, s);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+namespace jenga_decode {
+
+// Prefill on tcgen05; JENGA_ERR_UNSUPPORTED lets the caller use prefill.cu.
+int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_stride, void* out, const int32_t* cu_q,
+                       const int32_t* table, const int32_t* seq_lens, int kind, int64_t window, int max_blocks,
+                       int hq, int hkv, int tpp, int q_blocks_128, float qscale, float cap_log2, float inv_cap,
+                       int dtype, int head_dim, int batch, int total_tokens, const void* q, cudaStream_t s) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("JENGA_PREFILL_TC5");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (!enabled || (head_dim != 64 && head_dim != 128 && head_dim != 256)) return JENGA_ERR_UNSUPPORTED;
+  Prefill5Params prm{};
+  prm.arena = static_cast<const uint8_t*>(arena);
+  prm.start_offset = start_offset;
+  prm.page_stride = page_stride;
+  prm.out = out;
+  prm.cu_q = cu_q;
+  prm.table = table;
+  prm.seq_lens = seq_lens;
+  prm.kind = kind;
+  prm.window = window;
+  prm.max_blocks = max_blocks;
+  prm.hq = hq;
+  prm.hkv = hkv;
+  prm.tpp = tpp;
+  prm.q_blocks = q_blocks_128;
+  prm.qscale = qscale;
+  prm.cap_log2 = cap_log2;
+  prm.inv_cap = inv_cap;
+  const int G = hq / hkv;
+  if (dtype == JENGA_BF16) {
+    switch (head_dim) {
+      case 64: return dispatch_g<__nv_bfloat16, 64>(G, prm, dtype, batch, total_tokens, q, s);
+      case 128: return dispatch_g<__nv_bfloat16, 128>(G, prm, dtype, batch, total_tokens, q, s);
+      case 256: return dispatch_g<__nv_bfloat16, 256>(G, prm, dtype, batch, total_tokens, q, s);
+    }
+  } else {
+    switch (head_dim) {
+      case 64: return dispatch_g<__half, 64>(G, prm, dtype, batch, total_tokens, q, s);
+      case 128: return dispatch_g<__half, 128>(G, prm, dtype, batch, total_tokens, q, s);
+      case 256: return dispatch_g<__half, 256>(G, prm, dtype, batch, total_tokens, q, s);
+    }
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+}  // namespace jenga_decode

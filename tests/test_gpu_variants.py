@@ -22,3 +22,11 @@ def test_decode_variants_parity(env):
                         "-k", "gemma or decode_shapes or cross or toy"],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_prefill_mma_sync_variant_parity():
+    """JENGA_PREFILL_TC5=0 selects the mma.sync prefill kernel (prefill.cu)."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", str(ROOT / "tests" / "test_gpu_prefill.py")],
+                       env=dict(os.environ, JENGA_PREFILL_TC5="0"), capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
