@@ -298,6 +298,15 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     const int tok = t0 + r / G;
     const bool row_ok = tok < c_len;
     const int ipos = n - c_len + tok;
+    // row r attends keys [lo_r, hi_r] (empty range for padding rows)
+    int lo_r = 0, hi_r = cross ? n - 1 : ipos;
+    if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
+      lo_r = static_cast<int>(ipos + 1 - p.window);
+    if (!row_ok || hi_r < lo_r) lo_r = hi_r = 1 << 30;
+    const uint32_t span = static_cast<uint32_t>(hi_r - lo_r);
+    const bool softcap = p.cap_log2 > 0.f;
+    const float sc = softcap ? 1.f : p.qscale;  // scores -> log2 domain
+    const float qi = p.qscale * p.inv_cap;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
       const int sb = j & 1;
@@ -315,17 +324,19 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) jenga_dev::mbar_arrive(&s_empty[sb]);
+      if (softcap) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
+      }
+      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {  // boundary tile for this row
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
+      }
       float mt = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < KT; ++i) {
-        const int key = ktok0 + i;
-        bool ok = row_ok && key >= key_lo && key <= (cross ? n - 1 : ipos);
-        if (p.kind == JENGA_KIND_SLIDING_WINDOW) ok = ok && key + p.window > ipos;
-        float x = s[i] * p.qscale;
-        if (p.cap_log2 > 0.f) x = p.cap_log2 * tanhf(x * p.inv_cap);
-        s[i] = ok ? x : -INFINITY;
-        mt = fmaxf(mt, s[i]);
-      }
+      for (int i = 0; i < KT; ++i) mt = fmaxf(mt, s[i]);
+      mt *= sc;
       // Grow the reference max only when it moved by > 2^8 (P stays <= 256);
       // tcgen05.ld/st are warp-collective, so the warp rescales together.
       if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
@@ -348,15 +359,17 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         m_used = m_new;
       }
       uint32_t pk[KT / 2];
-      float rs = 0.f;
+      float rs0 = 0.f, rs1 = 0.f;
+      const float neg = m_used == -INFINITY ? 0.f : -m_used;  // masked: exp2(-inf) = 0
 #pragma unroll
       for (int i = 0; i < KT; i += 2) {
-        const float a = s[i] == -INFINITY ? 0.f : jenga_dev::fast_exp2(s[i] - m_used);
-        const float bb = s[i + 1] == -INFINITY ? 0.f : jenga_dev::fast_exp2(s[i + 1] - m_used);
-        rs += a + bb;
+        const float a = jenga_dev::fast_exp2(fmaf(s[i], sc, neg));
+        const float bb = jenga_dev::fast_exp2(fmaf(s[i + 1], sc, neg));
+        rs0 += a;
+        rs1 += bb;
         pk[i / 2] = pack2<T>(a, bb);
       }
-      l += rs;
+      l += rs0 + rs1;
       if (j >= 2) jenga_dev::mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);  // P buffer free (PV_{j-2} done)
       // P row r -> 128-byte line r of the K-major SW128 P buffer
       uint8_t* prow = pbuf + sb * P_BYTES + r * 128;
@@ -427,11 +440,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <typename T, int D, int G>
+template <typename T, int D, int G, int KT, int NS>
 int launch_tc5(const Prefill5Params& prm, int dtype, int batch, int total_tokens, const void* q, cudaStream_t s) {
-  constexpr int KT = D >= 256 ? 32 : 64;
   constexpr int NBOX = D / kBoxCols;
-  constexpr int NS = D >= 256 ? 3 : 2;
   const int smem = NBOX * kRows * 128 + NS * 2 * NBOX * KT * 128 + 2 * kRows * 128 + (1 + 2 * NS + 8) * 8 + 16 + 1024;
   auto fn = encode_fn();
   if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -470,13 +481,32 @@ int launch_tc5(const Prefill5Params& prm, int dtype, int batch, int total_tokens
   return jenga_dev::check_launch("paged_prefill_tc5_kernel");
 }
 
-template <typename T, int D>
+template <typename T, int D, int KT, int NS>
 int dispatch_g(int G, const Prefill5Params& prm, int dtype, int batch, int total, const void* q, cudaStream_t s) {
   switch (G) {
-    case 1: return launch_tc5<T, D, 1>(prm, dtype, batch, total, q, s);
-    case 2: return launch_tc5<T, D, 2>(prm, dtype, batch, total, q, s);
-    case 4: return launch_tc5<T, D, 4>(prm, dtype, batch, total, q, s);
-    case 8: return launch_tc5<T, D, 8>(prm, dtype, batch, total, q, s);
+    case 1: return launch_tc5<T, D, 1, KT, NS>(prm, dtype, batch, total, q, s);
+    case 2: return launch_tc5<T, D, 2, KT, NS>(prm, dtype, batch, total, q, s);
+    case 4: return launch_tc5<T, D, 4, KT, NS>(prm, dtype, batch, total, q, s);
+    case 8: return launch_tc5<T, D, 8, KT, NS>(prm, dtype, batch, total, q, s);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+template <typename T>
+int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, int batch, int total, const void* q,
+               cudaStream_t s) {
+  // KV tile: 64 tokens (32 for head_dim 256 unless JENGA_PREFILL_KT=64, which
+  // leaves room for only two 64 KB stages)
+  static const int kt256 = [] {
+    const char* e = std::getenv("JENGA_PREFILL_KT");
+    return e != nullptr && std::atoi(e) == 64 ? 64 : 32;
+  }();
+  switch (D) {
+    case 64: return dispatch_g<T, 64, 64, 2>(G, prm, dtype, batch, total, q, s);
+    case 128: return dispatch_g<T, 128, 64, 2>(G, prm, dtype, batch, total, q, s);
+    case 256:
+      return kt256 == 64 ? dispatch_g<T, 256, 64, 2>(G, prm, dtype, batch, total, q, s)
+                         : dispatch_g<T, 256, 32, 3>(G, prm, dtype, batch, total, q, s);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
@@ -514,20 +544,8 @@ int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_s
   prm.cap_log2 = cap_log2;
   prm.inv_cap = inv_cap;
   const int G = hq / hkv;
-  if (dtype == JENGA_BF16) {
-    switch (head_dim) {
-      case 64: return dispatch_g<__nv_bfloat16, 64>(G, prm, dtype, batch, total_tokens, q, s);
-      case 128: return dispatch_g<__nv_bfloat16, 128>(G, prm, dtype, batch, total_tokens, q, s);
-      case 256: return dispatch_g<__nv_bfloat16, 256>(G, prm, dtype, batch, total_tokens, q, s);
-    }
-  } else {
-    switch (head_dim) {
-      case 64: return dispatch_g<__half, 64>(G, prm, dtype, batch, total_tokens, q, s);
-      case 128: return dispatch_g<__half, 128>(G, prm, dtype, batch, total_tokens, q, s);
-      case 256: return dispatch_g<__half, 256>(G, prm, dtype, batch, total_tokens, q, s);
-    }
-  }
-  return JENGA_ERR_UNSUPPORTED;
+  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, batch, total_tokens, q, s);
+  return dispatch_d<__half>(head_dim, G, prm, dtype, batch, total_tokens, q, s);
 }
 
 }  // namespace jenga_decode
