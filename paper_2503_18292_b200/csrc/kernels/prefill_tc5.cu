@@ -45,6 +45,7 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescal
 struct Prefill5Params {
   const uint8_t* arena;
   uint64_t start_offset, page_stride;
+  const void* q;
   void* out;
   const int32_t* cu_q;
   const int32_t* table;
@@ -84,6 +85,14 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, 
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// A operand from TMEM (K-major, two 16-bit elements per 32-bit column).
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    jenga_dev::smem_u32(bar))
@@ -108,24 +117,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
+__device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
       "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(addr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
-      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
-      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
-      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
-      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
-      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 template <typename T>
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
@@ -138,45 +141,31 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int32_t c0, int32_t c1, int32_t c2,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];\n" ::"r"(jenga_dev::smem_u32(dst)),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(jenga_dev::smem_u32(bar))
-      : "memory");
-}
-
-// D = head_dim, G = query heads per KV head, KT = KV tokens per tile.
+// D = head_dim, G = query heads per KV head, KT = KV tokens per tile,
+// NS = K/V ring stages.
 template <typename T, int D, int G, int KT, int NS>
 __global__ void __launch_bounds__(kT5Threads, 1)
-    paged_prefill_tc5_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap kv_map,
-                             const __grid_constant__ CUtensorMap q_map) {
+    paged_prefill_tc5_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap kv_map) {
   constexpr int NBOX = D / kBoxCols;          // 64-column chunks of head_dim
   constexpr int QB = kRows / G;               // tokens per query block
-  constexpr int Q_CHUNK = kRows * 128;        // one 64-col chunk of Q (K-major atom column)
   constexpr int KV_CHUNK = KT * 128;          // one 64-col chunk of a K or V tile
   constexpr int KV_BYTES = NBOX * KV_CHUNK;   // K (or V) of one tile, one head
   constexpr int STAGE = 2 * KV_BYTES;
-  constexpr int P_BYTES = kRows * 128;        // P buffer: 128 rows x 128-byte line
   constexpr int PIECES = KT / kTile;          // 16-row TMA boxes per tile chunk
-  constexpr uint32_t TMEM_COLS = D + 2 * KT <= 256 ? 256 : 512;  // power of two >= O + S columns
-  constexpr int S_COL = D;                    // S double buffer after O
-  static_assert(KT == 32 || KT == 64, "KV tile is 32 or 64 tokens");
-  static_assert(D + 2 * KT <= 512, "TMEM budget");
+  constexpr int Q_COL = D;                    // Q: D/2 packed columns after O
+  constexpr int S_COL = D + D / 2;            // S double buffer (P overwrites its S in place)
+  constexpr uint32_t TMEM_COLS = S_COL + 2 * KT <= 256 ? 256 : 512;
+  static_assert(KT == 64, "KV tile is 64 tokens");
+  static_assert(S_COL + 2 * KT <= 512, "TMEM budget");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* qs = smem;
-  uint8_t* ring = qs + NBOX * Q_CHUNK;
-  uint8_t* pbuf = ring + NS * STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + 2 * P_BYTES);
+  uint8_t* ring = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + NS;
   uint64_t* s_full = kv_empty + NS;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
+  uint64_t* p_full = s_full + 2;
   uint64_t* p_empty = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
 
@@ -196,14 +185,13 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
 
   if (threadIdx.x == 0) {
-    jenga_dev::mbar_init(q_full, 1);
+    jenga_dev::mbar_init(q_full, kSoftWarps);
     for (int i = 0; i < NS; ++i) {
       jenga_dev::mbar_init(&kv_full[i], 1);
       jenga_dev::mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       jenga_dev::mbar_init(&s_full[i], 1);
-      jenga_dev::mbar_init(&s_empty[i], kSoftWarps);
       jenga_dev::mbar_init(&p_full[i], kSoftWarps);
       jenga_dev::mbar_init(&p_empty[i], 1);
     }
@@ -224,10 +212,6 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   if (warp == kProducerWarp) {
     if (lane == 0) {
       jenga_dev::prefetch_tmap(&kv_map);
-      jenga_dev::prefetch_tmap(&q_map);
-      jenga_dev::mbar_arrive_expect_tx(q_full, NBOX * Q_CHUNK);
-#pragma unroll
-      for (int bx = 0; bx < NBOX; ++bx) tma_load_3d(qs + bx * Q_CHUNK, &q_map, bx * kBoxCols, h * G, p.cu_q[b] + t0, q_full);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
       const int64_t row_bytes = D * 2;
       const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * p.tpp;
@@ -257,35 +241,30 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     if (lane == 0) {
       const uint32_t id_s = idesc_f16<T>(kRows, KT, 0);
       const uint32_t id_o = idesc_f16<T>(kRows, D, 1);
-      const uint32_t qs_u = jenga_dev::smem_u32(qs);
+      // O += P_jj V_jj: P (bf16/fp16, packed over S) from TMEM, V [KT][D] MN-major
       auto issue_pv = [&](int jj) {
         const int sb = jj & 1;
         jenga_dev::mbar_wait(&p_full[sb], (jj >> 1) & 1);
         tc_fence_after();
-        const uint32_t p_u = jenga_dev::smem_u32(pbuf + sb * P_BYTES);
         const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < KT / 16; ++k) {
-          const uint64_t da = umma_desc(p_u + k * 32, 16, 1024);                 // P [128][KT] K-major
-          const uint64_t db = umma_desc(v_u + k * 16 * 128, KV_CHUNK, 1024);     // V [KT][D] MN-major
-          umma(tmem, da, db, id_o, (jj > 0 || k > 0) ? 1u : 0u);
-        }
-        umma_commit(&p_empty[sb]);          // P buffer free, O updated
+        for (int k = 0; k < KT / 16; ++k)
+          umma_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * 16 * 128, KV_CHUNK, 1024), id_o,
+                  (jj > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&p_empty[sb]);          // O updated
         umma_commit(&kv_empty[jj % NS]);    // K/V stage free
       };
       jenga_dev::mbar_wait(q_full, 0);
+      // In-order issue: S_{j} (into the buffer P_{j-2} occupied) follows PV_{j-2}.
       for (int j = 0; j < ntiles; ++j) {
         const int st = j % NS, sb = j & 1;
         jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
-        if (j >= 2) jenga_dev::mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint64_t da = umma_desc(qs_u + (k >> 2) * Q_CHUNK + (k & 3) * 32, 16, 1024);   // Q [128][D]
-          const uint64_t db = umma_desc(k_u + (k >> 2) * KV_CHUNK + (k & 3) * 32, 16, 1024);   // K [KT][D]
-          umma(tmem + S_COL + sb * KT, da, db, id_s, k > 0 ? 1u : 0u);
-        }
+        for (int k = 0; k < D / 16; ++k)   // S = Q K^T: Q from TMEM, K [KT][D] K-major
+          umma_ts(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
+                  umma_desc(k_u + (k >> 2) * KV_CHUNK + (k & 3) * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
         umma_commit(&s_full[sb]);
         if (j >= 1) issue_pv(j - 1);
       }
@@ -298,6 +277,28 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     const int tok = t0 + r / G;
     const bool row_ok = tok < c_len;
     const int ipos = n - c_len + tok;
+    // Q row -> TMEM (D/2 packed columns), read once from global
+    {
+      const uint4* qrow = reinterpret_cast<const uint4*>(
+          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D);
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 x = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + i) : make_uint4(0, 0, 0, 0);
+          w[4 * i] = x.x;
+          w[4 * i + 1] = x.y;
+          w[4 * i + 2] = x.z;
+          w[4 * i + 3] = x.w;
+        }
+        tmem_st32u(tmem + lane_addr + Q_COL + c * 32, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) jenga_dev::mbar_arrive(q_full);
+    }
     // row r attends keys [lo_r, hi_r] (empty range for padding rows)
     int lo_r = 0, hi_r = cross ? n - 1 : ipos;
     if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
@@ -321,9 +322,6 @@ __global__ void __launch_bounds__(kT5Threads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c + i] = v[i];
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) jenga_dev::mbar_arrive(&s_empty[sb]);
       if (softcap) {
 #pragma unroll
         for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
@@ -349,11 +347,12 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           for (int c = 0; c < D; c += 32) {
             float v[32];
             tmem_ld32(tmem + lane_addr + c, v);
+            uint32_t u[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= alpha;
-            tmem_st32(tmem + lane_addr + c, v);
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
+            tmem_st32u(tmem + lane_addr + c, u);
           }
-          tc_fence_before();
+          tmem_st_wait();
           l *= alpha;
         }
         m_used = m_new;
@@ -370,13 +369,15 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         pk[i / 2] = pack2<T>(a, bb);
       }
       l += rs0 + rs1;
-      if (j >= 2) jenga_dev::mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);  // P buffer free (PV_{j-2} done)
-      // P row r -> 128-byte line r of the K-major SW128 P buffer
-      uint8_t* prow = pbuf + sb * P_BYTES + r * 128;
+      // P_j over S_j's first KT/2 columns (the A operand of O += P_j V_j)
 #pragma unroll
-      for (int c = 0; c < KT / 8; ++c)
-        *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      for (int c = 0; c < KT / 2; c += 32) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
+        tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
+      }
+      tmem_st_wait();
       // masked keys of a boundary tile may hold non-finite V bytes (0*NaN = NaN
       // in the MMA): zero those V rows; 128 threads cover KT rows x NBOX chunks
       if (ktok0 < key_lo || ktok0 + KT - 1 > key_hi) {
@@ -389,8 +390,8 @@ __global__ void __launch_bounds__(kT5Threads, 1)
 #pragma unroll
           for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
         }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) jenga_dev::mbar_arrive(&p_full[sb]);
@@ -441,9 +442,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <typename T, int D, int G, int KT, int NS>
-int launch_tc5(const Prefill5Params& prm, int dtype, int batch, int total_tokens, const void* q, cudaStream_t s) {
+int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   constexpr int NBOX = D / kBoxCols;
-  const int smem = NBOX * kRows * 128 + NS * 2 * NBOX * KT * 128 + 2 * kRows * 128 + (1 + 2 * NS + 8) * 8 + 16 + 1024;
+  const int smem = NS * 2 * NBOX * KT * 128 + (1 + 2 * NS + 6) * 8 + 16 + 1024;
   auto fn = encode_fn();
   if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   uint64_t bytes = 0;
@@ -451,62 +452,42 @@ int launch_tc5(const Prefill5Params& prm, int dtype, int batch, int total_tokens
     return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_prefill: arena_base must come from jenga_arena_create");
   const CUtensorMapDataType dt =
       dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap kv_map, q_map;
-  {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / (D * 2)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
-    cuuint32_t box[2] = {kBoxCols, kTile};
-    cuuint32_t es[2] = {1, 1};
-    if (fn(&kv_map, dt, 2, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-        CUDA_SUCCESS)
-      return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
-  }
-  {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(prm.hq),
-                          static_cast<cuuint64_t>(total_tokens)};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(prm.hq) * D * 2};
-    cuuint32_t box[3] = {kBoxCols, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(kRows / G)};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (fn(&q_map, dt, 3, const_cast<void*>(q), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-        CUDA_SUCCESS)
-      return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: Q tensor map encode failed");
-  }
+  CUtensorMap kv_map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / (D * 2)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+  cuuint32_t box[2] = {kBoxCols, kTile};
+  cuuint32_t es[2] = {1, 1};
+  if (fn(&kv_map, dt, 2, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
   auto kern = paged_prefill_tc5_kernel<T, D, G, KT, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
   dim3 grid(prm.q_blocks, prm.hkv, batch);
-  kern<<<grid, kT5Threads, smem, s>>>(prm, kv_map, q_map);
+  kern<<<grid, kT5Threads, smem, s>>>(prm, kv_map);
   return jenga_dev::check_launch("paged_prefill_tc5_kernel");
 }
 
-template <typename T, int D, int KT, int NS>
-int dispatch_g(int G, const Prefill5Params& prm, int dtype, int batch, int total, const void* q, cudaStream_t s) {
+template <typename T, int D, int NS>
+int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (G) {
-    case 1: return launch_tc5<T, D, 1, KT, NS>(prm, dtype, batch, total, q, s);
-    case 2: return launch_tc5<T, D, 2, KT, NS>(prm, dtype, batch, total, q, s);
-    case 4: return launch_tc5<T, D, 4, KT, NS>(prm, dtype, batch, total, q, s);
-    case 8: return launch_tc5<T, D, 8, KT, NS>(prm, dtype, batch, total, q, s);
+    case 1: return launch_tc5<T, D, 1, 64, NS>(prm, dtype, s, batch);
+    case 2: return launch_tc5<T, D, 2, 64, NS>(prm, dtype, s, batch);
+    case 4: return launch_tc5<T, D, 4, 64, NS>(prm, dtype, s, batch);
+    case 8: return launch_tc5<T, D, 8, 64, NS>(prm, dtype, s, batch);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
 
+// 64-token K/V tiles; ring depth sized to ~192 KB of shared memory (96 KB for
+// head_dim 64, so two CTAs share an SM: 256 TMEM columns each).
 template <typename T>
-int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, int batch, int total, const void* q,
-               cudaStream_t s) {
-  // KV tile: 64 tokens (32 for head_dim 256 unless JENGA_PREFILL_KT=64, which
-  // leaves room for only two 64 KB stages)
-  static const int kt256 = [] {
-    const char* e = std::getenv("JENGA_PREFILL_KT");
-    return e != nullptr && std::atoi(e) == 64 ? 64 : 32;
-  }();
+int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (D) {
-    case 64: return dispatch_g<T, 64, 64, 2>(G, prm, dtype, batch, total, q, s);
-    case 128: return dispatch_g<T, 128, 64, 2>(G, prm, dtype, batch, total, q, s);
-    case 256:
-      return kt256 == 64 ? dispatch_g<T, 256, 64, 2>(G, prm, dtype, batch, total, q, s)
-                         : dispatch_g<T, 256, 32, 3>(G, prm, dtype, batch, total, q, s);
+    case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
+    case 128: return dispatch_g<T, 128, 6>(G, prm, dtype, s, batch);
+    case 256: return dispatch_g<T, 256, 3>(G, prm, dtype, s, batch);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
@@ -544,8 +525,10 @@ int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_s
   prm.cap_log2 = cap_log2;
   prm.inv_cap = inv_cap;
   const int G = hq / hkv;
-  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, batch, total_tokens, q, s);
-  return dispatch_d<__half>(head_dim, G, prm, dtype, batch, total_tokens, q, s);
+  prm.q = q;
+  (void)total_tokens;
+  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, s, batch);
+  return dispatch_d<__half>(head_dim, G, prm, dtype, s, batch);
 }
 
 }  // namespace jenga_decode
