@@ -98,6 +98,10 @@ int jenga_spec_add_group(jenga_spec* spec, const char* name, int kind,
                          uint32_t num_layers, uint64_t bytes_per_token_per_layer,
                          uint32_t tokens_per_page, uint64_t window_tokens,
                          uint64_t checkpoint_interval_tokens);
+/* reference combine_with_draft (simulator.cpp:32-41): a new spec holding the
+ * target's groups then the draft's renamed "draft.<name>" — one LCM pool for
+ * both models (speculative decoding). */
+int jenga_spec_combine_with_draft(const jenga_spec* target, const jenga_spec* draft, jenga_spec** out);
 int jenga_spec_validate(const jenga_spec* spec);
 int jenga_spec_num_groups(const jenga_spec* spec);
 /* small_page_size(group g) — model_config.cpp:85-89 */
@@ -216,6 +220,26 @@ int jenga_pages_admit(jenga_pages* pl, uint64_t request, const uint64_t* tokens,
  * *consumed = positions stored; JENGA_ERR_OOM when an allocation failed. */
 int jenga_pages_prefill(jenga_pages* pl, uint64_t request, uint64_t budget, uint64_t now_step,
                         uint64_t* consumed);
+/* Vision-embedding pages (reference EngineConfig::vision_mode, simulator.hpp:
+ * 25-41; simulator.cpp:453-476, 504-547): mode 0 = on_demand (admit stores
+ * the embeddings of images the prefix hit does not cover; prefill frees them
+ * as image positions are consumed), 1 = full_reuse (admit stores all prompt
+ * KV up front and defers window frees to the prompt's end; embeddings are
+ * parked in the unwritten KV pages, see jenga_token_rows_scatter).  Set
+ * before admitting requests. */
+int jenga_pages_set_vision_mode(jenga_pages* pl, int mode);
+/* Speculative decoding (simulator.cpp:568-640).  Draft groups are those named
+ * "draft.*" (jenga_spec_combine_with_draft).  rollback_newest drops the newest
+ * `count` stored positions of group g, freeing pages that empty out.
+ * speculative_decode: the draft groups store propose_k positions, the
+ * propose_k - accepted rejected ones roll back, then the target groups store
+ * n_target (<= max(accepted, 1)) tokens.  JENGA_ERR_OOM: release the request. */
+int jenga_pages_rollback_newest(jenga_pages* pl, uint64_t request, int g, uint64_t count,
+                                uint64_t now_step);
+int jenga_pages_speculative_decode(jenga_pages* pl, uint64_t request, uint32_t propose_k,
+                                   uint64_t accepted, const uint64_t* target_tokens,
+                                   uint64_t n_target, uint64_t now_step);
+int jenga_pages_is_draft_group(const jenga_pages* pl, int g, int* is_draft);
 /* Mamba restore after a prefix hit: the pinned checkpoint page of group g
  * (*has=0 when none is pending).  The caller copies it into the working page
  * (jenga_page_copy) and then calls jenga_pages_finish_restore, which returns
@@ -332,6 +356,27 @@ int jenga_mamba_state_gather(const void* arena_base, jenga_layer_view view,
 int jenga_mamba_state_scatter(void* arena_base, jenga_layer_view view,
                               const int64_t* page_globals, int batch, const void* dense,
                               void* stream);
+/* Token rows <-> pages (vision-embedding pages, simulator.cpp:453-476,
+ * 525-542).  Row t (row_bytes, row_stride_bytes apart)
+ * of the token at slot_mapping[t] = page_global*tpp + off (negative = skip;
+ * gather writes zeros) is cut into piece_bytes pieces; piece p lives in layer
+ * p / pieces_per_layer of `view` (layer l at view.start_offset +
+ * l*view.exec_page_size), sub-slice q = p % pieces_per_layer:
+ *   start + layer*exec_page_size + page*page_stride + (q*tpp + off)*piece_bytes
+ * - a vision-embedding group's own pages: pieces_per_layer = 1,
+ *   piece_bytes = bytes_per_token_per_layer;
+ * - the full_reuse overlay into a KV group's unwritten pages:
+ *   pieces_per_layer = 2*Hkv, piece_bytes = D*dtype — exactly the bytes
+ *   jenga_reshape_and_cache later writes for the same token.
+ * row_bytes <= num_layers*pieces_per_layer*piece_bytes; 16-byte multiples. */
+int jenga_token_rows_scatter(void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                             uint32_t pieces_per_layer, uint32_t piece_bytes, uint32_t tokens_per_page,
+                             const void* rows, uint64_t row_bytes, int64_t row_stride_bytes,
+                             const int64_t* slot_mapping, int n_tokens, void* stream);
+int jenga_token_rows_gather(const void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                            uint32_t pieces_per_layer, uint32_t piece_bytes, uint32_t tokens_per_page,
+                            void* rows, uint64_t row_bytes, int64_t row_stride_bytes,
+                            const int64_t* slot_mapping, int n_tokens, void* stream);
 /* Whole-small-page copy (all layers of a group): checkpoint snapshot / restore
  * (simulator.cpp:231-242). Addresses = global * small_page_bytes. */
 int jenga_page_copy(void* arena_base, uint64_t small_page_bytes, const int64_t* src_globals,

@@ -376,3 +376,47 @@ int orc_page_copy(uint8_t* arena, uint64_t small_page_bytes, const int64_t* src,
   }
   return ORC_OK;
 }
+
+/* Token rows <-> pages: the vision-embedding page path (simulator.cpp:453-476,
+ * 525-542).  Piece p of row t lives in layer
+ * p / ppl, sub-slice q = p % ppl, at
+ *   start + layer*layer_stride + page*page_stride + (q*tpp + off)*piece
+ * for slot = page*tpp + off (the page-layer address of memory_layout.cpp:
+ * 41-55 plus our intra-slice layout).  Negative slots: scatter skips, gather
+ * yields zeros. */
+static uint8_t* orc_row_piece(uint8_t* arena, uint64_t start, uint64_t layer_stride, uint64_t page_stride,
+                              uint32_t tpp, uint32_t ppl, uint32_t piece, int64_t slot, uint64_t p) {
+  const uint64_t layer = p / ppl, q = p % ppl;
+  const uint64_t page = (uint64_t)slot / tpp, off = (uint64_t)slot % tpp;
+  return arena + start + layer * layer_stride + page * page_stride + (q * tpp + off) * piece;
+}
+
+int orc_token_rows_scatter(uint8_t* arena, uint64_t start, uint64_t layer_stride, uint64_t page_stride, uint32_t tpp,
+                           uint32_t ppl, uint32_t piece, const uint8_t* rows, uint64_t row_bytes, int64_t row_stride,
+                           const int64_t* slots, int n) {
+  if (piece == 0 || row_bytes % piece) return ORC_ERR_CONFIG;
+  for (int t = 0; t < n; ++t) {
+    if (slots[t] < 0) continue;
+    for (uint64_t p = 0; p < row_bytes / piece; ++p)
+      memcpy(orc_row_piece(arena, start, layer_stride, page_stride, tpp, ppl, piece, slots[t], p),
+             rows + (int64_t)t * row_stride + p * piece, piece);
+  }
+  return ORC_OK;
+}
+
+int orc_token_rows_gather(uint8_t* arena, uint64_t start, uint64_t layer_stride, uint64_t page_stride, uint32_t tpp,
+                          uint32_t ppl, uint32_t piece, uint8_t* rows, uint64_t row_bytes, int64_t row_stride,
+                          const int64_t* slots, int n) {
+  if (piece == 0 || row_bytes % piece) return ORC_ERR_CONFIG;
+  for (int t = 0; t < n; ++t) {
+    uint8_t* row = rows + (int64_t)t * row_stride;
+    if (slots[t] < 0) {
+      memset(row, 0, row_bytes);
+      continue;
+    }
+    for (uint64_t p = 0; p < row_bytes / piece; ++p)
+      memcpy(row + p * piece, orc_row_piece(arena, start, layer_stride, page_stride, tpp, ppl, piece, slots[t], p),
+             piece);
+  }
+  return ORC_OK;
+}

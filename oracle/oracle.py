@@ -47,6 +47,8 @@ class COracle:
         L.orc_mamba_gather.argtypes = [_p, _u64, _u64, _u64, _p, _int, _p]
         L.orc_mamba_scatter.argtypes = [_p, _u64, _u64, _u64, _p, _int, _p]
         L.orc_page_copy.argtypes = [_p, _u64, _p, _p, _int]
+        for f in (L.orc_token_rows_scatter, L.orc_token_rows_gather):
+            f.argtypes = [_p, _u64, _u64, _u64, _u32, _u32, _u32, _p, _u64, C.c_int64, _p, _int]
 
     @staticmethod
     def _ok(rc):
@@ -149,6 +151,21 @@ class COracle:
         self._ok(self.lib.orc_page_copy(arena.ctypes.data_as(_p), small_page_bytes, sp, dp, len(s)))
 
 
+    def token_rows_scatter(self, arena, view, ppl, piece, tpp, rows, slots):
+        """view = (start_offset, page_stride, exec_page_size); rows uint8 [T, bytes]."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint8)
+        sl, sp = _np(slots, np.int64)
+        self._ok(self.lib.orc_token_rows_scatter(arena.ctypes.data_as(_p), view[0], view[2], view[1], tpp, ppl, piece,
+                                                 rows.ctypes.data_as(_p), rows.shape[1], rows.shape[1], sp, len(sl)))
+
+    def token_rows_gather(self, arena, view, ppl, piece, tpp, row_bytes, slots):
+        sl, sp = _np(slots, np.int64)
+        rows = np.zeros((len(sl), row_bytes), dtype=np.uint8)
+        self._ok(self.lib.orc_token_rows_gather(arena.ctypes.data_as(_p), view[0], view[2], view[1], tpp, ppl, piece,
+                                                rows.ctypes.data_as(_p), row_bytes, row_bytes, sp, len(sl)))
+        return rows
+
+
 class RefError(RuntimeError):
     pass
 
@@ -193,6 +210,10 @@ class RefLib:
             "ref_kv_has_associated_empty": [_p, _int, _u64, C.POINTER(_int)],
             "ref_kv_check_invariants": [_p],
             "ref_sim_create": [_p, _u64, _u64, _int, _int, _p, _p, _p, _p, _p, _p, _p, C.POINTER(_p)],
+            "ref_sim_create_ex": [_p, _u64, _u64, _int, _int, _p, _p, _p, _p, _p, _p, _p, _int, _p, _u32, _dbl,
+                                  _u64, C.POINTER(_p)],
+            "ref_spec_accept_draws": [_u64, _u64, _u32, _dbl, _int, _p],
+            "ref_sim_draft_len": [_p, _u64, C.POINTER(_u64)],
             "ref_gen_multi_article": [_u32, _u32, _u64, _u64, _u64, _u64, _u64, _p, _p, _p, _p, _p, _int,
                                       C.POINTER(_int)],
             "ref_sim_step": [_p, C.POINTER(_u32)],
@@ -462,10 +483,18 @@ def multi_article_trace(ref: RefLib, articles=4, questions=3, article_tokens=400
              "segments": [[0, int(seg[i, 0])], [0, int(seg[i, 1])]]} for i in range(n.value)]
 
 
+def spec_accept_draws(ref, seed, rid, propose_k, acceptance, n):
+    """The reference's per-request acceptance draws (simulator.cpp:44-52, 109)."""
+    out = np.zeros(n, dtype=np.uint64)
+    ref.lib.ref_spec_accept_draws(seed, rid, propose_k, float(acceptance), n, out.ctypes.data_as(_p))
+    return [int(x) for x in out]
+
+
 class RefSim:
     """The reference SimEngine (stepped), page lists read back via the shim."""
 
-    def __init__(self, spec: RefSpec, budget, chunk, prefix_caching, requests: List[dict]):
+    def __init__(self, spec: RefSpec, budget, chunk, prefix_caching, requests: List[dict], vision_mode=0,
+                 draft: "RefSpec" = None, propose_k=4, acceptance=0.7, seed=0):
         self.spec, self.L, self.ref = spec, spec.L, spec.ref
         ids = np.array([r["id"] for r in requests], dtype=np.uint64)
         arr = np.array([r.get("arrival", 0) for r in requests], dtype=np.uint64)
@@ -476,10 +505,19 @@ class RefSim:
         grp = np.array([r.get("prefix_group", -1) for r in requests], dtype=np.int32)
         self._keep = (ids, arr, outs, segc, segi, segt, grp)
         self.h = _p()
-        self.ref.check(self.L.ref_sim_create(spec.h, budget, chunk, 1 if prefix_caching else 0, len(ids),
-                                             ids.ctypes.data_as(_p), arr.ctypes.data_as(_p), outs.ctypes.data_as(_p),
-                                             segc.ctypes.data_as(_p), segi.ctypes.data_as(_p),
-                                             segt.ctypes.data_as(_p), grp.ctypes.data_as(_p), C.byref(self.h)))
+        self.ref.check(self.L.ref_sim_create_ex(spec.h, budget, chunk, 1 if prefix_caching else 0, len(ids),
+                                                ids.ctypes.data_as(_p), arr.ctypes.data_as(_p),
+                                                outs.ctypes.data_as(_p), segc.ctypes.data_as(_p),
+                                                segi.ctypes.data_as(_p), segt.ctypes.data_as(_p),
+                                                grp.ctypes.data_as(_p), int(vision_mode),
+                                                None if draft is None else draft.h, propose_k, float(acceptance),
+                                                seed, C.byref(self.h)))
+        self._draft = draft
+
+    def draft_len(self, rid):
+        o = _u64()
+        self.ref.check(self.L.ref_sim_draft_len(self.h, rid, C.byref(o)))
+        return o.value
 
     def __del__(self):
         if getattr(self, "h", None):

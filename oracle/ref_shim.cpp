@@ -10,6 +10,7 @@
 //     (simulator.cpp:217-282) over the reference KvAllocator, used to build
 //     the bench workload's page lists with the reference's own allocator.
 // Never linked into the product.
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
@@ -287,6 +288,62 @@ EXPORT int ref_sim_create(void* s, uint64_t budget, uint64_t chunk, int prefix_c
       tr.requests.push_back(q);
     }
     *out = new SimEngine(static_cast<Spec*>(s)->spec, cfg, tr);
+  });
+}
+// As ref_sim_create plus the vision mode (0 on_demand, 1 full_reuse) and,
+// when draft != NULL, a speculative config (SpeculativeConfig, simulator.hpp:
+// 30-34) with the engine seed the acceptance draws derive from.
+EXPORT int ref_sim_create_ex(void* s, uint64_t budget, uint64_t chunk, int prefix_caching, int n_req,
+                             const uint64_t* ids, const uint64_t* arrival, const uint64_t* output_tokens,
+                             const int* seg_count, const int* seg_is_image, const uint64_t* seg_tokens,
+                             const int* prefix_group, int vision_mode, void* draft, uint32_t propose_k,
+                             double acceptance, uint64_t seed, void** out) {
+  return guarded([&] {
+    EngineConfig cfg;
+    cfg.memory_budget = budget;
+    cfg.chunked_prefill_size = chunk;
+    cfg.prefix_caching = prefix_caching != 0;
+    cfg.vision_mode = vision_mode ? VisionMode::kFullyAllocatedReuse : VisionMode::kAllocateOnDemand;
+    cfg.seed = seed;
+    if (draft) cfg.speculative = SpeculativeConfig{static_cast<Spec*>(draft)->spec, propose_k, acceptance};
+    Trace tr;
+    int k = 0;
+    for (int r = 0; r < n_req; ++r) {
+      TraceRequest q;
+      q.id = ids[r];
+      q.arrival_step = arrival[r];
+      q.output_tokens = output_tokens[r];
+      if (prefix_group && prefix_group[r] >= 0) q.prefix_group = "article-" + std::to_string(prefix_group[r]);
+      for (int i = 0; i < seg_count[r]; ++i, ++k) q.segments.push_back(Segment{seg_is_image[k] != 0, seg_tokens[k]});
+      tr.requests.push_back(q);
+    }
+    *out = new SimEngine(static_cast<Spec*>(s)->spec, cfg, tr);
+  });
+}
+// The acceptance draws of request `id` (simulator.cpp:109, 44-52 restated:
+// per request mt19937_64 seeded mix64(seed, mix64(id, 0x5bec)); each draw
+// counts successes of propose_k Bernoulli(acceptance) coins).
+EXPORT void ref_spec_accept_draws(uint64_t seed, uint64_t id, uint32_t propose_k, double acceptance, int n,
+                                  uint64_t* out) {
+  std::mt19937_64 rng;
+  rng.seed(mix64(seed, mix64(id, 0x5bec)));
+  for (int i = 0; i < n; ++i) {
+    std::bernoulli_distribution coin(std::clamp(acceptance, 0.0, 1.0));
+    uint64_t successes = 0;
+    for (uint32_t j = 0; j < propose_k; ++j)
+      if (coin(rng)) ++successes;
+    out[i] = successes;
+  }
+}
+// The reference draft_len of a request (speculative runs).
+EXPORT int ref_sim_draft_len(void* e, uint64_t id, uint64_t* draft_len) {
+  return guarded([&] {
+    for (auto& r : static_cast<SimEngine*>(e)->requests_) {
+      if (r.meta.id != id) continue;
+      *draft_len = r.draft_len;
+      return;
+    }
+    throw InvariantError("unknown request");
   });
 }
 // The reference multi-article prefix trace (trace.cpp:144-169), flattened:

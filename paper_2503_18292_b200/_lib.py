@@ -83,6 +83,7 @@ _SIGS = {
     "jenga_spec_destroy": (None, [_p]),
     "jenga_spec_add_group": (_int, [_p, C.c_char_p, _int, _u32, _u64, _u32, _u64, _u64]),
     "jenga_spec_validate": (_int, [_p]),
+    "jenga_spec_combine_with_draft": (_int, [_p, _p, C.POINTER(_p)]),
     "jenga_spec_num_groups": (_int, [_p]),
     "jenga_spec_small_page_size": (_int, [_p, _int, _pu64]),
     "jenga_spec_lcm_page_size": (_int, [_p, _pu64]),
@@ -129,6 +130,10 @@ _SIGS = {
     "jenga_pages_set_fix_mamba_restore": (_int, [_p, _int]),
     "jenga_pages_set_defer_window_free": (_int, [_p, _u64, _int]),
     "jenga_pages_apply_window_free": (_int, [_p, _u64, _u64]),
+    "jenga_pages_set_vision_mode": (_int, [_p, _int]),
+    "jenga_pages_rollback_newest": (_int, [_p, _u64, _int, _u64, _u64]),
+    "jenga_pages_speculative_decode": (_int, [_p, _u64, _u32, _u64, _p, _u64, _u64]),
+    "jenga_pages_is_draft_group": (_int, [_p, _int, C.POINTER(_int)]),
     "jenga_kv_cache_entries": (_int, [_p, _int, _pu64]),
     "jenga_pages_seq_len": (_int, [_p, _u64, _pu64]),
     "jenga_pages_group_state": (_int, [_p, _u64, _int, _pu64, _pu64, _pu64, _pu64, _pint, C.POINTER(SmallPage)]),
@@ -149,6 +154,8 @@ _SIGS = {
     "jenga_mamba_state_gather": (_int, [_p, LayerViewC, _p, _int, _p, _p]),
     "jenga_mamba_state_scatter": (_int, [_p, LayerViewC, _p, _int, _p, _p]),
     "jenga_page_copy": (_int, [_p, _u64, _p, _p, _int, _p]),
+    "jenga_token_rows_scatter": (_int, [_p, LayerViewC, _u32, _u32, _u32, _u32, _p, _u64, C.c_int64, _p, _int, _p]),
+    "jenga_token_rows_gather": (_int, [_p, LayerViewC, _u32, _u32, _u32, _u32, _p, _u64, C.c_int64, _p, _int, _p]),
     "jenga_kernel_launch_count": (_u64, []),
 }
 

@@ -105,6 +105,28 @@ JENGA_EXPORT int jenga_spec_add_group(jenga_spec* spec, const char* name, int ki
   });
 }
 
+// reference combine_with_draft (simulator.cpp:32-41): the target's groups
+// followed by the draft's, renamed "draft.<name>", validated.
+JENGA_EXPORT int jenga_spec_combine_with_draft(const jenga_spec* target, const jenga_spec* draft, jenga_spec** out) {
+  ARG_CHECK(target != nullptr && draft != nullptr && out != nullptr);
+  return guarded([&] {
+    auto* s = new jenga_spec;
+    s->spec = target->spec;
+    s->spec.name = target->spec.name + "+draft";
+    for (jenga::LayerGroupSpec g : draft->spec.groups) {
+      g.name = "draft." + g.name;
+      s->spec.groups.push_back(std::move(g));
+    }
+    try {
+      s->spec.validate();
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
 JENGA_EXPORT int jenga_spec_validate(const jenga_spec* spec) {
   ARG_CHECK(spec != nullptr);
   return guarded([&] { spec->spec.validate(); });
@@ -445,14 +467,43 @@ JENGA_EXPORT int jenga_pages_admit(jenga_pages* pl, uint64_t request, const uint
                                    const uint8_t* is_image, const uint64_t* image_ordinals, uint64_t n,
                                    uint64_t now, uint64_t* hit) {
   ARG_CHECK(pl != nullptr && (n == 0 || tokens != nullptr));
-  return guarded([&] {
+  bool oom = false;
+  const int rc = guarded([&] {
     std::vector<uint64_t> t(tokens, tokens + n);
     std::vector<uint8_t> img = is_image ? std::vector<uint8_t>(is_image, is_image + n) : std::vector<uint8_t>();
     std::vector<uint64_t> ord =
         image_ordinals ? std::vector<uint64_t>(image_ordinals, image_ordinals + n) : std::vector<uint64_t>();
-    const uint64_t h = pl->pl->admit(request, t, img, ord, now);
+    const uint64_t h = pl->pl->admit(request, t, img, ord, now, &oom);
     if (hit) *hit = h;
   });
+  if (rc == JENGA_OK && oom) return fail(JENGA_ERR_OOM, "out of KV memory at admission (preempt the request)");
+  return rc;
+}
+
+JENGA_EXPORT int jenga_pages_set_vision_mode(jenga_pages* pl, int mode) {
+  ARG_CHECK(pl != nullptr && (mode == 0 || mode == 1));
+  return guarded([&] { pl->pl->set_vision_mode(static_cast<jenga::PageLists::VisionMode>(mode)); });
+}
+
+JENGA_EXPORT int jenga_pages_rollback_newest(jenga_pages* pl, uint64_t request, int g, uint64_t count,
+                                             uint64_t now) {
+  ARG_CHECK(pl != nullptr && g >= 0);
+  return guarded([&] { pl->pl->rollback_newest(request, static_cast<size_t>(g), count, now); });
+}
+
+JENGA_EXPORT int jenga_pages_speculative_decode(jenga_pages* pl, uint64_t request, uint32_t propose_k,
+                                                uint64_t accepted, const uint64_t* target_tokens,
+                                                uint64_t n_target, uint64_t now) {
+  ARG_CHECK(pl != nullptr);
+  bool ok = true;
+  int rc = guarded([&] { ok = pl->pl->speculative_decode(request, propose_k, accepted, target_tokens, n_target, now); });
+  if (rc == JENGA_OK && !ok) return fail(JENGA_ERR_OOM, "out of KV memory (preempt the request)");
+  return rc;
+}
+
+JENGA_EXPORT int jenga_pages_is_draft_group(const jenga_pages* pl, int g, int* is_draft) {
+  ARG_CHECK(pl != nullptr && is_draft != nullptr && g >= 0);
+  return guarded([&] { *is_draft = pl->pl->is_draft_group(static_cast<size_t>(g)) ? 1 : 0; });
 }
 
 JENGA_EXPORT int jenga_pages_prefill(jenga_pages* pl, uint64_t request, uint64_t budget, uint64_t now,

@@ -406,6 +406,11 @@ class PageLists {
     uint64_t freed_blocks = 0, held_tokens = 0, live_blocks = 0;
     std::optional<SmallPageId> working_page;
     uint64_t checkpoints = 0;
+    uint64_t consumed_held = 0;      // vision: consumed ordinals still held
+    uint64_t consumed_ordinals = 0;  // vision: ordinals consumed by prefill
+  };
+  struct ImageSpan {
+    uint64_t begin = 0, end = 0;  // prompt positions, inclusive
   };
   struct Request {
     uint64_t id = 0;
@@ -424,7 +429,14 @@ class PageLists {
     // needs keys that left the window (the reference's suppress_window_free,
     // simulator.cpp:466-500); apply_window_free() performs them.
     bool defer_window_free = false;
+    // full_reuse vision mode: window frees suppressed until the prompt is
+    // written (simulator.cpp:466-500)
+    bool suppress_window_free = false;
+    std::vector<ImageSpan> images;  // admit(): maximal runs of one image
+    uint64_t draft_len = 0;         // speculative: draft sequence length
   };
+  // reference simulator.hpp:25 (EngineConfig::vision_mode)
+  enum class VisionMode { kAllocateOnDemand = 0, kFullyAllocatedReuse = 1 };
 
   void add_request(uint64_t id);
   bool has_request(uint64_t id) const { return index_.count(id) != 0; }
@@ -441,12 +453,31 @@ class PageLists {
   // Admission (reference simulator.cpp:435-452): install the prompt and, with
   // prefix caching, pin and adopt the longest cached prefix.  Returns the hit
   // length (prompt positions already resident).
+  // Vision pages are stored here too (on_demand: embeddings of images the
+  // hit does not cover; full_reuse: all prompt KV up front); *oom set when
+  // one of those allocations failed.
   uint64_t admit(uint64_t id, const std::vector<uint64_t>& tokens, const std::vector<uint8_t>& is_image,
-                 const std::vector<uint64_t>& image_ordinals, uint64_t now);
+                 const std::vector<uint64_t>& image_ordinals, uint64_t now, bool* oom = nullptr);
   // Chunked prefill of up to `budget` positions (reference simulator.cpp:
-  // 504-547, vision-embedding groups excluded).  Returns positions consumed;
-  // *oom set when an allocation failed.
+  // 504-547): on_demand mode frees consumed vision-embedding pages, and the
+  // prompt's last position finishes the prefill (finish_prefill, :484-502).
+  // Returns positions consumed; *oom set when an allocation failed.
   uint64_t prefill(uint64_t id, uint64_t budget, uint64_t now, bool* oom);
+  // Vision-embedding handling at admit / prefill (simulator.cpp:453-476,
+  // 525-542); set before admitting requests.
+  void set_vision_mode(VisionMode m) { vision_mode_ = m; }
+  VisionMode vision_mode() const { return vision_mode_; }
+  // reference simulator.cpp:568-597: drop the newest `count` stored
+  // positions of group g, freeing pages that empty out.
+  void rollback_newest(uint64_t id, size_t g, uint64_t count, uint64_t now);
+  // reference speculative_decode_one (simulator.cpp:600-640): the draft
+  // groups ("draft." prefix, simulator.cpp:76-78) store propose_k positions,
+  // the propose_k - accepted rejected ones roll back, then the target groups
+  // store n_target = max(accepted, 1) tokens (fewer when the request ends).
+  // Returns false on OOM (the request must be released).
+  bool speculative_decode(uint64_t id, uint32_t propose_k, uint64_t accepted, const uint64_t* target_tokens,
+                          uint64_t n_target, uint64_t now);
+  bool is_draft_group(size_t g) const { return draft_flags_[g] != 0; }
   // reference simulator.cpp:347-358
   void refresh_mamba_checkpoints(uint64_t id, uint64_t now);
   // The Mamba restore fix: forget (and free) a pinned checkpoint page once
@@ -462,9 +493,13 @@ class PageLists {
   std::vector<GroupLookupInput> build_lookup_inputs(const Request& r) const;
   void append_chain(Request& r, size_t g);
   void free_block(Request& r, size_t g, uint64_t b, bool allow_cache, uint64_t now);
+  void finish_prefill(Request& r, uint64_t now);
+  uint64_t adopt_prefix(Request& r, uint64_t now);
 
   KvAllocator* kv_;
   bool prefix_caching_;
+  VisionMode vision_mode_ = VisionMode::kAllocateOnDemand;
+  std::vector<uint8_t> draft_flags_;
   std::vector<Request> requests_;
   std::unordered_map<uint64_t, size_t> index_;
 };

@@ -10,6 +10,8 @@ namespace jenga {
 PageLists::PageLists(KvAllocator* kv, bool prefix_caching)
     : kv_(kv), prefix_caching_(prefix_caching) {
   JENGA_CHECK(kv_ != nullptr, "page lists need an allocator");
+  for (size_t g = 0; g < kv_->num_groups(); ++g)  // simulator.cpp:76-78
+    draft_flags_.push_back(kv_->group(g).name.rfind("draft.", 0) == 0 ? 1 : 0);
 }
 
 void PageLists::add_request(uint64_t id) {
@@ -64,9 +66,10 @@ void PageLists::append_chain(Request& r, size_t g) {
 bool PageLists::store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now) {
   Request& r = req(id);
   JENGA_CHECK(g < r.groups.size(), "group index out of range");
-  JENGA_CHECK(pos >= 1 && pos <= r.tokens.size(), "position beyond the sequence");
-  GroupRuntime& rt = r.groups[g];
   const LayerGroupSpec& grp = kv_->group(g);
+  // draft groups record draft-sequence ordinals (simulator.cpp:603-607)
+  JENGA_CHECK(pos >= 1 && (draft_flags_[g] || pos <= r.tokens.size()), "position beyond the sequence");
+  GroupRuntime& rt = r.groups[g];
   TypeAllocator& ta = kv_->type_allocator(g);
 
   if (grp.kind == LayerKind::kMamba) {
@@ -113,7 +116,7 @@ bool PageLists::store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now
   const uint64_t ordinal_value = grp.stores_image_tokens() ? r.image_ordinal[pos - 1] : pos;
   ta.set_prefix_length(rt.blocks[bidx].page, ordinal_value);
 
-  if (grp.kind == LayerKind::kSlidingWindow && !r.defer_window_free) {
+  if (grp.kind == LayerKind::kSlidingWindow && !r.defer_window_free && !r.suppress_window_free) {
     const uint64_t w = grp.window_tokens;
     if (rt.stored > w) {
       const uint64_t exited = rt.stored - w;
@@ -138,6 +141,7 @@ void PageLists::free_block(Request& r, size_t g, uint64_t b, bool allow_cache, u
   blk.live = false;
   rt.live_blocks--;
   rt.held_tokens -= covered;
+  if (kv_->group(g).kind == LayerKind::kVisionEmbedding) rt.consumed_held -= std::min(rt.consumed_held, covered);
   while (rt.freed_blocks < rt.blocks.size() && !rt.blocks[rt.freed_blocks].live) rt.freed_blocks++;
 }
 
@@ -197,8 +201,8 @@ std::vector<GroupLookupInput> PageLists::build_lookup_inputs(const Request& r) c
 
 // reference simulator.cpp:435-452 (admit) + 391-433 (adopt_lookup_result)
 uint64_t PageLists::admit(uint64_t id, const std::vector<uint64_t>& tokens, const std::vector<uint8_t>& is_image,
-                          const std::vector<uint64_t>& image_ordinals, uint64_t now) {
-  (void)now;
+                          const std::vector<uint64_t>& image_ordinals, uint64_t now, bool* oom) {
+  if (oom) *oom = false;
   Request& r = req(id);
   JENGA_CHECK(is_image.empty() || is_image.size() == tokens.size(), "is_image length mismatch");
   r.tokens = tokens;
@@ -209,7 +213,60 @@ uint64_t PageLists::admit(uint64_t id, const std::vector<uint64_t>& tokens, cons
   r.groups.assign(kv_->num_groups(), GroupRuntime{});
   r.restore.assign(kv_->num_groups(), std::nullopt);
   r.needs_release = false;
-  if (!prefix_caching_) return 0;
+  r.suppress_window_free = false;
+  r.draft_len = 0;
+  // image spans: maximal runs of image positions of one image (one ordinal);
+  // the reference keeps them per trace segment (simulator.cpp:130-137)
+  r.images.clear();
+  for (uint64_t pos = 1; pos <= r.prompt_len; ++pos) {
+    if (!r.is_image[pos - 1]) continue;
+    if (!r.images.empty() && r.images.back().end == pos - 1 && r.image_ordinal[pos - 2] == r.image_ordinal[pos - 1])
+      r.images.back().end = pos;
+    else
+      r.images.push_back(ImageSpan{pos, pos});
+  }
+  const uint64_t hit = prefix_caching_ ? adopt_prefix(r, now) : 0;
+  r.consumed = hit;
+  // reference simulator.cpp:453-476
+  if (vision_mode_ == VisionMode::kAllocateOnDemand) {
+    // encode: embeddings of every image the hit does not fully cover
+    for (size_t g = 0; g < kv_->num_groups(); ++g) {
+      if (kv_->group(g).kind != LayerKind::kVisionEmbedding) continue;
+      for (const ImageSpan& img : r.images) {
+        if (img.end <= r.consumed) continue;
+        for (uint64_t pos = img.begin; pos <= img.end; ++pos) {
+          if (!store_position(id, g, pos, now)) {
+            req(id).needs_release = true;
+            if (oom) *oom = true;
+            return hit;
+          }
+        }
+      }
+    }
+  } else {
+    // all prompt KV up front; embeddings overlay the unwritten pages
+    r.suppress_window_free = true;
+    for (uint64_t pos = r.consumed + 1; pos <= r.prompt_len; ++pos) {
+      for (size_t g = 0; g < kv_->num_groups(); ++g) {
+        if (kv_->group(g).kind == LayerKind::kVisionEmbedding) continue;
+        if (!group_stores_position(g, req(id), pos)) continue;
+        if (!store_position(id, g, pos, now)) {
+          req(id).needs_release = true;
+          if (oom) *oom = true;
+          return hit;
+        }
+      }
+    }
+  }
+  Request& rr = req(id);
+  if (rr.consumed >= rr.prompt_len) finish_prefill(rr, now);
+  return hit;
+}
+
+// reference simulator.cpp:441-448 (lookup) + 391-433 (adopt_lookup_result)
+uint64_t PageLists::adopt_prefix(Request& r, uint64_t now) {
+  (void)now;
+  const uint64_t id = r.id;
   const auto inputs = build_lookup_inputs(r);
   const LookupResult res = kv_->lookup_and_pin(inputs, r.prompt_len, id);
   const uint64_t hit = res.hit_length;
@@ -244,7 +301,6 @@ uint64_t PageLists::admit(uint64_t id, const std::vector<uint64_t>& tokens, cons
     }
     while (rt.freed_blocks < rt.blocks.size() && !rt.blocks[rt.freed_blocks].live) rt.freed_blocks++;
   }
-  r.consumed = hit;
   return hit;
 }
 
@@ -252,11 +308,13 @@ uint64_t PageLists::admit(uint64_t id, const std::vector<uint64_t>& tokens, cons
 uint64_t PageLists::prefill(uint64_t id, uint64_t budget, uint64_t now, bool* oom) {
   Request& r = req(id);
   if (oom) *oom = false;
+  const bool prealloc = vision_mode_ == VisionMode::kFullyAllocatedReuse;
   uint64_t done = 0;
   while (done < budget && r.consumed < r.prompt_len) {
     const uint64_t pos = r.consumed + 1;
     for (size_t g = 0; g < kv_->num_groups(); ++g) {
       if (kv_->group(g).kind == LayerKind::kVisionEmbedding) continue;
+      if (prealloc) continue;  // pages already exist
       if (!group_stores_position(g, r, pos)) continue;
       const GroupRuntime& rt = r.groups[g];
       if (!rt.stored_positions.empty() && pos <= rt.stored_positions.back()) continue;  // pinned block
@@ -268,9 +326,108 @@ uint64_t PageLists::prefill(uint64_t id, uint64_t budget, uint64_t now, bool* oo
     }
     r.consumed++;
     done++;
+    // consume the vision embeddings of image positions as they prefill
+    if (vision_mode_ == VisionMode::kAllocateOnDemand && r.is_image[pos - 1]) {
+      for (size_t g = 0; g < kv_->num_groups(); ++g) {
+        const LayerGroupSpec& grp = kv_->group(g);
+        if (grp.kind != LayerKind::kVisionEmbedding) continue;
+        GroupRuntime& rt = r.groups[g];
+        rt.consumed_ordinals++;
+        rt.consumed_held++;
+        const uint64_t t = grp.tokens_per_page;
+        while (rt.freed_blocks < rt.blocks.size() && rt.blocks[rt.freed_blocks].live &&
+               std::min(rt.stored, (rt.freed_blocks + 1) * t) <= rt.consumed_ordinals)
+          free_block(r, g, rt.freed_blocks, /*allow_cache=*/false, now);
+      }
+    }
   }
   refresh_mamba_checkpoints(id, now);
+  if (r.consumed >= r.prompt_len) finish_prefill(r, now);
   return done;
+}
+
+// reference simulator.cpp:484-502: the deferred out-of-window frees once the
+// prompt is written (a caller-held defer_window_free keeps them pending).
+void PageLists::finish_prefill(Request& r, uint64_t now) {
+  if (!r.suppress_window_free) return;
+  r.suppress_window_free = false;
+  if (r.defer_window_free) return;
+  apply_window_free(r.id, now);
+}
+
+// reference simulator.cpp:568-597
+void PageLists::rollback_newest(uint64_t id, size_t g, uint64_t count, uint64_t now) {
+  Request& r = req(id);
+  JENGA_CHECK(g < r.groups.size(), "group index out of range");
+  GroupRuntime& rt = r.groups[g];
+  const LayerGroupSpec& grp = kv_->group(g);
+  if (grp.kind == LayerKind::kMamba) {
+    const uint64_t drop = std::min(count, rt.stored);
+    rt.stored -= drop;
+    rt.stored_positions.resize(rt.stored);
+    return;
+  }
+  const uint64_t t = grp.tokens_per_page;
+  for (uint64_t i = 0; i < count && rt.stored > 0; ++i) {
+    const uint64_t bidx = (rt.stored - 1) / t;
+    rt.stored--;
+    rt.stored_positions.pop_back();
+    if (bidx < rt.blocks.size() && rt.blocks[bidx].live) {
+      rt.held_tokens--;
+      if (rt.stored <= bidx * t) {  // block emptied out: drop the page
+        kv_->type_allocator(g).touch(rt.blocks[bidx].page, now);
+        kv_->free(g, rt.blocks[bidx].page, std::nullopt);
+        rt.blocks[bidx].live = false;
+        rt.live_blocks--;
+        rt.blocks.pop_back();
+      }
+    }
+  }
+  while (!rt.chain.empty() && rt.chain.size() * t > rt.stored) rt.chain.pop_back();
+}
+
+// reference simulator.cpp:600-640
+bool PageLists::speculative_decode(uint64_t id, uint32_t propose_k, uint64_t accepted, const uint64_t* target_tokens,
+                                   uint64_t n_target, uint64_t now) {
+  JENGA_CHECK(accepted <= propose_k, "accepted more tokens than proposed");
+  JENGA_CHECK(n_target <= std::max<uint64_t>(accepted, 1), "more target tokens than max(accepted, 1)");
+  {
+    Request& r = req(id);
+    JENGA_CHECK(!r.needs_release, "decode after OOM: release (preempt) the request first");
+  }
+  for (uint32_t i = 1; i <= propose_k; ++i) {
+    const uint64_t pos = req(id).draft_len + i;
+    for (size_t g = 0; g < kv_->num_groups(); ++g) {
+      if (!draft_flags_[g]) continue;
+      if (!store_position(id, g, pos, now)) {
+        req(id).needs_release = true;
+        return false;
+      }
+    }
+  }
+  for (size_t g = 0; g < kv_->num_groups(); ++g)
+    if (draft_flags_[g]) rollback_newest(id, g, propose_k - accepted, now);
+  req(id).draft_len += accepted;
+  for (uint64_t j = 0; j < n_target; ++j) {
+    Request& r = req(id);
+    r.tokens.push_back(target_tokens ? target_tokens[j] : 0);
+    r.is_image.push_back(0);
+    r.image_ordinal.push_back(0);
+    const uint64_t pos = r.tokens.size();
+    for (size_t g = 0; g < kv_->num_groups(); ++g) {
+      if (draft_flags_[g]) continue;
+      if (!group_stores_position(g, req(id), pos)) continue;
+      if (!store_position(id, g, pos, now)) {
+        Request& rr = req(id);
+        rr.tokens.pop_back();
+        rr.is_image.pop_back();
+        rr.image_ordinal.pop_back();
+        rr.needs_release = true;
+        return false;
+      }
+    }
+  }
+  return true;
 }
 
 // reference simulator.cpp:347-358
@@ -326,6 +483,8 @@ void PageLists::release(uint64_t id, bool allow_cache, uint64_t now) {
   }
   r.groups.assign(kv_->num_groups(), GroupRuntime{});
   r.needs_release = false;
+  r.draft_len = 0;
+  r.suppress_window_free = false;
 }
 
 }  // namespace jenga

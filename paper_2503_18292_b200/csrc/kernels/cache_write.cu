@@ -70,6 +70,70 @@ __global__ void __launch_bounds__(256) paged_copy_kernel(const uint8_t* __restri
   for (; i < nvec; i += step) jenga_dev::st_v4(d + (i << 4), jenga_dev::ld_nc_v4(s + (i << 4)));
 }
 
+// Token rows <-> pages.  Row t (row_bytes) of the token at slot s = page*tpp +
+// off is cut into piece_bytes pieces; piece p sits in layer p / ppl, sub-slice
+// q = p % ppl of the page-layer layout:
+//     arena + start + layer*layer_stride + page*page_stride + (q*tpp + off)*piece_bytes
+// ppl = 1, piece = row: a vision-embedding group's own pages ([tpp][row]).
+// ppl = 2*Hkv, piece = D*e: the K|V, head rows reshape_and_cache will write
+// for that same token — the full_reuse overlay parks an embedding exactly in
+// its own token's unwritten KV bytes, so writing one token's KV never touches
+// another token's parked embedding.  One thread per 16-byte chunk.
+template <bool kScatter>
+__global__ void __launch_bounds__(256) token_rows_kernel(uint8_t* __restrict__ arena, uint64_t start_offset,
+                                                         uint64_t layer_stride, uint64_t page_stride, uint32_t tpp,
+                                                         uint32_t ppl, uint32_t piece_chunks, uint32_t row_chunks,
+                                                         uint8_t* __restrict__ rows, int64_t row_stride,
+                                                         const int64_t* __restrict__ slots, int n_tokens) {
+  const int64_t total = static_cast<int64_t>(n_tokens) * row_chunks;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(i / row_chunks);
+    const uint32_t c = static_cast<uint32_t>(i - static_cast<int64_t>(t) * row_chunks);
+    const uint32_t piece = c / piece_chunks, pc = c - piece * piece_chunks;
+    const uint32_t layer = piece / ppl, q = piece - layer * ppl;
+    uint8_t* row = rows + t * row_stride + (static_cast<int64_t>(c) << 4);
+    const int64_t slot = slots[t];
+    if (slot < 0) {
+      if (!kScatter) jenga_dev::st_v4(row, make_uint4(0, 0, 0, 0));
+      continue;
+    }
+    const int64_t page = slot / tpp, off = slot - page * tpp;
+    uint8_t* cell = arena + start_offset + layer * layer_stride + page * page_stride +
+                    ((static_cast<int64_t>(q) * tpp + off) * piece_chunks + pc) * 16;
+    if (kScatter)
+      jenga_dev::st_v4(cell, jenga_dev::ld_nc_v4(row));
+    else
+      jenga_dev::st_v4(row, jenga_dev::ld_nc_v4(cell));
+  }
+}
+
+int launch_token_rows(bool scatter, void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                      uint32_t pieces_per_layer, uint32_t piece_bytes, uint32_t tpp, void* rows, uint64_t row_bytes,
+                      int64_t row_stride_bytes, const int64_t* slots, int n_tokens, void* stream) {
+  using namespace jenga_dev;
+  const char* what = scatter ? "jenga_token_rows_scatter" : "jenga_token_rows_gather";
+  if (!arena_base || (n_tokens > 0 && (!rows || !slots)) || n_tokens < 0 || tpp == 0 || pieces_per_layer == 0 ||
+      piece_bytes == 0 || num_layers == 0 || row_bytes == 0)
+    return set_error(JENGA_ERR_ARG, std::string(what) + ": invalid arguments");
+  if (piece_bytes % 16 || row_bytes % piece_bytes || row_stride_bytes % 16 || view.start_offset % 16 ||
+      view.page_stride % 16 || view.exec_page_size % 16)
+    return set_error(JENGA_ERR_UNSUPPORTED, std::string(what) + ": pieces and rows must be 16-byte multiples");
+  if (static_cast<uint64_t>(pieces_per_layer) * tpp * piece_bytes > view.exec_page_size)
+    return set_error(JENGA_ERR_CONFIG, std::string(what) + ": pieces_per_layer*tpp*piece_bytes exceeds the layer slice");
+  if (row_bytes > static_cast<uint64_t>(num_layers) * pieces_per_layer * piece_bytes)
+    return set_error(JENGA_ERR_CONFIG, std::string(what) + ": row larger than the token's bytes in the group");
+  if (n_tokens == 0) return JENGA_OK;
+  const uint32_t row_chunks = static_cast<uint32_t>(row_bytes / 16);
+  const int64_t total = static_cast<int64_t>(n_tokens) * row_chunks;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  auto kern = scatter ? token_rows_kernel<true> : token_rows_kernel<false>;
+  kern<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint8_t*>(arena_base), view.start_offset, view.exec_page_size, view.page_stride, tpp,
+      pieces_per_layer, piece_bytes / 16, row_chunks, static_cast<uint8_t*>(rows), row_stride_bytes, slots, n_tokens);
+  return check_launch(scatter ? "token_rows_kernel<scatter>" : "token_rows_kernel<gather>");
+}
+
 int launch_paged_copy(const void* src_base, uint64_t src_off, uint64_t src_stride, const int64_t* src_idx,
                       void* dst_base, uint64_t dst_off, uint64_t dst_stride, const int64_t* dst_idx,
                       uint64_t bytes, int n, void* stream, const char* what) {
@@ -133,4 +197,20 @@ JENGA_EXPORT int jenga_page_copy(void* arena_base, uint64_t small_page_bytes, co
                                  const int64_t* dst_globals, int n_pages, void* stream) {
   return launch_paged_copy(arena_base, 0, small_page_bytes, src_globals, arena_base, 0, small_page_bytes,
                            dst_globals, small_page_bytes, n_pages, stream, "page_copy");
+}
+
+JENGA_EXPORT int jenga_token_rows_scatter(void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                                          uint32_t pieces_per_layer, uint32_t piece_bytes, uint32_t tokens_per_page,
+                                          const void* rows, uint64_t row_bytes, int64_t row_stride_bytes,
+                                          const int64_t* slot_mapping, int n_tokens, void* stream) {
+  return launch_token_rows(true, arena_base, view, num_layers, pieces_per_layer, piece_bytes, tokens_per_page,
+                           const_cast<void*>(rows), row_bytes, row_stride_bytes, slot_mapping, n_tokens, stream);
+}
+
+JENGA_EXPORT int jenga_token_rows_gather(const void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                                         uint32_t pieces_per_layer, uint32_t piece_bytes, uint32_t tokens_per_page,
+                                         void* rows, uint64_t row_bytes, int64_t row_stride_bytes,
+                                         const int64_t* slot_mapping, int n_tokens, void* stream) {
+  return launch_token_rows(false, const_cast<void*>(arena_base), view, num_layers, pieces_per_layer, piece_bytes,
+                           tokens_per_page, rows, row_bytes, row_stride_bytes, slot_mapping, n_tokens, stream);
 }

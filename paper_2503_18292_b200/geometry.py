@@ -27,7 +27,7 @@ class GroupGeometry:
     dtype: torch.dtype = torch.bfloat16
     tokens_per_page: int = 16
     window: int = 0
-    state_bytes: int = 0           # mamba: bytes of one layer's state
+    state_bytes: int = 0           # mamba: bytes of one layer's state; vision: embedding bytes per token
     checkpoint_interval: int = 512
 
     @property
@@ -36,7 +36,7 @@ class GroupGeometry:
 
     @property
     def bytes_per_token_per_layer(self) -> int:
-        if self.kind == LayerKind.kMamba:
+        if self.kind in (LayerKind.kMamba, LayerKind.kVisionEmbedding):
             return self.state_bytes
         return 2 * self.num_kv_heads * self.head_dim * _DTYPE_BYTES[self.dtype]
 

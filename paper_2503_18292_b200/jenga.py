@@ -9,6 +9,7 @@ exception types (ConfigError / InvariantError).
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import enum
 import json
 from dataclasses import dataclass, field
@@ -139,6 +140,16 @@ class ModelSpec:
     def validate(self) -> None:
         with self._native() as s:
             check(lib.jenga_spec_validate(s.h))
+
+    def combine_with_draft(self, draft: "ModelSpec") -> "ModelSpec":
+        """reference combine_with_draft (simulator.cpp:32-41): target groups then
+        the draft's renamed "draft.<name>", validated natively (one LCM pool)."""
+        with self._native() as t, draft._native() as d:
+            h = C.c_void_p()
+            check(lib.jenga_spec_combine_with_draft(t.h, d.h, C.byref(h)))
+            lib.jenga_spec_destroy(h)
+        groups = list(self.groups) + [dataclasses.replace(g, name="draft." + g.name) for g in draft.groups]
+        return ModelSpec(self.name + "+draft", groups)
 
     def has_cross_attention(self) -> bool:
         return any(g.kind == LayerKind.kCrossAttention for g in self.groups)
@@ -424,10 +435,13 @@ class PageLists:
         img = None if is_image is None else np.ascontiguousarray(np.asarray(is_image, dtype=np.uint8))
         ordn = None if image_ordinals is None else np.ascontiguousarray(np.asarray(image_ordinals, dtype=np.uint64))
         hit = C.c_uint64()
-        check(lib.jenga_pages_admit(self.h, request, t.ctypes.data_as(C.POINTER(C.c_uint64)),
-                                    None if img is None else img.ctypes.data_as(C.POINTER(C.c_uint8)),
-                                    None if ordn is None else ordn.ctypes.data_as(C.POINTER(C.c_uint64)),
-                                    len(t), now, C.byref(hit)))
+        rc = lib.jenga_pages_admit(self.h, request, t.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                   None if img is None else img.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                   None if ordn is None else ordn.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                   len(t), now, C.byref(hit))
+        if rc == _lib.JENGA_ERR_OOM:  # vision / full_reuse stores ran out: release the request
+            raise OutOfMemory(_lib.last_error())
+        check(rc)
         return hit.value
 
     def prefill(self, request: int, budget: int, now: int = 0):
@@ -455,6 +469,39 @@ class PageLists:
 
     def apply_window_free(self, request: int, now: int = 0) -> None:
         check(lib.jenga_pages_apply_window_free(self.h, request, now))
+
+    ON_DEMAND, FULL_REUSE = 0, 1
+
+    def set_vision_mode(self, mode) -> None:
+        """reference EngineConfig::vision_mode: 0/"on_demand", 1/"full_reuse"."""
+        if isinstance(mode, str):
+            mode = {"on_demand": 0, "full_reuse": 1}[mode]
+        check(lib.jenga_pages_set_vision_mode(self.h, int(mode)))
+
+    def rollback_newest(self, request: int, g: int, count: int, now: int = 0) -> None:
+        """reference rollback_newest (simulator.cpp:568-597)."""
+        check(lib.jenga_pages_rollback_newest(self.h, request, g, count, now))
+
+    def speculative_decode(self, request: int, propose_k: int, accepted: int, target_tokens=None,
+                           n_target: Optional[int] = None, now: int = 0) -> bool:
+        """reference speculative_decode_one (simulator.cpp:600-640). False on OOM."""
+        if n_target is None:
+            n_target = max(accepted, 1) if target_tokens is None else len(target_tokens)
+        tok = None
+        if target_tokens is not None:
+            tok = np.ascontiguousarray(np.asarray(target_tokens, dtype=np.uint64))
+        rc = lib.jenga_pages_speculative_decode(self.h, request, propose_k, accepted,
+                                                None if tok is None else tok.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                n_target, now)
+        if rc == _lib.JENGA_ERR_OOM:
+            return False
+        check(rc)
+        return True
+
+    def is_draft_group(self, g: int) -> bool:
+        v = C.c_int()
+        check(lib.jenga_pages_is_draft_group(self.h, g, C.byref(v)))
+        return bool(v.value)
 
     def seq_len(self, request: int) -> int:
         n = C.c_uint64()

@@ -174,6 +174,33 @@ def page_copy(arena: Arena, small_page_bytes: int, src_globals: torch.Tensor, ds
                               src_globals.numel(), _stream()))
 
 
+def _token_rows(scatter: bool, arena: Arena, view: LayerView, num_layers: int, pieces_per_layer: int,
+                piece_bytes: int, tokens_per_page: int, rows: torch.Tensor, slot_mapping: torch.Tensor) -> None:
+    _need(slot_mapping, torch.int64, "slot_mapping")
+    if rows.dim() != 2 or rows.stride(1) != 1:
+        raise ValueError("rows must be [T, row_elems] with contiguous rows")
+    if rows.shape[0] != slot_mapping.numel():
+        raise ValueError("one slot per row")
+    e = rows.element_size()
+    fn = lib.jenga_token_rows_scatter if scatter else lib.jenga_token_rows_gather
+    check(fn(arena.base, view.c(), num_layers, pieces_per_layer, piece_bytes, tokens_per_page, _ptr(rows),
+             rows.shape[1] * e, rows.stride(0) * e, _ptr(slot_mapping), rows.shape[0], _stream()))
+
+
+def token_rows_scatter(arena: Arena, view: LayerView, num_layers: int, pieces_per_layer: int, piece_bytes: int,
+                       tokens_per_page: int, rows: torch.Tensor, slot_mapping: torch.Tensor) -> None:
+    """Rows [T, bytes] -> pages (vision-embedding pages; pieces_per_layer=2*Hkv,
+    piece_bytes=D*e parks them in the token's own unwritten KV bytes)."""
+    _token_rows(True, arena, view, num_layers, pieces_per_layer, piece_bytes, tokens_per_page, rows, slot_mapping)
+
+
+def token_rows_gather(arena: Arena, view: LayerView, num_layers: int, pieces_per_layer: int, piece_bytes: int,
+                      tokens_per_page: int, rows: torch.Tensor, slot_mapping: torch.Tensor) -> torch.Tensor:
+    """Pages -> rows [T, bytes] (negative slots read as zeros)."""
+    _token_rows(False, arena, view, num_layers, pieces_per_layer, piece_bytes, tokens_per_page, rows, slot_mapping)
+    return rows
+
+
 def kernel_launch_count() -> int:
     return int(lib.jenga_kernel_launch_count())
 

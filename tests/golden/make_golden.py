@@ -229,6 +229,104 @@ def sim_pages(ref):
     return out
 
 
+def _snapshot(sim, reqs, ng, step):
+    snap = {"step": step, "requests": []}
+    for r in reqs:
+        rq = sim.request(r["id"])
+        toks, img = sim.tokens(r["id"])
+        groups = []
+        for g in range(ng):
+            st = sim.group_state(r["id"], g)
+            groups.append({"pages": st["pages"].tolist(), "live": st["live"].astype(int).tolist(),
+                           "stored": st["stored"], "freed": st["freed"],
+                           "working": None if st["working"] is None else [int(x) for x in st["working"]]})
+        snap["requests"].append({"id": r["id"], "phase": rq["phase"], "seq_len": rq["seq_len"],
+                                 "consumed": rq["consumed"], "tokens": [str(int(t)) for t in toks],
+                                 "is_image": img.astype(int).tolist(), "groups": groups})
+    return snap
+
+
+VISION_MODELS = {
+    # cross-attention VLM: images stored by the cross group only
+    "mllama_vis": spec_json("mllama-vis", [
+        {"name": "self", "kind": "full", "num_layers": 4, "bytes_per_token_per_layer": 128, "tokens_per_page": 4},
+        {"name": "cross", "kind": "cross_attention", "num_layers": 2, "bytes_per_token_per_layer": 128,
+         "tokens_per_page": 4},
+        {"name": "vision", "kind": "vision_embedding", "num_layers": 1, "bytes_per_token_per_layer": 320,
+         "tokens_per_page": 3}]),
+    # decoder-only VLM (llava-style): the decoder stores image tokens too
+    "llava_vis": spec_json("llava-vis", [
+        {"name": "self", "kind": "full", "num_layers": 3, "bytes_per_token_per_layer": 128, "tokens_per_page": 4},
+        {"name": "window", "kind": "sliding_window", "num_layers": 2, "bytes_per_token_per_layer": 128,
+         "window_tokens": 24, "tokens_per_page": 4},
+        {"name": "vision", "kind": "vision_embedding", "num_layers": 1, "bytes_per_token_per_layer": 512,
+         "tokens_per_page": 2}]),
+}
+
+
+def sim_vision(ref):
+    """Reference SimEngine in both vision modes (simulator.cpp:453-476,
+    504-547): on_demand frees consumed embeddings, full_reuse allocates the
+    whole prompt at admission."""
+    out = []
+    for model, mode, budget, chunk, reqs, checkpoints in (
+            ("mllama_vis", 0, 64 << 20, 16,
+             [{"id": i, "segments": [[0, 5], [1, 21 + 3 * i], [0, 9], [1, 7]], "output": 12} for i in range(3)],
+             [1, 2, 3, 5, 8, 14]),
+            ("mllama_vis", 1, 64 << 20, 16,
+             [{"id": i, "segments": [[0, 5], [1, 21 + 3 * i], [0, 9]], "output": 12} for i in range(3)],
+             [1, 2, 4, 7, 14]),
+            ("llava_vis", 0, 64 << 20, 20,
+             [{"id": i, "segments": [[0, 3 + i], [1, 30], [0, 11]], "output": 40} for i in range(3)],
+             [1, 2, 3, 6, 12, 40]),
+            ("llava_vis", 1, 64 << 20, 20,
+             [{"id": i, "segments": [[0, 3 + i], [1, 30], [0, 11]], "output": 40} for i in range(3)],
+             [1, 2, 3, 6, 12, 40])):
+        s = ref.spec(VISION_MODELS[model])
+        sim = RefSim(s, budget, chunk, False, reqs, vision_mode=mode)
+        ng = len(json.loads(VISION_MODELS[model])["groups"])
+        snaps, step = [], 0
+        for target in checkpoints:
+            while step < target and not sim.done():
+                sim.step()
+                step += 1
+            snaps.append(_snapshot(sim, reqs, ng, step))
+        out.append({"model": model, "spec": json.loads(VISION_MODELS[model]), "vision_mode": mode,
+                    "budget": budget, "chunk": chunk, "requests": reqs, "snapshots": snaps})
+    return out
+
+
+def sim_spec(ref):
+    """Reference SimEngine with a speculative config (simulator.cpp:32-41,
+    568-640): draft groups in the same LCM pool, rollback of rejections."""
+    from oracle.oracle import spec_accept_draws
+    draft = spec_json("draft", [
+        {"name": "self", "kind": "full", "num_layers": 1, "bytes_per_token_per_layer": 64, "tokens_per_page": 4}])
+    out = []
+    for model, k, acc, seed, reqs, checkpoints in (
+            ("window", 4, 0.7, 11, [{"id": i, "segments": [[0, 19 + 9 * i]], "output": 60} for i in range(4)],
+             [2, 5, 9, 17, 30]),
+            ("window", 3, 0.0, 12, [{"id": i, "segments": [[0, 30 + i]], "output": 25} for i in range(3)],
+             [2, 6, 15]),
+            ("window", 5, 1.0, 13, [{"id": i, "segments": [[0, 13 + i]], "output": 33} for i in range(2)],
+             [2, 4, 8])):
+        s = ref.spec(SIM_MODELS[model])
+        d = ref.spec(draft)
+        sim = RefSim(s, 64 << 20, 32, False, reqs, draft=d, propose_k=k, acceptance=acc, seed=seed)
+        ng = len(json.loads(SIM_MODELS[model])["groups"]) + 1
+        snaps, step = [], 0
+        for target in checkpoints:
+            while step < target and not sim.done():
+                sim.step()
+                step += 1
+            snaps.append(_snapshot(sim, reqs, ng, step))
+        draws = {str(r["id"]): spec_accept_draws(ref, seed, r["id"], k, acc, 200) for r in reqs}
+        out.append({"model": model, "spec": json.loads(SIM_MODELS[model]), "draft": json.loads(draft),
+                    "propose_k": k, "acceptance": acc, "seed": seed, "budget": 64 << 20, "chunk": 32,
+                    "requests": reqs, "draws": draws, "snapshots": snaps})
+    return out
+
+
 PREFIX_MODELS = {
     "window": spec_json("win", [
         {"name": "self", "kind": "full", "num_layers": 2, "bytes_per_token_per_layer": 64, "tokens_per_page": 4},
@@ -293,7 +391,8 @@ def main():
         raise SystemExit("reference library unavailable: build oracle/_ref first (oracle/build_oracle.py)")
     for name, fn in (("fig6.json", fig6), ("configs.json", configs), ("random_geometries.json", random_geometries),
                      ("alloc_sequences.json", alloc_sequences), ("policies.json", policies),
-                     ("sim_pages.json", sim_pages), ("sim_prefix.json", sim_prefix)):
+                     ("sim_pages.json", sim_pages), ("sim_prefix.json", sim_prefix),
+                     ("sim_vision.json", sim_vision), ("sim_spec.json", sim_spec)):
         data = fn(ref)
         with open(OUT / name, "w") as f:
             json.dump(data, f, separators=(",", ":"))

@@ -183,3 +183,37 @@ def test_oracle_reshape_and_cache_roundtrip(orc):
             vr = base + ((1 * hkv + h) * tpp + off) * d * e
             np.testing.assert_array_equal(arena[kr:kr + d * e].view(np.float32), K[t, h])
             np.testing.assert_array_equal(arena[vr:vr + d * e].view(np.float32), V[t, h])
+
+
+def test_oracle_token_rows_overlay_is_reshape_layout(orc):
+    """The full_reuse overlay mapping (pieces_per_layer = 2*Hkv, piece = D*e)
+    puts row bytes exactly where reshape_and_cache puts that token's K|V, so
+    parking an embedding never touches another token's bytes; gather inverts
+    scatter for both layouts."""
+    rng = np.random.default_rng(9)
+    hkv, d, tpp, e, layers = 2, 16, 4, 4, 3
+    per_layer = 2 * hkv * tpp * d * e
+    stride = layers * per_layer + 64
+    arena = rng.integers(0, 256, 8 * stride, dtype=np.uint8)
+    slots = np.array([0, 5, 31, -1, 13, 6], dtype=np.int64)
+    kv = rng.standard_normal((len(slots), 2, hkv, d)).astype(np.float32)
+    rows = kv.reshape(len(slots), -1).view(np.uint8)
+    a1, a2 = arena.copy(), arena.copy()
+    orc.reshape_and_cache(a1, (per_layer, stride, per_layer), F32, hkv, d, tpp, kv[:, 0], kv[:, 1], slots)
+    orc.token_rows_scatter(a2, (per_layer, stride, per_layer), 2 * hkv, d * e, tpp, rows, slots)
+    np.testing.assert_array_equal(a1, a2)
+    # rows spanning several layers round-trip; negative slots gather zeros
+    big = rng.integers(0, 256, (len(slots), 2 * per_layer // tpp), dtype=np.uint8)
+    orc.token_rows_scatter(a2, (0, stride, per_layer), 2 * hkv, d * e, tpp, big, slots)
+    back = orc.token_rows_gather(a2, (0, stride, per_layer), 2 * hkv, d * e, tpp, big.shape[1], slots)
+    want = big.copy()
+    want[slots < 0] = 0
+    np.testing.assert_array_equal(back, want)
+    # vision-group layout: one piece per layer
+    emb = rng.integers(0, 256, (len(slots), 48), dtype=np.uint8)
+    orc.token_rows_scatter(a2, (16, stride, 48 * tpp), 1, 48, tpp, emb, slots)
+    for t, s in enumerate(slots):
+        if s >= 0:
+            page, off = divmod(int(s), tpp)
+            at = 16 + page * stride + off * 48
+            np.testing.assert_array_equal(a2[at:at + 48], emb[t])
