@@ -309,7 +309,8 @@ int jenga_slot_mapping(const int32_t* block_table, int max_blocks, const int32_t
                        int64_t* slot_mapping, void* stream);
 
 /* Intra-slice layout (documented in DESIGN.md): one layer's slice of one small
- * page is [K|V][Hkv][tpp][D] of dtype — exec_page_size = 2*Hkv*D*e*tpp.
+ * page is [Hkv][K|V][tpp][D] of dtype (head-major: head h's K rows, then its
+ * V rows) — exec_page_size = 2*Hkv*D*e*tpp.
  * Scatter K/V[T][Hkv][D] (row stride kv_row_stride elements between tokens)
  * into their slots; slot < 0 skips. */
 int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view, int dtype,

@@ -152,11 +152,12 @@ static inline double ld_elem(const uint8_t* p, int dtype) {
 
 static inline int dtype_size(int dtype) { return dtype == ORC_F32 ? 4 : 2; }
 
-/* Slice layout of one (small page, layer): [K|V][Hkv][tpp][D] of dtype, so
+/* Slice layout of one (small page, layer): [Hkv][K|V][tpp][D] of dtype, so
  * exec_page_size = 2*Hkv*tpp*D*e (memory_layout.cpp:16-17 sizes it as
  * bytes_per_token_per_layer*tpp with bptl = 2*Hkv*D*e). */
 static inline int64_t slice_row(int kv, int h, int hkv, int tpp, int off) {
-  return (((int64_t)kv * hkv + h) * tpp + off);
+  (void)hkv;
+  return (((int64_t)h * 2 + kv) * tpp + off);
 }
 
 /* reshape_and_cache: row t of K/V -> slot s = page*tpp + off. */

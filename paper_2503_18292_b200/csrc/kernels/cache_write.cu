@@ -3,9 +3,10 @@
 //
 // Slot layout inside one layer's slice of a small page (our definition of the
 // bytes the reference only sizes, memory_layout.cpp:16-17):
-//     slice = [K | V] x [Hkv] x [tpp] x [D]   (exec_page_size = 2*Hkv*tpp*D*e)
-// so token `off` of head h is one contiguous D*e row, and a (page, head)
-// chunk of tpp rows is contiguous for bulk copies.  Source and destination
+//     slice = [Hkv] x [K | V] x [tpp] x [D]   (exec_page_size = 2*Hkv*tpp*D*e)
+// head-major: token `off` of head h is one contiguous D*e row, and one
+// head's K and V tiles of a page are a single contiguous 2*tpp*D*e run (the
+// DRAM-locality choice measured in profiles/r01_sweeps.md).  Source and destination
 // rows are both contiguous, so one warp moves a 256..512-B row with 16-B
 // vector stores — fully coalesced on both sides.
 #include "common.cuh"
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(256) reshape_and_cache_kernel(
     const uint8_t* src = (kv ? value : key) + t * token_stride_bytes + static_cast<int64_t>(h) * row_bytes +
                          (c << 4);
     uint8_t* dst = arena + start_offset + page * page_stride +
-                   ((static_cast<int64_t>(kv) * hkv + h) * tpp + off) * row_bytes + (c << 4);
+                   ((static_cast<int64_t>(h) * 2 + kv) * tpp + off) * row_bytes + (c << 4);
     jenga_dev::st_v4(dst, jenga_dev::ld_nc_v4(src));
   }
 }

@@ -4,8 +4,8 @@
 // PAPER.md:830-838): a layer is {start_offset, page_stride, exec_page_size}
 // and a block table of AddressMap global page indices; the bytes of (page,
 // layer) start at arena + start_offset + global*page_stride.  Inside the
-// slice K/V are [K|V][Hkv][tpp][D] (cache_write.cu), so the tpp rows of one
-// (page, head) are contiguous and move with one bulk copy.
+// slice K/V are [Hkv][K|V][tpp][D] (cache_write.cu), so the tpp K rows and
+// then the tpp V rows of one (page, head) are contiguous bulk copies.
 //
 // Liveness follows LayerPolicy::needs_token (layer_policies.cpp:105-120):
 // full / cross attend ordinals 1..n; sliding window attends i + W > n, i.e.
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(kThreads) paged_decode_kernel(const DecodePara
   __syncthreads();
 
   const int64_t head_chunk = static_cast<int64_t>(p.tpp) * ROW;  // bytes of one (page, head) K chunk
-  const int64_t v_offset = static_cast<int64_t>(p.hkv) * head_chunk;
-  const uint8_t* layer_base = p.arena + p.start_offset + static_cast<int64_t>(h) * head_chunk;
+  const int64_t v_offset = head_chunk;  // head-major slice: [Hkv][K|V][tpp][D]
+  const uint8_t* layer_base = p.arena + p.start_offset + static_cast<int64_t>(h) * 2 * head_chunk;
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
   if (warp == kConsumerWarps) {

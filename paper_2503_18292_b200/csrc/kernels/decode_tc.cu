@@ -6,12 +6,12 @@
 //  * K/V tiles move with 2-D TMA tensor loads (cp.async.bulk.tensor -> UTMALDG)
 //    over the whole arena viewed as a [rows][D] matrix, rows = one token of
 //    one (page, layer, K|V, head): row index = (start_offset + global*
-//    page_stride + (h*tpp + off)*D*e) / (D*e).  Boxes of 64 x 16 land in
+//    page_stride + ((2h + kv)*tpp + off)*D*e) / (D*e).  Boxes of 64 x 16 land in
 //    shared memory with the 128-byte swizzle, so ldmatrix is conflict-free.
 //  * One CTA serves HG KV heads of a request: a pipeline stage holds the same
-//    16-token tile of all HG heads, which are adjacent in the page-layer slice
-//    ([K|V][Hkv][tpp][D]), so each stage is one contiguous HG x 8 KiB run of K
-//    and one of V.  Long contiguous runs keep DRAM row locality high under the
+//    16-token tile of all HG heads, which are adjacent in the head-major
+//    page-layer slice ([Hkv][K|V][tpp][D]), so each stage is one contiguous
+//    HG x 16 KiB run of K and V.  Long contiguous runs keep DRAM row locality high under the
 //    page-layer layout, where one layer is only a 128 KiB slice of every
 //    2.75 MiB page (measured: the busiest DRAM channels idle ~18% with 8 KiB
 //    runs).
@@ -257,8 +257,9 @@ __device__ __forceinline__ void head_store(HeadState<D>& st, float* s_acc, float
   }
 }
 
-// TMA loads of one tile (16 tokens) of HG heads into a stage:
-// K of heads h0..h0+HG-1 in address order, then V — two contiguous runs.
+// TMA loads of one tile (16 tokens) of HG heads into a stage: K of heads
+// h0..h0+HG-1, then their V (head-major slice: head h's K rows at 2*h*tpp,
+// its V rows tpp later).
 template <int D, int HG>
 __device__ __forceinline__ void load_stage(const CUtensorMap* tmap, uint8_t* stage, uint64_t* bar, int32_t row,
                                            int tpp, int v_rows, uint64_t policy) {
@@ -269,20 +270,20 @@ __device__ __forceinline__ void load_stage(const CUtensorMap* tmap, uint8_t* sta
   for (int hl = 0; hl < HG; ++hl)
 #pragma unroll
     for (int bx = 0; bx < NBOX; ++bx)
-      jenga_dev::tma_load_2d(stage + hl * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols, row + hl * tpp, bar,
-                             policy);
+      jenga_dev::tma_load_2d(stage + hl * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols, row + hl * 2 * tpp,
+                             bar, policy);
 #pragma unroll
   for (int hl = 0; hl < HG; ++hl)
 #pragma unroll
     for (int bx = 0; bx < NBOX; ++bx)
       jenga_dev::tma_load_2d(stage + (HG + hl) * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols,
-                             row + v_rows + hl * tpp, bar, policy);
+                             row + v_rows + hl * 2 * tpp, bar, policy);
 }
 
 // Arena row of the first K row of (page of token tok0, head h0).
 __device__ __forceinline__ int32_t tile_row(const DecodeParams& p, const int32_t* table, int h0, int tok0,
                                             int64_t row_bytes) {
-  const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h0) * p.tpp;
+  const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h0) * 2 * p.tpp;
   const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
   return static_cast<int32_t>(base_row + static_cast<int64_t>(table[tok0 / p.tpp]) * page_rows + tok0 % p.tpp);
 }
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
     if (lane == 0) {  // producer: one elected lane
       jenga_dev::prefetch_tmap(&tmap);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int v_rows = p.hkv * p.tpp;
+      const int v_rows = p.tpp;
       bool waited = false;
       for (int it = 0; it < wk.t_count; ++it) {
         const int st = it % NS;
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
     if (lane == 0) {  // producer: fetch items, stream their tiles
       jenga_dev::prefetch_tmap(&tmap);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int v_rows = p.hkv * p.tpp;
+      const int v_rows = p.tpp;
       int seq = 0;
       for (int ic = 0;; ++ic) {
         const int j = ic % kItemSlots;

@@ -165,9 +165,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tma_load_3d(qs + bx * Q_BOX, &q_map, bx * kBoxCols, h * G, p.cu_q[b] + t0, q_full);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
       const int64_t row_bytes = D * 2;
-      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * p.tpp;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
       const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
-      const int v_rows = p.hkv * p.tpp;
+      const int v_rows = p.tpp;  // head-major slice
       for (int it = 0; it < ntiles; ++it) {
         const int st = it % NS;
         if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);

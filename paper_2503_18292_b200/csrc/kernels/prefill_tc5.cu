@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       jenga_dev::prefetch_tmap(&kv_map);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
       const int64_t row_bytes = D * 2;
-      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * p.tpp;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
       const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
-      const int v_rows = p.hkv * p.tpp;
+      const int v_rows = p.tpp;  // head-major slice
       for (int j = 0; j < ntiles; ++j) {
         const int st = j % NS;
         if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);

@@ -95,8 +95,8 @@ def _np_attention(arena, view, kind, window, q, table, seq_lens, hq, hkv, d, tpp
             pages = table[b, toks // tpp]
             offs = toks % tpp
             base = view[0] + pages.astype(np.int64) * view[1]
-            krow = base + ((0 * hkv + h) * tpp + offs) * d * e
-            vrow = base + ((1 * hkv + h) * tpp + offs) * d * e
+            krow = base + ((2 * h + 0) * tpp + offs) * d * e  # head-major slice
+            vrow = base + ((2 * h + 1) * tpp + offs) * d * e
             K = np.stack([_decode(arena[r:r + d * e], dtype) for r in krow])
             V = np.stack([_decode(arena[r:r + d * e], dtype) for r in vrow])
             for g in range(G):
@@ -179,8 +179,8 @@ def test_oracle_reshape_and_cache_roundtrip(orc):
         page, off = divmod(int(s), tpp)
         base = view[0] + page * stride
         for h in range(hkv):
-            kr = base + ((0 * hkv + h) * tpp + off) * d * e
-            vr = base + ((1 * hkv + h) * tpp + off) * d * e
+            kr = base + ((2 * h + 0) * tpp + off) * d * e  # head-major [Hkv][K|V][tpp][D]
+            vr = base + ((2 * h + 1) * tpp + off) * d * e
             np.testing.assert_array_equal(arena[kr:kr + d * e].view(np.float32), K[t, h])
             np.testing.assert_array_equal(arena[vr:vr + d * e].view(np.float32), V[t, h])
 
@@ -196,10 +196,11 @@ def test_oracle_token_rows_overlay_is_reshape_layout(orc):
     stride = layers * per_layer + 64
     arena = rng.integers(0, 256, 8 * stride, dtype=np.uint8)
     slots = np.array([0, 5, 31, -1, 13, 6], dtype=np.int64)
-    kv = rng.standard_normal((len(slots), 2, hkv, d)).astype(np.float32)
+    kv = rng.standard_normal((len(slots), hkv, 2, d)).astype(np.float32)  # row = [h0 K, h0 V, h1 K, ...]
     rows = kv.reshape(len(slots), -1).view(np.uint8)
     a1, a2 = arena.copy(), arena.copy()
-    orc.reshape_and_cache(a1, (per_layer, stride, per_layer), F32, hkv, d, tpp, kv[:, 0], kv[:, 1], slots)
+    orc.reshape_and_cache(a1, (per_layer, stride, per_layer), F32, hkv, d, tpp, np.ascontiguousarray(kv[:, :, 0]),
+                          np.ascontiguousarray(kv[:, :, 1]), slots)
     orc.token_rows_scatter(a2, (per_layer, stride, per_layer), 2 * hkv, d * e, tpp, rows, slots)
     np.testing.assert_array_equal(a1, a2)
     # rows spanning several layers round-trip; negative slots gather zeros
