@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--tpp", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly instead of one CUDA graph "
+                                                          "per step")
     p.add_argument("--layers-per-group", type=int, default=21)
     return p.parse_args()
 
@@ -231,10 +233,19 @@ def run_ours(a, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     bptl = 2 * Hkv * D * 2
     slot = {i: j for j, (i, _, _) in enumerate(attn)}
+    attn_layers_per_group = {}
+    for _, g, _ in attn:
+        attn_layers_per_group[g] = attn_layers_per_group.get(g, 0) + 1
 
-    def step(ev=None):
+    def host_step():
+        """Host half of a step: allocator append + CSR pack into pinned memory."""
         eng.append()
-        eng.sync_tables()
+        return eng.pack_tables()
+
+    def device_step(totals=None, ev=None, hooks=None):
+        """Device half: table upload/build, then per layer KV write + decode
+        (fixed shape when totals is None, so it can be graph-captured)."""
+        eng.upload_tables(None, totals)
         pg = {}
         for i, (g, l) in enumerate(wl.layers):
             kind = eng.tables[g].geom.kind
@@ -246,6 +257,8 @@ def run_ours(a, rank, world, local_rank):
                 ops.mamba_state_scatter(eng.arena, v, pg[g], state)  # (SSM update out of scope)
                 continue
             j = slot[i]
+            if hooks is not None:
+                hooks["before"](j)
             if kind != LayerKind.kCrossAttention:  # cross KV (image tokens) is static during decode
                 eng.write_kv(g, l, kn[j], vn[j])
             if ev is not None:
@@ -253,19 +266,48 @@ def run_ours(a, rank, world, local_rank):
             eng.decode(g, l, q[j], out[j])
             if ev is not None:
                 ev[j][1].record(stream)
+            if hooks is not None:
+                hooks["after"](j)
+
+    def step(ev=None, hooks=None):
+        device_step(host_step(), ev, hooks)
+
+    graph = None
+    per_replay = 0
+    if not a.no_graph:
+        # capture the device half once (after warm-up: tensor maps, smem
+        # attributes); each step then = host append + pack + one graph launch
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        host_step()
+        c0 = ops.kernel_launch_count()
+        with torch.cuda.graph(graph):
+            device_step()
+        per_replay = ops.kernel_launch_count() - c0
+        graph.replay()
+        torch.cuda.synchronize()
+
+    def timed_step():
+        if graph is None:
+            step()
+        else:
+            host_step()
+            graph.replay()
 
     def step_bytes():
         """(KV bytes read by decode, Mamba state bytes moved) for this step."""
         kv = 0
-        for _, g, _ in attn:
-            kv += int(eng.live_tokens(g).sum()) * bptl
+        for g, n_layers in attn_layers_per_group.items():  # one host read per group, not per layer
+            kv += int(eng.live_tokens(g).sum()) * bptl * n_layers
         st = 0
         for _, g, l in mamba:
             st += 2 * B * eng.view(g, l).exec_page_size
         return kv, st
 
     for _ in range(a.warmup):
-        step()
+        timed_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -277,13 +319,13 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
     start.record(stream)
     for s in range(a.steps):
-        step()  # no per-layer events here: they would break programmatic (PDL) overlap
+        timed_step()  # no per-layer events here: they would break programmatic (PDL) overlap
         kb, sb = step_bytes()
         kv_bytes += kb
         st_bytes += sb
     end.record(stream)
     torch.cuda.synchronize()
-    launches = ops.kernel_launch_count() - launches0
+    launches = ops.kernel_launch_count() - launches0 + (a.steps * per_replay if graph is not None else 0)
     ms = start.elapsed_time(end)
     # per-launch decode durations: a short pass right after, with events
     # bracketing every paged-decode launch on its stream
@@ -318,13 +360,60 @@ def run_ours(a, rank, world, local_rank):
         hk.copy_(kn)
         hv.copy_(vn)
 
+        # Copies ride a side stream in layer chunks: chunk c+1's inputs land
+        # while chunk c decodes, chunk c's outputs leave as soon as it is done
+        # (one cross-stream wait per chunk keeps PDL chaining inside chunks).
+        cs = torch.cuda.Stream(device=dev)
+        # geometric chunks: the first layer waits only for its own inputs, the
+        # last layer's outputs leave alone (short start-up and drain)
+        grow = [0]
+        while grow[-1] < na:
+            grow.append(min(na, 2 * grow[-1] + 1))
+        in_bounds = grow
+        out_bounds = sorted({na - x for x in grow})
+        ev_in = [torch.cuda.Event() for _ in range(len(in_bounds) - 1)]
+        ev_out = [torch.cuda.Event() for _ in range(len(out_bounds) - 1)]
+        in_start = {in_bounds[c]: c for c in range(len(in_bounds) - 1)}
+        out_end = {out_bounds[c + 1] - 1: c for c in range(len(out_bounds) - 1)}
+
+        def e2e_device(totals):
+            cs.wait_stream(torch.cuda.current_stream())  # previous step's readers of q/k/v are done
+            with torch.cuda.stream(cs):
+                for c in range(len(in_bounds) - 1):
+                    lo, hi = in_bounds[c], in_bounds[c + 1]
+                    q[lo:hi].copy_(hq[lo:hi], non_blocking=True)
+                    kn[lo:hi].copy_(hk[lo:hi], non_blocking=True)
+                    vn[lo:hi].copy_(hv[lo:hi], non_blocking=True)
+                    ev_in[c].record(cs)
+            cur = torch.cuda.current_stream()
+            chunk_hooks = {"before": lambda j: cur.wait_event(ev_in[in_start[j]]) if j in in_start else None,
+                           "after": lambda j: ev_out[out_end[j]].record(cur) if j in out_end else None}
+            device_step(totals, hooks=chunk_hooks)
+            for c in range(len(out_bounds) - 1):
+                cs.wait_event(ev_out[c])
+                with torch.cuda.stream(cs):
+                    lo, hi = out_bounds[c], out_bounds[c + 1]
+                    ho[lo:hi].copy_(out[lo:hi], non_blocking=True)
+            cur.wait_stream(cs)
+
+        e2e_graph = None
+        if graph is not None:
+            host_step()
+            e2e_graph = torch.cuda.CUDAGraph()
+            c0 = ops.kernel_launch_count()
+            with torch.cuda.graph(e2e_graph):
+                e2e_device(None)
+            e2e_per_replay = ops.kernel_launch_count() - c0
+            e2e_graph.replay()
+            torch.cuda.synchronize()
+
         def e2e_step():
-            q.copy_(hq, non_blocking=True)
-            kn.copy_(hk, non_blocking=True)
-            vn.copy_(hv, non_blocking=True)
-            step()
-            ho.copy_(out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()  # the caller reads the step's result
+            if e2e_graph is None:
+                e2e_device(host_step())
+            else:
+                host_step()
+                e2e_graph.replay()
+            stream.synchronize()  # the caller reads the step's result
         for _ in range(a.warmup):
             e2e_step()
         if world > 1:

@@ -106,8 +106,15 @@ class DecodeEngine:
     # ------------------------------------------------------------ device tables
     def sync_tables(self, groups: Optional[Sequence[int]] = None) -> None:
         """Pack page lists -> pinned -> H2D (async) -> device block-table build."""
+        totals = self.pack_tables(groups)
+        self.upload_tables(groups, totals)
+
+    def pack_tables(self, groups: Optional[Sequence[int]] = None) -> Dict[int, int]:
+        """Host half: CSR page lists of the batch into the pinned buffers.
+        Returns the page count per group."""
         n = len(self.requests)
         rp = self._req_arr.ctypes.data_as(C.POINTER(C.c_uint64))
+        totals = {}
         for g in (range(len(self.tables)) if groups is None else groups):
             t = self.tables[g]
             check(lib.jenga_pages_pack_csr(
@@ -118,6 +125,18 @@ class DecodeEngine:
             total = int(t.h_offsets[n])
             if total > t.h_pages.shape[0]:
                 raise OverflowError("page lists exceed the table capacity (raise max_tokens)")
+            totals[g] = total
+        return totals
+
+    def upload_tables(self, groups: Optional[Sequence[int]] = None, totals: Optional[Dict[int, int]] = None) -> None:
+        """Device half: pinned -> device copies and the block-table build.
+        With totals=None the whole table capacity is copied, so the call has a
+        fixed shape and can be captured in a CUDA graph (replayed after
+        pack_tables refilled the pinned buffers)."""
+        n = len(self.requests)
+        for g in (range(len(self.tables)) if groups is None else groups):
+            t = self.tables[g]
+            total = t.h_pages.shape[0] if totals is None else totals[g]
             t.d_offsets[: n + 1].copy_(t.h_offsets[: n + 1], non_blocking=True)
             if total:
                 t.d_pages[:total].copy_(t.h_pages[:total], non_blocking=True)
