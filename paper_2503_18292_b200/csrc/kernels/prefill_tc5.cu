@@ -428,6 +428,357 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   }
 }
 
+// ---------------------------------------------------------------- 2-SM pair
+// Same algorithm on a CTA pair (cluster of 2, cta_group::2): the leader issues
+// M=256 MMAs over both CTAs' 128 query rows (adjacent query blocks of one
+// (request, KV head)); each CTA holds HALF of every K/V tile — K rows of its
+// half of the tile's keys, V columns of its half of head_dim — so each SM
+// streams half the K/V bytes per flop.  TMA loads of both CTAs complete on the
+// leader's barrier; the leader's commits are multicast to both CTAs; the
+// peer's softmax warps arrive remotely on the leader's q_full / p_full.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta0(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(jenga_dev::smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// Remote arrive on the leader's barrier.  The default (.release.cta) form is a
+// bare SYNCS.ARRIVE; P / Q visibility to the MMA comes from tcgen05.wait::st +
+// tcgen05.fence::before_thread_sync.  Only generic shared-memory writes the
+// leader's MMA must see (zeroed V rows) need the cluster-scope release, whose
+// MEMBAR.GPU + ERRBAR cost ~25% of the kernel when paid every tile.
+__device__ __forceinline__ void arrive_cta0(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void arrive_cta0_release(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void expect_tx_cta0(uint32_t cluster_bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;\n" ::"r"(cluster_bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, int32_t c0, int32_t c1,
+                                                 uint32_t cluster_bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(cluster_bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          jenga_dev::smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <typename T, int D, int G, int KT, int NS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
+    paged_prefill_tc5_pair_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap kv_map) {
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int VB = NBOX / 2;                // V column chunks held by each CTA
+  constexpr int QB = kRows / G;
+  constexpr int KH = KT / 2;                  // keys of the K tile held by each CTA
+  constexpr int K_CHUNK = KH * 128;
+  constexpr int K_BYTES = NBOX * K_CHUNK;
+  constexpr int V_CHUNK = KT * 128;
+  constexpr int V_BYTES = VB * V_CHUNK;
+  constexpr int STAGE = K_BYTES + V_BYTES;
+  constexpr int Q_COL = D, S_COL = D + D / 2;
+  constexpr uint32_t TMEM_COLS = 512;
+  static_assert(NBOX % 2 == 0 && KT == 64 && S_COL + 2 * KT <= 512, "pair kernel shape");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
+  uint64_t* q_full = bars;                    // leader: 8 softmax warps of the pair
+  uint64_t* kv_full = bars + 1;               // leader: both CTAs' TMA bytes
+  uint64_t* kv_empty = kv_full + NS;          // both: multicast commit
+  uint64_t* s_full = kv_empty + NS;           // both: multicast commit
+  uint64_t* p_full = s_full + 2;              // leader: 8 softmax warps of the pair
+  uint64_t* p_empty = p_full + 2;             // both: multicast commit
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
+  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
+  const int pt0 = 2 * pair * QB;
+  if (pt0 >= c_len) return;  // uniform over the pair
+  const int n = p.seq_lens[b];
+  const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
+  const int pos0 = n - c_len + pt0;
+  const int pos1 = n - c_len + min(pt0 + 2 * QB, c_len) - 1;
+  int key_lo = 0;
+  const int key_hi = cross ? n - 1 : pos1;
+  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
+  const int tile_lo = key_lo / KT;
+  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
+  const int t0 = pt0 + static_cast<int>(rank) * QB;
+
+  if (threadIdx.x == 0) {
+    jenga_dev::mbar_init(q_full, 2 * kSoftWarps);
+    for (int i = 0; i < NS; ++i) {
+      jenga_dev::mbar_init(&kv_full[i], 1);
+      jenga_dev::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      jenga_dev::mbar_init(&s_full[i], 1);
+      jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
+      jenga_dev::mbar_init(&p_empty[i], 1);
+    }
+    jenga_dev::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     jenga_dev::smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
+
+  if (warp == kProducerWarp) {
+    if (lane == 0) {
+      jenga_dev::prefetch_tmap(&kv_map);
+      const uint64_t policy = jenga_dev::l2_policy_evict_first();
+      const int64_t row_bytes = D * 2;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
+      const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+      auto row_of = [&](int tok) {
+        const int32_t page = table[min(tok / p.tpp, p.max_blocks - 1)];
+        return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
+      };
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j % NS;
+        if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+        const uint32_t full0 = map_to_cta0(&kv_full[st]);
+        if (rank == 0) expect_tx_cta0(full0, 2 * STAGE);
+        uint8_t* ks = ring + st * STAGE;
+        uint8_t* vs = ks + K_BYTES;
+        const int ktok0 = (tile_lo + j) * KT;
+        for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys (K rows)
+          const int32_t row = row_of(ktok0 + static_cast<int>(rank) * KH + pc * kTile);
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx)
+            tma_load_2d_pair(ks + bx * K_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols, row, full0, policy);
+        }
+        for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim (V columns)
+          const int32_t row = row_of(ktok0 + pc * kTile) + p.tpp;
+#pragma unroll
+          for (int bx = 0; bx < VB; ++bx)
+            tma_load_2d_pair(vs + bx * V_CHUNK + pc * kTile * 128, &kv_map,
+                             (static_cast<int>(rank) * VB + bx) * kBoxCols, row, full0, policy);
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (rank == 0 && lane == 0) {
+      const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
+      const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
+      auto issue_pv = [&](int jj) {
+        const int sb = jj & 1;
+        jenga_dev::mbar_wait(&p_full[sb], (jj >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + K_BYTES);
+#pragma unroll
+        for (int k = 0; k < KT / 16; ++k)
+          umma2_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * 16 * 128, V_CHUNK, 1024), id_o,
+                   (jj > 0 || k > 0) ? 1u : 0u);
+        umma2_commit_both(&p_empty[sb]);
+        umma2_commit_both(&kv_empty[jj % NS]);
+      };
+      jenga_dev::mbar_wait(q_full, 0);
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j % NS, sb = j & 1;
+        jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
+        tc_fence_after();
+        const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          umma2_ts(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
+                   umma_desc(k_u + (k >> 2) * K_CHUNK + (k & 3) * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+        umma2_commit_both(&s_full[sb]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      if (ntiles > 0) issue_pv(ntiles - 1);
+    }
+  } else {
+    const int r = threadIdx.x;
+    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+    const int tok = t0 + r / G;
+    const bool row_ok = tok < c_len;
+    const int ipos = n - c_len + tok;
+    const uint32_t q_full0 = map_to_cta0(q_full);
+    const uint32_t p_full0[2] = {map_to_cta0(&p_full[0]), map_to_cta0(&p_full[1])};
+    {
+      const uint4* qrow = reinterpret_cast<const uint4*>(
+          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 x = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + i) : make_uint4(0, 0, 0, 0);
+          w[4 * i] = x.x;
+          w[4 * i + 1] = x.y;
+          w[4 * i + 2] = x.z;
+          w[4 * i + 3] = x.w;
+        }
+        tmem_st32u(tmem + lane_addr + Q_COL + c * 32, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cta0(q_full0);
+    }
+    int lo_r = 0, hi_r = cross ? n - 1 : ipos;
+    if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
+      lo_r = static_cast<int>(ipos + 1 - p.window);
+    if (!row_ok || hi_r < lo_r) lo_r = hi_r = 1 << 30;
+    const uint32_t span = static_cast<uint32_t>(hi_r - lo_r);
+    const bool softcap = p.cap_log2 > 0.f;
+    const float sc = softcap ? 1.f : p.qscale;
+    const float qi = p.qscale * p.inv_cap;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int sb = j & 1;
+      const int ktok0 = (tile_lo + j) * KT;
+      jenga_dev::mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s[KT];
+#pragma unroll
+      for (int c = 0; c < KT; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + lane_addr + S_COL + sb * KT + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c + i] = v[i];
+      }
+      if (softcap) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
+      }
+      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
+      }
+      float mt = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) mt = fmaxf(mt, s[i]);
+      mt *= sc;
+      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+        const float m_new = fmaxf(m_used, mt);
+        if (j >= 1) {
+          const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
+          jenga_dev::mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + c, v);
+            uint32_t u[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
+            tmem_st32u(tmem + lane_addr + c, u);
+          }
+          tmem_st_wait();
+          l *= alpha;
+        }
+        m_used = m_new;
+      }
+      uint32_t pk[KT / 2];
+      float rs0 = 0.f, rs1 = 0.f;
+      const float neg = m_used == -INFINITY ? 0.f : -m_used;
+#pragma unroll
+      for (int i = 0; i < KT; i += 2) {
+        const float a = jenga_dev::fast_exp2(fmaf(s[i], sc, neg));
+        const float bb = jenga_dev::fast_exp2(fmaf(s[i + 1], sc, neg));
+        rs0 += a;
+        rs1 += bb;
+        pk[i / 2] = pack2<T>(a, bb);
+      }
+      l += rs0 + rs1;
+#pragma unroll
+      for (int c = 0; c < KT / 2; c += 32) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
+        tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
+      }
+      tmem_st_wait();
+      // zero this CTA's V columns of keys outside the pair's range
+      const bool boundary = ktok0 < key_lo || ktok0 + KT - 1 > key_hi;
+      if (boundary) {
+        uint8_t* vs = ring + (j % NS) * STAGE + K_BYTES;
+        for (int idx = r; idx < KT * VB; idx += kRows) {
+          const int vrow = idx % KT, chunk = idx / KT;
+          const int key = ktok0 + vrow;
+          if (key >= key_lo && key <= key_hi) continue;
+          uint4* line = reinterpret_cast<uint4*>(vs + chunk * V_CHUNK + vrow * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (boundary)
+          arrive_cta0_release(p_full0[sb]);
+        else
+          arrive_cta0(p_full0[sb]);
+      }
+    }
+    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      float v[32];
+      if (ntiles > 0) {
+        tmem_ld32(tmem + lane_addr + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
+                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
+                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
+                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's last remote arrivals and MMAs are done
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -469,6 +820,46 @@ int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) 
   return jenga_dev::check_launch("paged_prefill_tc5_kernel");
 }
 
+template <typename T, int D, int G, int KT, int NS>
+int launch_tc5_pair(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int STAGE = NBOX * (KT / 2) * 128 + (NBOX / 2) * KT * 128;
+  const int smem = NS * STAGE + (1 + 2 * NS + 6) * 8 + 16 + 1024;
+  auto fn = encode_fn();
+  if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  uint64_t bytes = 0;
+  if (!jenga_dev::arena_extent(prm.arena, &bytes))
+    return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_prefill: arena_base must come from jenga_arena_create");
+  const CUtensorMapDataType dt =
+      dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap kv_map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / (D * 2)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
+  cuuint32_t box[2] = {kBoxCols, kTile};
+  cuuint32_t es[2] = {1, 1};
+  if (fn(&kv_map, dt, 2, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
+  auto kern = paged_prefill_tc5_pair_kernel<T, D, G, KT, NS>;
+  static std::atomic<uint64_t> configured{0};
+  if (int rc = configure_smem(kern, smem, configured)) return rc;
+  dim3 grid((prm.q_blocks + 1) / 2 * 2, prm.hkv, batch);
+  kern<<<grid, kT5Threads, smem, s>>>(prm, kv_map);
+  return jenga_dev::check_launch("paged_prefill_tc5_pair_kernel");
+}
+
+template <typename T, int D, int NS>
+int dispatch_pair(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  switch (G) {
+    case 1: return launch_tc5_pair<T, D, 1, 64, NS>(prm, dtype, s, batch);
+    case 2: return launch_tc5_pair<T, D, 2, 64, NS>(prm, dtype, s, batch);
+    case 4: return launch_tc5_pair<T, D, 4, 64, NS>(prm, dtype, s, batch);
+    case 8: return launch_tc5_pair<T, D, 8, 64, NS>(prm, dtype, s, batch);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
 template <typename T, int D, int NS>
 int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (G) {
@@ -484,6 +875,14 @@ int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int 
 // head_dim 64, so two CTAs share an SM: 256 TMEM columns each).
 template <typename T>
 int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  // CTA pairs (cta_group::2) halve the K/V bytes each SM streams; head_dim 64
+  // has a single 64-column chunk, too few to split V between the pair.
+  static const bool pair = [] {
+    const char* e = std::getenv("JENGA_PREFILL_2SM");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (pair && D == 256) return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
+  if (pair && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
   switch (D) {
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
     case 128: return dispatch_g<T, 128, 6>(G, prm, dtype, s, batch);
