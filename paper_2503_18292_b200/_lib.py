@@ -64,7 +64,7 @@ class LayerViewC(C.Structure):
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2503_18292_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2503_18292_b200/build.py` "
             "(or __graft_entry__.build()); there is no fallback implementation")
     return C.CDLL(str(LIB_PATH))
 
