@@ -156,6 +156,16 @@ class Workload:
     def max_tokens(self, steps):
         return max(self.ctx + self.image_tokens + steps + 16, 64)
 
+    def group_max_tokens(self, steps):
+        """Per-group ordinal bounds: cross-attention groups store image
+        positions only, decoder groups text only when the model has cross
+        attention (simulator.cpp:151-158)."""
+        from paper_2503_18292_b200.jenga import LayerKind
+        if not self.image_tokens:
+            return None
+        return {g: (self.image_tokens + 16 if gg.kind == LayerKind.kCrossAttention else self.ctx + steps + 16)
+                for g, gg in enumerate(self.geom.groups)}
+
     def arena_large_pages(self, steps):
         from paper_2503_18292_b200 import AddressMap
         from paper_2503_18292_b200.jenga import LayerKind
@@ -205,7 +215,8 @@ def run_ours(a, rank, world, local_rank):
     wl = Workload(a)
     B = wl.B
     total_steps = a.warmup + a.steps + (0 if a.no_e2e else a.warmup + a.steps) + 2
-    eng = DecodeEngine(wl.geom, wl.arena_large_pages(total_steps), B, wl.max_tokens(total_steps), dev)
+    eng = DecodeEngine(wl.geom, wl.arena_large_pages(total_steps), B, wl.max_tokens(total_steps), dev,
+                       group_max_tokens=wl.group_max_tokens(total_steps))
     ids = shard_requests(list(range(B * world)), rank, world)  # this GPU's requests; its pool is private
     eng.add_requests(ids)
     t0 = time.time()

@@ -28,6 +28,16 @@ bool pdl_enabled() {
   }();
   return on;
 }
+
+int num_sms() {
+  int dev = 0, v = 148;
+  cudaGetDevice(&dev);
+  static std::atomic<int> cached[64] = {};
+  if (dev < 64 && cached[dev].load()) return cached[dev].load();
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cached[dev].store(v);
+  return v;
+}
 }  // namespace jenga_dev
 
 struct jenga_arena {

@@ -9,66 +9,180 @@
 // DRAM-locality choice measured in profiles/r01_sweeps.md).  Source and destination
 // rows are both contiguous, so one warp moves a 256..512-B row with 16-B
 // vector stores — fully coalesced on both sides.
-#include "common.cuh"
+#include <array>
+#include <cstdio>
+
+#include "decode_common.cuh"
 
 namespace {
 
-// One thread per 16-byte chunk of one (token, head, K|V) row.
+// Division by a run-time constant for dividends < 2^31: q = umulhi(n, m) >> s
+// with m = ceil(2^(31+l) / d), l = ceil(log2 d) (Granlund-Montgomery).
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t div) : d(div) {
+    if (d <= 1) return;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    m = static_cast<uint32_t>(((1ull << (31 + l)) + d - 1) / d);
+    s = l - 1;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return d == 1 ? n : (__umulhi(n, m) >> s); }
+};
+
+// One thread per 16-byte chunk of one (token, head, K|V) row, four chunks in
+// flight per thread (loads first, then stores); index math by multiply-shift
+// (the host launches at most 2^30 chunks at a time).
+constexpr int kRcUnroll = 4;
+
 __global__ void __launch_bounds__(256) reshape_and_cache_kernel(
-    uint8_t* __restrict__ arena, uint64_t start_offset, uint64_t page_stride, int hkv, int row_bytes,
-    uint32_t tpp, const uint8_t* __restrict__ key, const uint8_t* __restrict__ value,
-    int64_t token_stride_bytes, const int64_t* __restrict__ slots, int n_tokens) {
-  const int chunks_per_row = row_bytes >> 4;
+    uint8_t* __restrict__ arena, uint64_t start_offset, uint64_t page_stride, uint32_t row_bytes, uint32_t tpp,
+    FastDiv per_token, FastDiv per_row, FastDiv by_tpp, const uint8_t* __restrict__ key,
+    const uint8_t* __restrict__ value, int64_t token_stride_bytes, const int64_t* __restrict__ slots, uint32_t total) {
   // PDL: let the decode kernel that follows get resident now; wait for our own
   // prerequisites (the previous layer's decode) before touching the arena.
   jenga_dev::pdl_launch_dependents();
   jenga_dev::pdl_wait();
-  const int64_t total = static_cast<int64_t>(n_tokens) * hkv * 2 * chunks_per_row;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(i % chunks_per_row);
-    int64_t r = i / chunks_per_row;
-    const int kv = static_cast<int>(r % 2);
-    r /= 2;
-    const int h = static_cast<int>(r % hkv);
-    const int t = static_cast<int>(r / hkv);
-    const int64_t slot = slots[t];
-    if (slot < 0) continue;
-    const int64_t page = slot / tpp;
-    const int64_t off = slot % tpp;
-    const uint8_t* src = (kv ? value : key) + t * token_stride_bytes + static_cast<int64_t>(h) * row_bytes +
-                         (c << 4);
-    uint8_t* dst = arena + start_offset + page * page_stride +
-                   ((static_cast<int64_t>(h) * 2 + kv) * tpp + off) * row_bytes + (c << 4);
-    jenga_dev::st_v4(dst, jenga_dev::ld_nc_v4(src));
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += kRcUnroll * stride) {
+    uint4 v[kRcUnroll];
+    uint8_t* dst[kRcUnroll];
+#pragma unroll
+    for (int u = 0; u < kRcUnroll; ++u) {
+      dst[u] = nullptr;
+      const uint32_t i = i0 + u * stride;
+      if (i >= total) continue;
+      const uint32_t t = per_token.div(i);            // token
+      const uint32_t w = i - t * per_token.d;         // chunk within the token's 2*Hkv rows
+      const uint32_t row = per_row.div(w);            // (head, K|V) = (row >> 1, row & 1)
+      const uint32_t c = w - row * per_row.d;
+      const int64_t slot = slots[t];
+      if (slot < 0) continue;
+      uint64_t page;
+      uint32_t off;
+      if (slot < (1ll << 31)) {
+        const uint32_t s32 = static_cast<uint32_t>(slot);
+        const uint32_t pg = by_tpp.div(s32);
+        page = pg;
+        off = s32 - pg * tpp;
+      } else {
+        page = static_cast<uint64_t>(slot) / tpp;
+        off = static_cast<uint32_t>(static_cast<uint64_t>(slot) - page * tpp);
+      }
+      v[u] = jenga_dev::ld_nc_v4(((row & 1u) ? value : key) + t * token_stride_bytes + (row >> 1) * row_bytes +
+                                 (c << 4));
+      // head-major slice: row (h, kv) of token `off` at ((2h + kv) * tpp + off) * row_bytes
+      dst[u] = arena + start_offset + page * page_stride + static_cast<uint64_t>(row * tpp + off) * row_bytes +
+               (c << 4);
+    }
+#pragma unroll
+    for (int u = 0; u < kRcUnroll; ++u)
+      if (dst[u] != nullptr) jenga_dev::st_v4(dst[u], v[u]);
   }
 }
 
-// dst[b] <- src[b], `bytes` per item, 16-B vectors, 4 in flight per thread.
-__global__ void __launch_bounds__(256) paged_copy_kernel(const uint8_t* __restrict__ src_base,
-                                                         uint64_t src_off, uint64_t src_stride,
-                                                         const int64_t* __restrict__ src_idx,
-                                                         uint8_t* __restrict__ dst_base, uint64_t dst_off,
-                                                         uint64_t dst_stride,
-                                                         const int64_t* __restrict__ dst_idx,
-                                                         uint64_t bytes) {
-  const int b = blockIdx.y;
-  const int64_t si = src_idx ? src_idx[b] : b;
-  const int64_t di = dst_idx ? dst_idx[b] : b;
-  if (si < 0 || di < 0) return;
-  const uint8_t* s = src_base + src_off + si * src_stride;
-  uint8_t* d = dst_base + dst_off + di * dst_stride;
-  const uint64_t nvec = bytes >> 4;
-  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 3 * step < nvec; i += 4 * step) {
-    uint4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = jenga_dev::ld_nc_v4(s + ((i + u * step) << 4));
-#pragma unroll
-    for (int u = 0; u < 4; ++u) jenga_dev::st_v4(d + ((i + u * step) << 4), v[u]);
+// dst[b] <- src[b], `nvec` 16-byte units per item, through the TMA bulk-copy
+// engine: a persistent grid, each CTA owning an equal contiguous share of the
+// flattened (item, unit) space; one elected thread streams it in <= kCopyChunk
+// pieces (never crossing an item) through a kCopyStages-deep shared-memory ring
+// (cp.async.bulk global->shared, completion on an mbarrier, then
+// cp.async.bulk shared->global).  The thread refills the stage of the
+// previous chunk as soon as its store has finished reading shared memory, so
+// kCopyStages-1 loads stay in flight; items with a negative index are skipped.
+// Default 16 KiB x 6 stages, 2 CTAs per SM (2 x 96 KiB rings per SM);
+// JENGA_COPY_CFG="chunk_kib,stages,ctas_per_sm" selects another instantiation (A/B runs).
+
+struct CopyArgs {
+  const uint8_t* src_base;
+  uint64_t src_off, src_stride;
+  const int64_t* src_idx;
+  uint8_t* dst_base;
+  uint64_t dst_off, dst_stride;
+  const int64_t* dst_idx;
+  uint64_t nvec;  // 16-byte units per item
+  int n;
+  int src_keep, dst_keep;  // 1: L2 evict_last (a dense staging buffer reused next kernel), 0: evict_first
+};
+
+struct CopyChunk {
+  const uint8_t* s;
+  uint8_t* d;
+  uint32_t bytes;
+};
+
+template <int kCopyChunk>
+__device__ __forceinline__ bool next_copy_chunk(const CopyArgs& a, uint64_t& pos, uint64_t hi, CopyChunk& c) {
+  while (pos < hi) {
+    const uint64_t b = pos / a.nvec;
+    const uint64_t off = pos - b * a.nvec;
+    const uint64_t end = min(hi, (b + 1) * a.nvec);
+    const int64_t si = a.src_idx ? a.src_idx[b] : static_cast<int64_t>(b);
+    const int64_t di = a.dst_idx ? a.dst_idx[b] : static_cast<int64_t>(b);
+    if (si < 0 || di < 0) {
+      pos = end;
+      continue;
+    }
+    const uint64_t len = min(end - pos, static_cast<uint64_t>(kCopyChunk / 16));
+    c.s = a.src_base + a.src_off + si * a.src_stride + off * 16;
+    c.d = a.dst_base + a.dst_off + di * a.dst_stride + off * 16;
+    c.bytes = static_cast<uint32_t>(len * 16);
+    pos += len;
+    return true;
   }
-  for (; i < nvec; i += step) jenga_dev::st_v4(d + (i << 4), jenga_dev::ld_nc_v4(s + (i << 4)));
+  return false;
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(gmem_dst),
+               "r"(jenga_dev::smem_u32(smem_src)), "r"(bytes), "l"(policy)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+
+template <int kCopyChunk, int kCopyStages>
+__global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ uint64_t full[kCopyStages];
+  // PDL: the next kernel may get resident; our reads/writes wait for the previous one.
+  jenga_dev::pdl_launch_dependents();
+  if (threadIdx.x != 0) return;
+  const uint64_t total = a.nvec * static_cast<uint64_t>(a.n);
+  uint64_t pos = total * blockIdx.x / gridDim.x;
+  const uint64_t hi = total * (blockIdx.x + 1) / gridDim.x;
+  if (pos >= hi) return;
+  for (int i = 0; i < kCopyStages; ++i) jenga_dev::mbar_init(&full[i], 1);
+  jenga_dev::fence_mbar_init();
+  jenga_dev::pdl_wait();
+  // arena pages stream through L2 once; a dense staging buffer (Mamba state
+  // between gather, the SSM update and scatter) is kept resident
+  const uint64_t src_pol = a.src_keep ? jenga_dev::l2_policy_evict_last() : jenga_dev::l2_policy_evict_first();
+  const uint64_t dst_pol = a.dst_keep ? jenga_dev::l2_policy_evict_last() : jenga_dev::l2_policy_evict_first();
+  CopyChunk ring_c[kCopyStages];
+  int issued = 0;
+  bool more = true;
+  auto issue = [&](int j) {
+    CopyChunk c;
+    if (!next_copy_chunk<kCopyChunk>(a, pos, hi, c)) return false;
+    const int st = j % kCopyStages;
+    ring_c[st] = c;
+    jenga_dev::mbar_arrive_expect_tx(&full[st], c.bytes);
+    jenga_dev::bulk_g2s_evict_first(ring + st * kCopyChunk, c.s, c.bytes, &full[st], src_pol);
+    return true;
+  };
+  for (; issued < kCopyStages && (more = issue(issued)); ++issued) {
+  }
+  for (int k = 0; k < issued; ++k) {
+    const int st = k % kCopyStages;
+    jenga_dev::mbar_wait(&full[st], (k / kCopyStages) & 1);
+    bulk_s2g(ring_c[st].d, ring + st * kCopyChunk, ring_c[st].bytes, dst_pol);
+    if (k >= 1 && more) {
+      // chunk k-1's store has read its stage: refill it with chunk k-1+kCopyStages
+      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      if ((more = issue(issued))) ++issued;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // Token rows <-> pages.  Row t (row_bytes) of the token at slot s = page*tpp +
@@ -135,22 +249,51 @@ int launch_token_rows(bool scatter, void* arena_base, jenga_layer_view view, uin
   return check_launch(scatter ? "token_rows_kernel<scatter>" : "token_rows_kernel<gather>");
 }
 
+template <int CHUNK, int STAGES>
+int launch_copy(const CopyArgs& args, int ctas_per_sm, void* stream, const char* what) {
+  constexpr int smem = CHUNK * STAGES;
+  auto kern = paged_copy_kernel<CHUNK, STAGES>;
+  static std::atomic<uint64_t> configured{0};
+  if (int rc = jenga_decode::configure_smem(kern, smem, configured)) return rc;
+  // enough CTAs to fill every SM, none without at least one chunk of work
+  const uint64_t chunks = (args.nvec * 16 * static_cast<uint64_t>(args.n) + CHUNK - 1) / CHUNK;
+  const int grid = static_cast<int>(
+      std::min<uint64_t>(chunks, static_cast<uint64_t>(jenga_dev::num_sms()) * std::max(1, ctas_per_sm)));
+  jenga_dev::launch_maybe_pdl(kern, dim3(grid), dim3(32), smem, static_cast<cudaStream_t>(stream), args);
+  return jenga_dev::check_launch(what);
+}
+
 int launch_paged_copy(const void* src_base, uint64_t src_off, uint64_t src_stride, const int64_t* src_idx,
                       void* dst_base, uint64_t dst_off, uint64_t dst_stride, const int64_t* dst_idx,
-                      uint64_t bytes, int n, void* stream, const char* what) {
+                      uint64_t bytes, int n, void* stream, const char* what, int src_keep, int dst_keep) {
   using namespace jenga_dev;
   if (n <= 0 || bytes == 0) return JENGA_OK;
   if (bytes % 16 != 0 || src_off % 16 != 0 || dst_off % 16 != 0 || src_stride % 16 != 0 ||
-      dst_stride % 16 != 0)
+      dst_stride % 16 != 0 || reinterpret_cast<uintptr_t>(src_base) % 16 || reinterpret_cast<uintptr_t>(dst_base) % 16)
     return set_error(JENGA_ERR_UNSUPPORTED, std::string(what) + ": sizes/offsets must be 16-byte multiples");
-  const uint64_t nvec = bytes >> 4;
-  int gx = static_cast<int>(std::min<uint64_t>((nvec + 1023) / 1024, 512));
-  if (gx < 1) gx = 1;
-  dim3 grid(gx, n);
-  paged_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint8_t*>(src_base), src_off, src_stride, src_idx, static_cast<uint8_t*>(dst_base),
-      dst_off, dst_stride, dst_idx, bytes);
-  return check_launch(what);
+  static const bool keep_ok = [] {  // JENGA_COPY_L2_KEEP=0: no evict_last hints (A/B runs)
+    const char* e = std::getenv("JENGA_COPY_L2_KEEP");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (!keep_ok) src_keep = dst_keep = 0;
+  static const std::array<int, 3> cfg = [] {
+    std::array<int, 3> c{16, 6, 2};
+    if (const char* e = std::getenv("JENGA_COPY_CFG")) std::sscanf(e, "%d,%d,%d", &c[0], &c[1], &c[2]);
+    return c;
+  }();
+  const CopyArgs args{static_cast<const uint8_t*>(src_base), src_off, src_stride, src_idx,
+                      static_cast<uint8_t*>(dst_base), dst_off, dst_stride, dst_idx, bytes / 16, n,
+                      src_keep, dst_keep};
+  const int key = cfg[0] * 100 + cfg[1];
+  switch (key) {
+    case 806: return launch_copy<8192, 6>(args, cfg[2], stream, what);
+    case 812: return launch_copy<8192, 12>(args, cfg[2], stream, what);
+    case 1606: return launch_copy<16384, 6>(args, cfg[2], stream, what);
+    case 1612: return launch_copy<16384, 12>(args, cfg[2], stream, what);
+    case 3206: return launch_copy<32768, 6>(args, cfg[2], stream, what);
+    case 3203: return launch_copy<32768, 3>(args, cfg[2], stream, what);
+  }
+  return set_error(JENGA_ERR_ARG, "JENGA_COPY_CFG: unsupported chunk/stages");
 }
 
 }  // namespace
@@ -170,12 +313,22 @@ JENGA_EXPORT int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view
   if (row_bytes % 16 != 0 || view.start_offset % 16 != 0 || view.page_stride % 16 != 0)
     return set_error(JENGA_ERR_UNSUPPORTED, "jenga_reshape_and_cache: rows must be 16-byte aligned");
   if (n_tokens == 0) return JENGA_OK;
-  const int64_t total = static_cast<int64_t>(n_tokens) * num_kv_heads * 2 * (row_bytes / 16);
-  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  launch_maybe_pdl(reshape_and_cache_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
-                   static_cast<uint8_t*>(arena_base), view.start_offset, view.page_stride, num_kv_heads, row_bytes,
-                   tokens_per_page, static_cast<const uint8_t*>(key), static_cast<const uint8_t*>(value),
-                   kv_token_stride * e, slot_mapping, n_tokens);
+  const uint64_t per_token = static_cast<uint64_t>(num_kv_heads) * 2 * (row_bytes / 16);
+  const int max_tokens = static_cast<int>(std::max<uint64_t>(1, (1ull << 30) / per_token));
+  const auto* k8 = static_cast<const uint8_t*>(key);
+  const auto* v8 = static_cast<const uint8_t*>(value);
+  for (int t0 = 0; t0 < n_tokens; t0 += max_tokens) {  // 32-bit chunk indices per launch
+    const int nt = std::min(max_tokens, n_tokens - t0);
+    const uint32_t total = static_cast<uint32_t>(nt * per_token);
+    const int blocks = static_cast<int>(
+        std::min<uint64_t>((total + 256 * kRcUnroll - 1) / (256 * kRcUnroll), static_cast<uint64_t>(num_sms()) * 8));
+    launch_maybe_pdl(reshape_and_cache_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                     static_cast<uint8_t*>(arena_base), view.start_offset, view.page_stride,
+                     static_cast<uint32_t>(row_bytes), tokens_per_page, FastDiv(static_cast<uint32_t>(per_token)),
+                     FastDiv(static_cast<uint32_t>(row_bytes / 16)), FastDiv(tokens_per_page),
+                     k8 + static_cast<int64_t>(t0) * kv_token_stride * e, v8 + static_cast<int64_t>(t0) * kv_token_stride * e,
+                     kv_token_stride * e, slot_mapping + t0, total);
+  }
   return check_launch("reshape_and_cache_kernel");
 }
 
@@ -183,7 +336,7 @@ JENGA_EXPORT int jenga_mamba_state_gather(const void* arena_base, jenga_layer_vi
                                           const int64_t* page_globals, int batch, void* dense, void* stream) {
   return launch_paged_copy(arena_base, view.start_offset, view.page_stride, page_globals, dense, 0,
                            view.exec_page_size, nullptr, view.exec_page_size, batch, stream,
-                           "mamba_state_gather");
+                           "mamba_state_gather", 0, 1);
 }
 
 JENGA_EXPORT int jenga_mamba_state_scatter(void* arena_base, jenga_layer_view view,
@@ -191,13 +344,13 @@ JENGA_EXPORT int jenga_mamba_state_scatter(void* arena_base, jenga_layer_view vi
                                            void* stream) {
   return launch_paged_copy(dense, 0, view.exec_page_size, nullptr, arena_base, view.start_offset,
                            view.page_stride, page_globals, view.exec_page_size, batch, stream,
-                           "mamba_state_scatter");
+                           "mamba_state_scatter", 1, 0);
 }
 
 JENGA_EXPORT int jenga_page_copy(void* arena_base, uint64_t small_page_bytes, const int64_t* src_globals,
                                  const int64_t* dst_globals, int n_pages, void* stream) {
   return launch_paged_copy(arena_base, 0, small_page_bytes, src_globals, arena_base, 0, small_page_bytes,
-                           dst_globals, small_page_bytes, n_pages, stream, "page_copy");
+                           dst_globals, small_page_bytes, n_pages, stream, "page_copy", 0, 0);
 }
 
 JENGA_EXPORT int jenga_token_rows_scatter(void* arena_base, jenga_layer_view view, uint32_t num_layers,

@@ -124,6 +124,12 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* smem_dst, const void*
       : "memory");
 }
 
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
@@ -192,6 +198,7 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 bool pdl_enabled();  // JENGA_PDL=0 disables (A/B runs)
+int num_sms();       // SMs of the current device (cached per device)
 
 // Launch with the programmatic-stream-serialization attribute when enabled.
 template <typename... KArgs, typename... Args>

@@ -414,6 +414,13 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
   prm.grid_order = grid_order();
   prm.batch = batch;
   prm.max_splits = splits_for(max_blocks, tpp, tiles_per_split());
+  if (kind == JENGA_KIND_SLIDING_WINDOW) {
+    // live ordinals (n-W, n] span at most ceil(W/16)+1 tiles: no grid slices for
+    // splits a window can never reach (the table is still indexed by absolute block)
+    const int64_t win_tiles = (static_cast<int64_t>(window) + kTile - 1) / kTile + 1;
+    const int64_t ws = (win_tiles + prm.tiles_per_split - 1) / prm.tiles_per_split;
+    if (ws < prm.max_splits) prm.max_splits = static_cast<int>(ws);
+  }
   if (softcap > 0.f) {
     prm.qscale = scale;
     prm.cap_log2 = softcap * kLog2e;

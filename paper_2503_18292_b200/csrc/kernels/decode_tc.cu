@@ -586,16 +586,6 @@ int tensor_map(const void* base, int D, int dtype, CUtensorMap* out) {
   return JENGA_OK;
 }
 
-int num_sms() {
-  static const int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
 // Persistent scheduling only with JENGA_DECODE_PERSISTENT=1: measured slower
 // than three grid CTAs per SM on the bench shapes (profiles/r01_sweeps.md).
 bool use_persistent(int batch) {
@@ -625,7 +615,7 @@ int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaS
     int per_sm = 0;  // resident CTAs per SM at this shared-memory size
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
       per_sm = 1;
-    kern<<<num_sms() * std::min(per_sm, CTAS_PER_SM), kThreads, smem, stream>>>(prm, tmap);
+    kern<<<jenga_dev::num_sms() * std::min(per_sm, CTAS_PER_SM), kThreads, smem, stream>>>(prm, tmap);
     return jenga_dev::check_launch("paged_decode_tc_persistent");
   }
   constexpr int NS = stages<D, HG>();

@@ -44,7 +44,11 @@ class GroupTables:
 
 class DecodeEngine:
     def __init__(self, geom: ModelGeometry, num_large_pages: int, max_batch: int, max_tokens: int,
-                 device: Optional[torch.device] = None, prefix_caching: bool = False):
+                 device: Optional[torch.device] = None, prefix_caching: bool = False,
+                 group_max_tokens: Optional[Dict[int, int]] = None):
+        """group_max_tokens: optional per-group bound on stored ordinals (e.g. a
+        cross-attention group holds only image tokens) — narrows that group's
+        block-table width and so the decode grid's split dimension."""
         self.geom = geom
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         self.spec = geom.spec()
@@ -60,7 +64,8 @@ class DecodeEngine:
         self.tables: List[GroupTables] = []
         for g, gg in enumerate(geom.groups):
             tpp = self.spec.groups[g].tokens_per_page
-            max_blocks = 1 if gg.kind == LayerKind.kMamba else math.ceil(max_tokens / tpp) + 1
+            mt = (group_max_tokens or {}).get(g, max_tokens)
+            max_blocks = 1 if gg.kind == LayerKind.kMamba else math.ceil(mt / tpp) + 1
             pin = dict(dtype=torch.int32, pin_memory=True)
             dev = dict(dtype=torch.int32, device=self.device)
             t = GroupTables(

@@ -155,14 +155,24 @@ def paged_prefill(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out
     return out
 
 
+def _need_dense(dense: torch.Tensor, view: LayerView, batch: int) -> None:
+    if not dense.is_cuda or not dense.is_contiguous():
+        raise ValueError("dense state must be a contiguous CUDA tensor")
+    if dense.numel() * dense.element_size() < batch * view.exec_page_size:
+        raise ValueError(f"dense state holds {dense.numel() * dense.element_size()} bytes, "
+                         f"need batch * exec_page_size = {batch * view.exec_page_size}")
+
+
 def mamba_state_gather(arena: Arena, view: LayerView, page_globals: torch.Tensor, dense: torch.Tensor) -> None:
     _need(page_globals, torch.int64, "page_globals")
+    _need_dense(dense, view, page_globals.numel())
     check(lib.jenga_mamba_state_gather(arena.base, view.c(), _ptr(page_globals), page_globals.numel(),
                                        _ptr(dense), _stream()))
 
 
 def mamba_state_scatter(arena: Arena, view: LayerView, page_globals: torch.Tensor, dense: torch.Tensor) -> None:
     _need(page_globals, torch.int64, "page_globals")
+    _need_dense(dense, view, page_globals.numel())
     check(lib.jenga_mamba_state_scatter(arena.base, view.c(), _ptr(page_globals), page_globals.numel(),
                                         _ptr(dense), _stream()))
 

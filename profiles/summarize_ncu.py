@@ -90,7 +90,47 @@ def full(tag, src):
              "launches": traffic, "traffic_bytes_per_launch": per}, indent=1))
 
 
+def dram(tag, src):
+    """Per-kernel achieved DRAM bandwidth from profiles/run_ncu_kernels.sh CSVs:
+    one table per workload, grouped by (kernel, grid)."""
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() \
+        else 7672.0
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
+             "nsecond": 1e-9, "ms": 1e-3, "msecond": 1e-3}
+    out = [f"# {tag}: per-kernel DRAM bandwidth (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+           "dram__bytes_write.sum --clock-control none)", "",
+           "Each launch replayed alone with ncu's cache control (cold L2), so small launches pay their ramp-up;",
+           f"GB/s = (DRAM read + write bytes) / device time; % = of the measured copy peak {peak} GB/s.", ""]
+    for path in sorted(src.glob("*.csv")):
+        rows = [r for r in csv.DictReader(l for l in open(path) if l.startswith('"'))]
+        per = defaultdict(dict)
+        for r in rows:
+            v = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1)
+            per[(r["ID"], short(r["Kernel Name"]), r.get("Grid Size", ""))][r["Metric Name"]] = v
+        agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+        for (_, k, grid), m in per.items():
+            a = agg[(k, grid)]
+            a[0] += 1
+            a[1] += m.get("gpu__time_duration.sum", 0.0)
+            a[2] += m.get("dram__bytes_read.sum", 0.0)
+            a[3] += m.get("dram__bytes_write.sum", 0.0)
+        if not agg:
+            continue
+        out += [f"## {path.stem}", "", "| kernel | grid | launches | mean us | read MB | write MB | GB/s | % peak |",
+                "|---|---|---|---|---|---|---|---|"]
+        for (k, grid), (n, t, rd, wr) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            gbs = (rd + wr) / t / 1e9 if t else 0.0
+            out.append(f"| `{k}` | {grid} | {n} | {t / n * 1e6:.1f} | {rd / n / 1e6:.1f} | {wr / n / 1e6:.1f} | "
+                       f"{gbs:.0f} | {gbs / peak:.1%} |")
+        out.append("")
+    (ROOT / "profiles" / f"{tag}_kernels_dram.md").write_text("\n".join(out) + "\n")
+    print("\n".join(out))
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--dram":
+        dram(sys.argv[2], Path(sys.argv[3]) if len(sys.argv) > 3 else ROOT / "gpurun_out" / "kernels")
+        sys.exit(0)
     tag = sys.argv[1]
     src = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "gpurun_out"
     launches(tag, src)

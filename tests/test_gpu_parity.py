@@ -167,6 +167,41 @@ def test_mamba_state_gather_scatter_and_checkpoint_copy(orc):
     np.testing.assert_array_equal(arena_host(eng), want)
 
 
+@pytest.mark.parametrize("state_bytes", [622592, 20480])
+def test_mamba_state_copy_large_and_skipped(orc, state_bytes):
+    """Jamba-size state slices (many 16 KiB bulk-copy chunks per request, CTA
+    shares crossing request boundaries) and odd sizes; index -1 = skipped."""
+    geom = ModelGeometry("hyb", [
+        GroupGeometry("attn", LayerKind.kFullAttention, 1, 8, 32, 128, torch.bfloat16, 16),
+        GroupGeometry("ssm", LayerKind.kMamba, 3, state_bytes=state_bytes)])
+    lens = [3, 1, 2, 5, 1, 4, 2, 7, 1, 3, 2]
+    eng, ids = make_engine(geom, lens, poison=False)
+    g = 1
+    B = len(ids)
+    pg = eng.mamba_page_globals(g).clone()
+    pg[4] = -1
+    pg[9] = -1
+    gen = torch.Generator(device=eng.device).manual_seed(11)
+    eng.arena.tensor().random_(0, 256, generator=gen)
+    for layer in (0, 2):
+        view = eng.view(g, layer)
+        before = arena_host(eng)
+        got = torch.full((B, view.exec_page_size), 7, device=eng.device, dtype=torch.uint8)
+        ops.mamba_state_gather(eng.arena, view, pg, got)
+        torch.cuda.synchronize()
+        want = orc.mamba_gather(before, tuple(view), pg.cpu().numpy(), B)
+        keep = pg.cpu().numpy() >= 0
+        np.testing.assert_array_equal(got.cpu().numpy()[keep], want[keep])
+        assert (got.cpu().numpy()[~keep] == 7).all()  # skipped rows untouched
+        dense = torch.randint(0, 256, (B, view.exec_page_size), generator=gen, device=eng.device,
+                              dtype=torch.uint8)
+        ops.mamba_state_scatter(eng.arena, view, pg, dense)
+        torch.cuda.synchronize()
+        want = before.copy()
+        orc.mamba_scatter(want, tuple(view), pg.cpu().numpy(), dense.cpu().numpy())
+        np.testing.assert_array_equal(arena_host(eng), want)
+
+
 def test_launch_counter_and_errors():
     n0 = ops.kernel_launch_count()
     geom = toy(16)
