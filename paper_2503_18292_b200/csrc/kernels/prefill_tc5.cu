@@ -141,6 +141,35 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
+// Warp-cooperative look-ahead over one request's block table for the TMA
+// producer: lane l holds table[base + l] (cur) and table[base + 32 + l] (nxt),
+// so a page lookup is a shuffle instead of a dependent global load per 16-row
+// piece (which serialised ~6 L2 round trips into every tile).  Lookups must be
+// warp-uniform and non-decreasing; indices clamp to the last block like the
+// direct form table[min(blk, max_blocks - 1)].
+struct PageLookahead {
+  const int32_t* table;
+  int max_blocks, base, cur, nxt;
+  __device__ __forceinline__ int load(int i, int lane) const {
+    return __ldg(table + min(i + lane, max_blocks - 1));
+  }
+  __device__ __forceinline__ void init(const int32_t* t, int mb, int first, int lane) {
+    table = t;
+    max_blocks = mb;
+    base = first;
+    cur = load(base, lane);
+    nxt = load(base + 32, lane);
+  }
+  __device__ __forceinline__ int32_t get(int blk, int lane) {
+    while (blk >= base + 32) {
+      base += 32;
+      cur = nxt;
+      nxt = load(base + 32, lane);
+    }
+    return __shfl_sync(0xffffffffu, cur, blk - base);
+  }
+};
+
 // D = head_dim, G = query heads per KV head, KT = KV tokens per tile,
 // NS = K/V ring stages.
 template <typename T, int D, int G, int KT, int NS>
@@ -209,24 +238,26 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   const uint32_t tmem = *tmem_slot;
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
-  if (warp == kProducerWarp) {
-    if (lane == 0) {
-      jenga_dev::prefetch_tmap(&kv_map);
-      const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int64_t row_bytes = D * 2;
-      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
-      const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
-      const int v_rows = p.tpp;  // head-major slice
-      for (int j = 0; j < ntiles; ++j) {
-        const int st = j % NS;
-        if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
-        uint8_t* ks = ring + st * STAGE;
-        jenga_dev::mbar_arrive_expect_tx(&kv_full[st], STAGE);
-        for (int pc = 0; pc < PIECES; ++pc) {
-          const int tok = (tile_lo + j) * KT + pc * kTile;
-          const int32_t page = table[min(tok / p.tpp, p.max_blocks - 1)];
-          const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows +
-                                                   tok % p.tpp);
+  if (warp == kProducerWarp) {  // the whole warp walks the table; lane 0 issues
+    if (lane == 0) jenga_dev::prefetch_tmap(&kv_map);
+    const uint64_t policy = jenga_dev::l2_policy_evict_first();
+    const int64_t row_bytes = D * 2;
+    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
+    const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+    const int v_rows = p.tpp;  // head-major slice
+    PageLookahead pl;
+    pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % NS;
+      if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+      uint8_t* ks = ring + st * STAGE;
+      if (lane == 0) jenga_dev::mbar_arrive_expect_tx(&kv_full[st], STAGE);
+      for (int pc = 0; pc < PIECES; ++pc) {
+        const int tok = (tile_lo + j) * KT + pc * kTile;
+        const int32_t page = pl.get(tok / p.tpp, lane);
+        const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows +
+                                                 tok % p.tpp);
+        if (lane == 0) {
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx) {
             jenga_dev::tma_load_2d(ks + bx * KV_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols, row, &kv_full[st],
@@ -556,33 +587,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
   const uint32_t tmem = *tmem_slot;
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
-  if (warp == kProducerWarp) {
-    if (lane == 0) {
-      jenga_dev::prefetch_tmap(&kv_map);
-      const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int64_t row_bytes = D * 2;
-      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
-      const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
-      auto row_of = [&](int tok) {
-        const int32_t page = table[min(tok / p.tpp, p.max_blocks - 1)];
-        return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
-      };
-      for (int j = 0; j < ntiles; ++j) {
-        const int st = j % NS;
-        if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
-        const uint32_t full0 = map_to_cta0(&kv_full[st]);
-        if (rank == 0) expect_tx_cta0(full0, 2 * STAGE);
-        uint8_t* ks = ring + st * STAGE;
-        uint8_t* vs = ks + K_BYTES;
-        const int ktok0 = (tile_lo + j) * KT;
+  if (warp == kProducerWarp) {  // the whole warp walks the table; lane 0 issues
+    if (lane == 0) jenga_dev::prefetch_tmap(&kv_map);
+    const uint64_t policy = jenga_dev::l2_policy_evict_first();
+    const int64_t row_bytes = D * 2;
+    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
+    const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+    PageLookahead pl;
+    pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
+    // pages of one tile (KT / tpp <= 4 for tpp >= 16), looked up once in key order
+    auto row_of = [&](int32_t page, int tok) {
+      return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
+    };
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % NS;
+      if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+      const uint32_t full0 = map_to_cta0(&kv_full[st]);
+      if (rank == 0 && lane == 0) expect_tx_cta0(full0, 2 * STAGE);
+      uint8_t* ks = ring + st * STAGE;
+      uint8_t* vs = ks + K_BYTES;
+      const int ktok0 = (tile_lo + j) * KT;
+      int32_t pages[KT / kTile];
+#pragma unroll
+      for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
+      if (lane == 0) {
+#pragma unroll
         for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys (K rows)
-          const int32_t row = row_of(ktok0 + static_cast<int>(rank) * KH + pc * kTile);
+          const int kp = static_cast<int>(rank) * (KH / kTile) + pc;
+          const int32_t row = row_of(rank ? pages[KH / kTile + pc] : pages[pc], ktok0 + kp * kTile);
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx)
             tma_load_2d_pair(ks + bx * K_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols, row, full0, policy);
         }
+#pragma unroll
         for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim (V columns)
-          const int32_t row = row_of(ktok0 + pc * kTile) + p.tpp;
+          const int32_t row = row_of(pages[pc], ktok0 + pc * kTile) + p.tpp;
 #pragma unroll
           for (int bx = 0; bx < VB; ++bx)
             tma_load_2d_pair(vs + bx * V_CHUNK + pc * kTile * 128, &kv_map,
@@ -920,6 +959,7 @@ int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_s
   prm.hkv = hkv;
   prm.tpp = tpp;
   prm.q_blocks = q_blocks_128;
+
   prm.qscale = qscale;
   prm.cap_log2 = cap_log2;
   prm.inv_cap = inv_cap;
