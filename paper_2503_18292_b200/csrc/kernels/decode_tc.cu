@@ -340,16 +340,20 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
       const int v_rows = p.tpp;
       bool waited = false;
+      // the next tile's arena row is read one iteration ahead, so the block-table
+      // load is off the empty-slot -> refill path
+      int32_t row = wk.t_count > 0 ? tile_row(p, table, h0, wk.t_begin * kTile, D * 2) : 0;
       for (int it = 0; it < wk.t_count; ++it) {
         const int st = it % NS;
-        if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
         const int tok0 = (wk.t_begin + it) * kTile;
+        const int32_t next = it + 1 < wk.t_count ? tile_row(p, table, h0, tok0 + kTile, D * 2) : 0;
+        if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
         if (!waited && tok0 + kTile >= wk.n) {  // the tile holding the newest token
           jenga_dev::pdl_wait();
           waited = true;
         }
-        load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], tile_row(p, table, h0, tok0, D * 2), p.tpp,
-                          v_rows, policy);
+        load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], row, p.tpp, v_rows, policy);
+        row = next;
       }
     }
     return;
