@@ -301,14 +301,19 @@ int splits_for(int max_blocks, int tpp, int tiles_per_split) {
   return static_cast<int>((max_tiles + tiles_per_split - 1) / tiles_per_split);
 }
 
-// Tiles per CTA; JENGA_DECODE_TILES_PER_SPLIT overrides for tuning sweeps.
-int tiles_per_split() {
-  static const int v = [] {
+// Tiles per CTA, sized by bytes: a CTA pays a fixed prologue / merge cost, so
+// it should stream ~512-768 KiB of one head's K+V.  head_dim 256: 32 tiles
+// (512 KiB); head_dim <= 128: 96 * 128/D tiles (768 KiB) — measured +7% (Llama
+// vision) and +10% (Jamba attention) over 32 tiles at D=128
+// (profiles/r01_sweeps.md).  JENGA_DECODE_TILES_PER_SPLIT overrides for sweeps.
+int tiles_per_split(int head_dim) {
+  static const int forced = [] {
     const char* e = std::getenv("JENGA_DECODE_TILES_PER_SPLIT");
     const int x = e ? std::atoi(e) : 0;
-    return x >= kMinTilesPerSplit ? x : kTilesPerSplit;
+    return x >= kMinTilesPerSplit ? x : 0;
   }();
-  return v;
+  if (forced) return forced;
+  return head_dim >= 256 ? kTilesPerSplit : 96 * 128 / std::max(head_dim, 16);
 }
 
 int grid_order() {
@@ -410,10 +415,10 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
   prm.hq = num_q_heads;
   prm.hkv = num_kv_heads;
   prm.tpp = tpp;
-  prm.tiles_per_split = tiles_per_split();
+  prm.tiles_per_split = tiles_per_split(head_dim);
   prm.grid_order = grid_order();
   prm.batch = batch;
-  prm.max_splits = splits_for(max_blocks, tpp, tiles_per_split());
+  prm.max_splits = splits_for(max_blocks, tpp, prm.tiles_per_split);
   if (kind == JENGA_KIND_SLIDING_WINDOW) {
     // live ordinals (n-W, n] span at most ceil(W/16)+1 tiles: no grid slices for
     // splits a window can never reach (the table is still indexed by absolute block)

@@ -111,6 +111,19 @@ def test_gemma_shapes_bf16_long_context(orc):
         run_decode_parity(orc, eng, g, 1, softcap=50.0)
 
 
+@pytest.mark.parametrize("kind", [LayerKind.kFullAttention, LayerKind.kSlidingWindow])
+def test_head_dim_128_multi_split(orc, kind):
+    """D=128 streams 96 tiles (1536 tokens) per CTA: contexts around and past
+    that boundary exercise the split merge of the Llama/Jamba head shape."""
+    window = 3000 if kind == LayerKind.kSlidingWindow else 0
+    geom = ModelGeometry("d128", [GroupGeometry("g", kind, 2, 8, 32, 128, torch.bfloat16, 16, window=window)])
+    lens = [4000, 3100, 1537, 1536, 1535, 5, 3073]
+    eng, ids = make_engine(geom, lens, seed=5)
+    check_tables(orc, eng)
+    fill_group_kv(eng, 0, [0], seed=8)
+    run_decode_parity(orc, eng, 0, 0, seed=2)
+
+
 def test_cross_attention_image_tokens(orc):
     """Llama-3.2-Vision style: self (text only) + cross (image ordinals only),
     including a request with no image tokens (n=0 -> zero output)."""
