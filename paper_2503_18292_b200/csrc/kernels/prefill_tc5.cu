@@ -54,6 +54,7 @@ struct Prefill5Params {
   int64_t window;
   int max_blocks, hq, hkv, tpp, q_blocks;
   float qscale, cap_log2, inv_cap;
+  int diag;  // JENGA_PREFILL_DIAG (pair kernel, timing experiments only): 1 no softmax math, 2 no K/V loads
 };
 
 // ---------------------------------------------------------------- tcgen05
@@ -595,11 +596,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
     const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
     PageLookahead pl;
     pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
+    const int ptiles = (p.diag & 2) ? 0 : ntiles;
     // pages of one tile (KT / tpp <= 4 for tpp >= 16), looked up once in key order
     auto row_of = [&](int32_t page, int tok) {
       return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
     };
-    for (int j = 0; j < ntiles; ++j) {
+    for (int j = 0; j < ptiles; ++j) {
       const int st = j % NS;
       if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
       const uint32_t full0 = map_to_cta0(&kv_full[st]);
@@ -648,7 +650,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       jenga_dev::mbar_wait(q_full, 0);
       for (int j = 0; j < ntiles; ++j) {
         const int st = j % NS, sb = j & 1;
-        jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
+        if (!(p.diag & 2)) jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
         tc_fence_after();
         const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
 #pragma unroll
@@ -703,6 +705,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       const int ktok0 = (tile_lo + j) * KT;
       jenga_dev::mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
+      if (p.diag & 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_cta0(p_full0[sb]);
+        continue;
+      }
       float s[KT];
 #pragma unroll
       for (int c = 0; c < KT; c += 32) {
@@ -959,6 +967,11 @@ int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_s
   prm.hkv = hkv;
   prm.tpp = tpp;
   prm.q_blocks = q_blocks_128;
+  static const int diag = [] {
+    const char* e = std::getenv("JENGA_PREFILL_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  prm.diag = diag;
 
   prm.qscale = qscale;
   prm.cap_log2 = cap_log2;
