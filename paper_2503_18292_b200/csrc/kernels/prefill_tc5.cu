@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <utility>
 
 #include "decode_common.cuh"
 
@@ -504,6 +505,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, in
       "l"(tmap), "r"(cluster_bar), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// 3-D box over the arena viewed as [chunk][row][64 cols] (dim0 = 64 columns,
+// dim1 = rows at row_bytes, dim2 = 64-column chunks at 128 B): one TMA covers
+// several head_dim chunks of a run of rows, landing chunk-major in shared memory.
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, int32_t c1, int32_t c2,
+                                                 uint32_t cluster_bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(cluster_bar), "r"(0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void umma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
                                          uint32_t acc) {
   asm volatile(
@@ -521,15 +533,21 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
 
 template <typename T, int D, int G, int KT, int NS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
-    paged_prefill_tc5_pair_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap kv_map) {
+    paged_prefill_tc5_pair_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
+                                  const __grid_constant__ CUtensorMap v_map) {
+  // Shared-memory layouts (all 128-byte swizzled, one TMA box per group / piece):
+  //   K: [8-key group g][chunk c][8 rows][128 B]  (k_map box {64, 8, NBOX});
+  //      the K-major descriptor walks chunks at 1 KiB, 8-key groups at SBO = NBOX KiB
+  //   V: [16-key piece][chunk c][16 rows][128 B]  (v_map box {64, 16, VB});
+  //      the MN-major descriptor walks chunks at LBO = 2 KiB, 8-key groups at 1 KiB
   constexpr int NBOX = D / kBoxCols;
   constexpr int VB = NBOX / 2;                // V column chunks held by each CTA
   constexpr int QB = kRows / G;
   constexpr int KH = KT / 2;                  // keys of the K tile held by each CTA
-  constexpr int K_CHUNK = KH * 128;
-  constexpr int K_BYTES = NBOX * K_CHUNK;
-  constexpr int V_CHUNK = KT * 128;
-  constexpr int V_BYTES = VB * V_CHUNK;
+  constexpr int K_GROUP = NBOX * 8 * 128;     // one 8-key group, all chunks
+  constexpr int K_BYTES = (KH / 8) * K_GROUP;
+  constexpr int V_PIECE = VB * kTile * 128;   // one 16-key piece, this CTA's chunks
+  constexpr int V_BYTES = (KT / kTile) * V_PIECE;
   constexpr int STAGE = K_BYTES + V_BYTES;
   constexpr int Q_COL = D, S_COL = D + D / 2;
   constexpr uint32_t TMEM_COLS = 512;
@@ -589,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
   if (warp == kProducerWarp) {  // the whole warp walks the table; lane 0 issues
-    if (lane == 0) jenga_dev::prefetch_tmap(&kv_map);
+    if (lane == 0) { jenga_dev::prefetch_tmap(&k_map); jenga_dev::prefetch_tmap(&v_map); }
     const uint64_t policy = jenga_dev::l2_policy_evict_first();
     const int64_t row_bytes = D * 2;
     const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
@@ -605,7 +623,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       const int st = j % NS;
       if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
       const uint32_t full0 = map_to_cta0(&kv_full[st]);
-      if (rank == 0 && lane == 0) expect_tx_cta0(full0, 2 * STAGE);
+      if (rank == 0 && lane == 0)
+        expect_tx_cta0(full0, (p.diag & 4) ? 2 * K_BYTES : ((p.diag & 8) ? 2 * V_BYTES : 2 * STAGE));
       uint8_t* ks = ring + st * STAGE;
       uint8_t* vs = ks + K_BYTES;
       const int ktok0 = (tile_lo + j) * KT;
@@ -614,20 +633,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
       if (lane == 0) {
 #pragma unroll
-        for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys (K rows)
-          const int kp = static_cast<int>(rank) * (KH / kTile) + pc;
-          const int32_t row = row_of(rank ? pages[KH / kTile + pc] : pages[pc], ktok0 + kp * kTile);
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_2d_pair(ks + bx * K_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols, row, full0, policy);
+        for (int g = 0; g < ((p.diag & 8) ? 0 : KH / 8); ++g) {  // this CTA's half of the keys, 8 at a time
+          const int kk = static_cast<int>(rank) * KH + g * 8;   // key offset within the tile
+          const int32_t pg = rank ? pages[(KH + g * 8) / kTile] : pages[(g * 8) / kTile];
+          const int32_t row = row_of(pg, ktok0 + kk);
+          tma_load_3d_pair(ks + g * K_GROUP, &k_map, row, 0, full0, policy);
         }
 #pragma unroll
-        for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim (V columns)
+        for (int pc = 0; pc < ((p.diag & 4) ? 0 : KT / kTile); ++pc) {  // all keys, this CTA's half of head_dim
           const int32_t row = row_of(pages[pc], ktok0 + pc * kTile) + p.tpp;
-#pragma unroll
-          for (int bx = 0; bx < VB; ++bx)
-            tma_load_2d_pair(vs + bx * V_CHUNK + pc * kTile * 128, &kv_map,
-                             (static_cast<int>(rank) * VB + bx) * kBoxCols, row, full0, policy);
+          tma_load_3d_pair(vs + pc * V_PIECE, &v_map, row, static_cast<int>(rank) * VB, full0, policy);
         }
       }
     }
@@ -642,7 +657,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
         const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + K_BYTES);
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k)
-          umma2_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * 16 * 128, V_CHUNK, 1024), id_o,
+          umma2_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o,
                    (jj > 0 || k > 0) ? 1u : 0u);
         umma2_commit_both(&p_empty[sb]);
         umma2_commit_both(&kv_empty[jj % NS]);
@@ -656,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
           umma2_ts(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
-                   umma_desc(k_u + (k >> 2) * K_CHUNK + (k & 3) * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+                   umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
         umma2_commit_both(&s_full[sb]);
         if (j >= 1) issue_pv(j - 1);
       }
@@ -780,7 +795,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
           const int vrow = idx % KT, chunk = idx / KT;
           const int key = ktok0 + vrow;
           if (key >= key_lo && key <= key_hi) continue;
-          uint4* line = reinterpret_cast<uint4*>(vs + chunk * V_CHUNK + vrow * 128);
+          uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
+                                                 (vrow % kTile) * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
         }
@@ -879,20 +895,24 @@ int launch_tc5_pair(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
     return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_prefill: arena_base must come from jenga_arena_create");
   const CUtensorMapDataType dt =
       dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap kv_map;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / (D * 2)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
-  cuuint32_t box[2] = {kBoxCols, kTile};
-  cuuint32_t es[2] = {1, 1};
-  if (fn(&kv_map, dt, 2, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
+  // the arena as [chunk][row][64 columns]: dim1 steps rows (D*2 bytes), dim2 steps
+  // 64-column chunks (128 bytes) — so one box spans several chunks of a row run
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBoxCols), bytes / (D * 2), static_cast<cuuint64_t>(NBOX)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, 128};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap k_map, v_map;
+  cuuint32_t kbox[3] = {kBoxCols, 8, NBOX};            // 8 keys x all chunks (K-major K)
+  cuuint32_t vbox[3] = {kBoxCols, kTile, NBOX / 2};    // 16 keys x this CTA's half of head_dim (V)
+  for (auto [map, box] : {std::pair<CUtensorMap*, cuuint32_t*>{&k_map, kbox}, {&v_map, vbox}})
+    if (fn(map, dt, 3, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
   auto kern = paged_prefill_tc5_pair_kernel<T, D, G, KT, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
   dim3 grid((prm.q_blocks + 1) / 2 * 2, prm.hkv, batch);
-  kern<<<grid, kT5Threads, smem, s>>>(prm, kv_map);
+  kern<<<grid, kT5Threads, smem, s>>>(prm, k_map, v_map);
   return jenga_dev::check_launch("paged_prefill_tc5_pair_kernel");
 }
 
@@ -928,6 +948,12 @@ int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t 
     const char* e = std::getenv("JENGA_PREFILL_2SM");
     return e == nullptr || std::atoi(e) != 0;
   }();
+  static const int ns_env = [] {
+    const char* e = std::getenv("JENGA_PREFILL_NS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (pair && D == 256 && ns_env == 3) return dispatch_pair<T, 256, 3>(G, prm, dtype, s, batch);
+  if (pair && D == 256 && ns_env == 4) return dispatch_pair<T, 256, 4>(G, prm, dtype, s, batch);
   if (pair && D == 256) return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
   if (pair && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
   switch (D) {
