@@ -516,6 +516,16 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const void* tmap, in
       "l"(tmap), "r"(cluster_bar), "r"(0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// 4-D box over the arena as [8-row half][chunk][row][64 cols]: one TMA loads a
+// 16-row page piece of every head_dim chunk in the K layout [half][chunk][8 rows].
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* tmap, int32_t row, uint32_t cluster_bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(cluster_bar), "r"(0), "r"(row), "r"(0), "r"(0), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void umma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
                                          uint32_t acc) {
   asm volatile(
@@ -536,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
     paged_prefill_tc5_pair_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
                                   const __grid_constant__ CUtensorMap v_map) {
   // Shared-memory layouts (all 128-byte swizzled, one TMA box per group / piece):
-  //   K: [8-key group g][chunk c][8 rows][128 B]  (k_map box {64, 8, NBOX});
+  //   K: [8-key group g][chunk c][8 rows][128 B]  (k_map 4-D box {64, 8, NBOX, 2}: one 16-key piece);
   //      the K-major descriptor walks chunks at 1 KiB, 8-key groups at SBO = NBOX KiB
   //   V: [16-key piece][chunk c][16 rows][128 B]  (v_map box {64, 16, VB});
   //      the MN-major descriptor walks chunks at LBO = 2 KiB, 8-key groups at 1 KiB
@@ -633,11 +643,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
       if (lane == 0) {
 #pragma unroll
-        for (int g = 0; g < ((p.diag & 8) ? 0 : KH / 8); ++g) {  // this CTA's half of the keys, 8 at a time
-          const int kk = static_cast<int>(rank) * KH + g * 8;   // key offset within the tile
-          const int32_t pg = rank ? pages[(KH + g * 8) / kTile] : pages[(g * 8) / kTile];
-          const int32_t row = row_of(pg, ktok0 + kk);
-          tma_load_3d_pair(ks + g * K_GROUP, &k_map, row, 0, full0, policy);
+        for (int pc = 0; pc < ((p.diag & 8) ? 0 : KH / kTile); ++pc) {  // this CTA's half of the keys, a page piece each
+          const int kk = static_cast<int>(rank) * KH + pc * kTile;   // key offset within the tile
+          const int32_t pg = rank ? pages[KH / kTile + pc] : pages[pc];
+          tma_load_4d_pair(ks + pc * 2 * K_GROUP, &k_map, row_of(pg, ktok0 + kk), full0, policy);
         }
 #pragma unroll
         for (int pc = 0; pc < ((p.diag & 4) ? 0 : KT / kTile); ++pc) {  // all keys, this CTA's half of head_dim
@@ -901,13 +910,20 @@ int launch_tc5_pair(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, 128};
   cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap k_map, v_map;
-  cuuint32_t kbox[3] = {kBoxCols, 8, NBOX};            // 8 keys x all chunks (K-major K)
   cuuint32_t vbox[3] = {kBoxCols, kTile, NBOX / 2};    // 16 keys x this CTA's half of head_dim (V)
-  for (auto [map, box] : {std::pair<CUtensorMap*, cuuint32_t*>{&k_map, kbox}, {&v_map, vbox}})
-    if (fn(map, dt, 3, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-        CUDA_SUCCESS)
-      return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
+  if (fn(&v_map, dt, 3, const_cast<uint8_t*>(prm.arena), dims, strides, vbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: V tensor map encode failed");
+  // K: a fourth dimension steps 8 rows, so one box = 16 keys laid out [half][chunk][8 rows]
+  cuuint64_t kdims[4] = {static_cast<cuuint64_t>(kBoxCols), bytes / (D * 2), static_cast<cuuint64_t>(NBOX), 2};
+  cuuint64_t kstrides[3] = {static_cast<cuuint64_t>(D) * 2, 128, static_cast<cuuint64_t>(D) * 2 * 8};
+  cuuint32_t kbox[4] = {kBoxCols, 8, NBOX, 2};
+  cuuint32_t kes[4] = {1, 1, 1, 1};
+  if (fn(&k_map, dt, 4, const_cast<uint8_t*>(prm.arena), kdims, kstrides, kbox, kes, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: K tensor map encode failed");
   auto kern = paged_prefill_tc5_pair_kernel<T, D, G, KT, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
