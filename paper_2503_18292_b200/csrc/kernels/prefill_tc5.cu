@@ -55,7 +55,6 @@ struct Prefill5Params {
   int64_t window;
   int max_blocks, hq, hkv, tpp, q_blocks;
   float qscale, cap_log2, inv_cap;
-  int diag;  // JENGA_PREFILL_DIAG (pair kernel, timing experiments only): 1 no softmax math, 2 no K/V loads
 };
 
 // ---------------------------------------------------------------- tcgen05
@@ -624,17 +623,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
     const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
     PageLookahead pl;
     pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
-    const int ptiles = (p.diag & 2) ? 0 : ntiles;
     // pages of one tile (KT / tpp <= 4 for tpp >= 16), looked up once in key order
     auto row_of = [&](int32_t page, int tok) {
       return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
     };
-    for (int j = 0; j < ptiles; ++j) {
+    for (int j = 0; j < ntiles; ++j) {
       const int st = j % NS;
       if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
       const uint32_t full0 = map_to_cta0(&kv_full[st]);
-      if (rank == 0 && lane == 0)
-        expect_tx_cta0(full0, (p.diag & 4) ? 2 * K_BYTES : ((p.diag & 8) ? 2 * V_BYTES : 2 * STAGE));
+      if (rank == 0 && lane == 0) expect_tx_cta0(full0, 2 * STAGE);
       uint8_t* ks = ring + st * STAGE;
       uint8_t* vs = ks + K_BYTES;
       const int ktok0 = (tile_lo + j) * KT;
@@ -643,13 +640,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
       if (lane == 0) {
 #pragma unroll
-        for (int pc = 0; pc < ((p.diag & 8) ? 0 : KH / kTile); ++pc) {  // this CTA's half of the keys, a page piece each
+        for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys, a page piece each
           const int kk = static_cast<int>(rank) * KH + pc * kTile;   // key offset within the tile
           const int32_t pg = rank ? pages[KH / kTile + pc] : pages[pc];
           tma_load_4d_pair(ks + pc * 2 * K_GROUP, &k_map, row_of(pg, ktok0 + kk), full0, policy);
         }
 #pragma unroll
-        for (int pc = 0; pc < ((p.diag & 4) ? 0 : KT / kTile); ++pc) {  // all keys, this CTA's half of head_dim
+        for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim
           const int32_t row = row_of(pages[pc], ktok0 + pc * kTile) + p.tpp;
           tma_load_3d_pair(vs + pc * V_PIECE, &v_map, row, static_cast<int>(rank) * VB, full0, policy);
         }
@@ -674,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       jenga_dev::mbar_wait(q_full, 0);
       for (int j = 0; j < ntiles; ++j) {
         const int st = j % NS, sb = j & 1;
-        if (!(p.diag & 2)) jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
+        jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
         tc_fence_after();
         const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
 #pragma unroll
@@ -693,7 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
     const bool row_ok = tok < c_len;
     const int ipos = n - c_len + tok;
     const uint32_t q_full0 = map_to_cta0(q_full);
-    const uint32_t p_full0[2] = {map_to_cta0(&p_full[0]), map_to_cta0(&p_full[1])};
+    const uint32_t p_full0_base = map_to_cta0(&p_full[0]);  // the leader's p_full[i] = base + 8 i
     {
       const uint4* qrow = reinterpret_cast<const uint4*>(
           static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
@@ -729,12 +726,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       const int ktok0 = (tile_lo + j) * KT;
       jenga_dev::mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      if (p.diag & 1) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_cta0(p_full0[sb]);
-        continue;
-      }
       float s[KT];
 #pragma unroll
       for (int c = 0; c < KT; c += 32) {
@@ -815,9 +806,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
       __syncwarp();
       if (lane == 0) {
         if (boundary)
-          arrive_cta0_release(p_full0[sb]);
+          arrive_cta0_release((p_full0_base + 8u * sb));
         else
-          arrive_cta0(p_full0[sb]);
+          arrive_cta0((p_full0_base + 8u * sb));
       }
     }
     if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
@@ -964,12 +955,6 @@ int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t 
     const char* e = std::getenv("JENGA_PREFILL_2SM");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  static const int ns_env = [] {
-    const char* e = std::getenv("JENGA_PREFILL_NS");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (pair && D == 256 && ns_env == 3) return dispatch_pair<T, 256, 3>(G, prm, dtype, s, batch);
-  if (pair && D == 256 && ns_env == 4) return dispatch_pair<T, 256, 4>(G, prm, dtype, s, batch);
   if (pair && D == 256) return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
   if (pair && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
   switch (D) {
@@ -1009,11 +994,6 @@ int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_s
   prm.hkv = hkv;
   prm.tpp = tpp;
   prm.q_blocks = q_blocks_128;
-  static const int diag = [] {
-    const char* e = std::getenv("JENGA_PREFILL_DIAG");
-    return e ? std::atoi(e) : 0;
-  }();
-  prm.diag = diag;
 
   prm.qscale = qscale;
   prm.cap_log2 = cap_log2;
