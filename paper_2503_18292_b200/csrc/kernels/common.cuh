@@ -146,6 +146,16 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, in
       : "memory");
 }
 
+// 4-D TMA tensor load (UTMALDG.4D) of the box at {0, row, 0, 0}.
+__device__ __forceinline__ void tma_load_4d_row(void* smem_dst, const void* tmap, int32_t row, uint64_t* bar,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %2, %2}], [%4], %5;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(0), "r"(row), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // L2 prefetch of a 2-D TMA box (no shared-memory destination): raises the
 // bytes in flight beyond what the shared-memory ring can hold.
 __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int32_t c0, int32_t c1) {

@@ -39,6 +39,7 @@ struct DecodeParams {
   float* part_acc; // [B][Hkv][max_splits][G][D]
   float* part_ml;  // [B][Hkv][max_splits][G][2]
   int* counters;   // [B][Hkv]
+  int kv_box;      // tensor-core kernel, one head per CTA: tmap is the 4-D K+V box view
 };
 
 // Grid = (Hkv, batch, max_splits) when grid_order == 0 (default);

@@ -262,10 +262,16 @@ __device__ __forceinline__ void head_store(HeadState<D>& st, float* s_acc, float
 // its V rows tpp later).
 template <int D, int HG>
 __device__ __forceinline__ void load_stage(const CUtensorMap* tmap, uint8_t* stage, uint64_t* bar, int32_t row,
-                                           int tpp, int v_rows, uint64_t policy) {
+                                           int tpp, int v_rows, uint64_t policy, bool kv_box) {
   constexpr int NBOX = D / kBoxCols;
   constexpr int TILE_BYTES = NBOX * kBoxBytes;
   jenga_dev::mbar_arrive_expect_tx(bar, 2 * HG * TILE_BYTES);
+  if (HG == 1 && kv_box) {
+    // one 4-D box = the head's K and V tiles of the page: {64 cols, 16 rows, NBOX
+    // chunks, K|V}, landing [K|V][chunk][16 rows][128 B] — the ldmatrix layout
+    jenga_dev::tma_load_4d_row(stage, tmap, row, bar, policy);
+    return;
+  }
 #pragma unroll
   for (int hl = 0; hl < HG; ++hl)
 #pragma unroll
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
           jenga_dev::pdl_wait();
           waited = true;
         }
-        load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], row, p.tpp, v_rows, policy);
+        load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], row, p.tpp, v_rows, policy, p.kv_box != 0);
         row = next;
       }
     }
@@ -499,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
           if (seq >= NS) jenga_dev::mbar_wait(&empty[st], ((seq / NS) & 1) ^ 1);
           const int tok0 = (d.t_begin + it) * kTile;
           load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], tile_row(p, table, d.h0, tok0, D * 2), p.tpp,
-                            v_rows, policy);
+                            v_rows, policy, p.kv_box != 0);
         }
       }
     }
@@ -559,11 +565,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// One [rows][D] view of the arena per (arena, D, dtype); encoded once.
-int tensor_map(const void* base, int D, int dtype, CUtensorMap* out) {
+// Views of the arena, encoded once per (arena, D, dtype, tpp, kind):
+//  * 2-D [rows][D] with 64 x 16 boxes (several heads per CTA);
+//  * 4-D {64 cols, rows, D/64 chunks at 128 B, K|V at tpp rows} with one box =
+//    a whole head's K and V tile of a page (one head per CTA): 1 TMA op per 16 KiB
+//    instead of 2*D/64 (measured on the prefill producer: TMA op count, not bytes,
+//    bounded delivery).
+int tensor_map(const void* base, int D, int dtype, int tpp, bool kv_box, CUtensorMap* out) {
   static std::mutex mu;
-  static std::map<std::tuple<uintptr_t, int, int>, CUtensorMap> cache;
-  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), D, dtype);
+  static std::map<std::tuple<uintptr_t, int, int, int, bool>, CUtensorMap> cache;
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), D, dtype, kv_box ? tpp : 0, kv_box);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -575,14 +586,27 @@ int tensor_map(const void* base, int D, int dtype, CUtensorMap* out) {
   auto fn = encode_fn();
   if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const uint64_t row_bytes = static_cast<uint64_t>(D) * 2;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / row_bytes};
-  cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile)};
-  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt =
+      dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap m;
-  CUresult r = fn(&m, dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (kv_box) {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(kBoxCols), bytes / row_bytes, static_cast<cuuint64_t>(D / kBoxCols),
+                          2};
+    cuuint64_t strides[3] = {row_bytes, 128, static_cast<cuuint64_t>(tpp) * row_bytes};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile),
+                         static_cast<cuuint32_t>(D / kBoxCols), 2};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    r = fn(&m, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / row_bytes};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile)};
+    cuuint32_t estr[2] = {1, 1};
+    r = fn(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS)
     return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   cache[key] = m;
@@ -663,6 +687,16 @@ int dispatch_d(int D, int G, int hg, const DecodeParams& prm, const CUtensorMap&
   return JENGA_ERR_UNSUPPORTED;
 }
 
+// One 4-D box per (page, head) K+V tile (default); JENGA_DECODE_KV_BOX=0 selects
+// the 2-D boxes for A/B runs.
+bool use_kv_box() {
+  static const bool v = [] {
+    const char* e = std::getenv("JENGA_DECODE_KV_BOX");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 // KV heads per CTA: 1 by default — three 1-head CTAs per SM overlap each
 // other's prologue/epilogue and measured fastest on the Gemma shard
 // (profiles/r01_sweeps.md); JENGA_DECODE_HEADS_PER_CTA=2|4 selects the
@@ -684,12 +718,14 @@ namespace jenga_decode {
 int launch_decode_tc(const DecodeParams& prm, int dtype, int head_dim, int G, int batch, cudaStream_t stream) {
   if (prm.tpp % kTile != 0 || head_dim % kBoxCols != 0 || G > 8) return JENGA_ERR_UNSUPPORTED;
   if (prm.start_offset % (head_dim * 2) || prm.page_stride % (head_dim * 2)) return JENGA_ERR_UNSUPPORTED;
-  CUtensorMap m;
-  const int rc = tensor_map(prm.arena, head_dim, dtype, &m);
-  if (rc != JENGA_OK) return rc;
   const int hg = heads_per_cta(prm.hkv);
-  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, hg, prm, m, batch, stream);
-  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, hg, prm, m, batch, stream);
+  CUtensorMap m;
+  DecodeParams p2 = prm;
+  p2.kv_box = hg == 1 && use_kv_box();
+  const int rc = tensor_map(prm.arena, head_dim, dtype, prm.tpp, p2.kv_box != 0, &m);
+  if (rc != JENGA_OK) return rc;
+  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, hg, p2, m, batch, stream);
+  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, hg, p2, m, batch, stream);
   return JENGA_ERR_UNSUPPORTED;
 }
 
