@@ -573,16 +573,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 //    bounded delivery).
 int tensor_map(const void* base, int D, int dtype, int tpp, bool kv_box, CUtensorMap* out) {
   static std::mutex mu;
-  static std::map<std::tuple<uintptr_t, int, int, int, bool>, CUtensorMap> cache;
-  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), D, dtype, kv_box ? tpp : 0, kv_box);
+  static std::map<std::tuple<uintptr_t, uint64_t, int, int, int, bool>, CUtensorMap> cache;
+  uint64_t bytes = 0;
+  if (!jenga_dev::arena_extent(base, &bytes)) return JENGA_ERR_UNSUPPORTED;  // not a jenga arena
+  // keyed by the extent too: a new arena may reuse a freed arena's address
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), bytes, D, dtype, kv_box ? tpp : 0, kv_box);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
     *out = it->second;
     return JENGA_OK;
   }
-  uint64_t bytes = 0;
-  if (!jenga_dev::arena_extent(base, &bytes)) return JENGA_ERR_UNSUPPORTED;  // not a jenga arena
   auto fn = encode_fn();
   if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const uint64_t row_bytes = static_cast<uint64_t>(D) * 2;
