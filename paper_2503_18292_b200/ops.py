@@ -90,6 +90,13 @@ def build_block_tables(offsets: torch.Tensor, pages: torch.Tensor, first_live: t
 
 def slot_mapping(block_table: torch.Tensor, max_blocks: int, req: torch.Tensor, ordinal: torch.Tensor,
                  tokens_per_page: int, out: torch.Tensor) -> None:
+    """Slot (global page * tpp + offset) of each (request row, 1-based ordinal)."""
+    _need(block_table, torch.int32, "block_table")
+    _need(req, torch.int32, "req")
+    _need(ordinal, torch.int32, "ordinal")
+    _need(out, torch.int64, "out")
+    if ordinal.numel() != req.numel() or out.numel() < req.numel():
+        raise ValueError("req, ordinal and out must describe the same tokens")
     check(lib.jenga_slot_mapping(_ptr(block_table), max_blocks, _ptr(req), _ptr(ordinal), req.numel(),
                                  tokens_per_page, _ptr(out), _stream()))
 
@@ -102,7 +109,11 @@ def reshape_and_cache(arena: Arena, view: LayerView, key: torch.Tensor, value: t
     _need(slots, torch.int64, "slot_mapping")
     if key.stride(-1) != 1 or key.stride(-2) != key.shape[-1] or value.stride() != key.stride():
         raise ValueError("key/value rows must be contiguous with equal strides")
+    if key.dtype != value.dtype or key.dtype not in DTYPE_CODE:
+        raise TypeError("key/value must share one of float32 / bfloat16 / float16")
     T, hkv, d = key.shape
+    if slots.numel() < T:
+        raise ValueError(f"{T} tokens but only {slots.numel()} slots")
     check(lib.jenga_reshape_and_cache(arena.base, view.c(), DTYPE_CODE[key.dtype], hkv, d, tokens_per_page,
                                       _ptr(key), _ptr(value), key.stride(0), _ptr(slots), T, _stream()))
 
@@ -121,11 +132,17 @@ def paged_decode(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out:
                  scale: float, window: int = 0, softcap: float = 0.0,
                  workspace: Optional[DecodeWorkspace] = None) -> torch.Tensor:
     """q/out [B, Hq, D]; block_table int32 [B, max_blocks]; seq_lens int32 [B]."""
+    if q.dim() != 3 or q.dtype not in DTYPE_CODE:
+        raise ValueError("q must be [B, Hq, D] float32 / bfloat16 / float16")
     B, hq, d = q.shape
     _need(q, q.dtype, "q")
     _need(out, q.dtype, "out")
+    if out.shape != q.shape:
+        raise ValueError(f"out shape {tuple(out.shape)} != q shape {tuple(q.shape)}")
     _need(block_table, torch.int32, "block_table")
     _need(seq_lens, torch.int32, "seq_lens")
+    if block_table.dim() != 2 or block_table.shape[0] < B or seq_lens.numel() < B:
+        raise ValueError("block_table must be [>=B, max_blocks] and seq_lens [>=B]")
     max_blocks = block_table.shape[-1]
     if workspace is None:
         workspace = DecodeWorkspace(B, hq, num_kv_heads, d, max_blocks, tokens_per_page, q.device)
@@ -140,8 +157,12 @@ def paged_prefill(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out
                   max_chunk: int, block_table: torch.Tensor, seq_lens: torch.Tensor, num_kv_heads: int,
                   tokens_per_page: int, scale: float, window: int = 0, softcap: float = 0.0) -> torch.Tensor:
     """Chunked-prefill attention: q/out [T, Hq, D] (bf16/fp16), cu_q int32 [B+1]."""
+    if q.dim() != 3:
+        raise ValueError("q must be [T, Hq, D]")
     T, hq, d = q.shape
     _need(out, q.dtype, "out")
+    if out.shape != q.shape:
+        raise ValueError(f"out shape {tuple(out.shape)} != q shape {tuple(q.shape)}")
     _need(cu_q, torch.int32, "cu_q")
     _need(block_table, torch.int32, "block_table")
     _need(seq_lens, torch.int32, "seq_lens")
