@@ -62,11 +62,32 @@ class DecodeEngine:
         self._req_arr = np.zeros(max_batch, dtype=np.uint64)
         self.now = 0
         self.tables: List[GroupTables] = []
+        # Every group's CSR page lists live in ONE pinned staging buffer with a
+        # device mirror, so a step's table upload is a single H2D copy.
+        widths = []
         for g, gg in enumerate(geom.groups):
             tpp = self.spec.groups[g].tokens_per_page
             mt = (group_max_tokens or {}).get(g, max_tokens)
-            max_blocks = 1 if gg.kind == LayerKind.kMamba else math.ceil(mt / tpp) + 1
-            pin = dict(dtype=torch.int32, pin_memory=True)
+            widths.append(1 if gg.kind == LayerKind.kMamba else math.ceil(mt / tpp) + 1)
+        sizes = [(max_batch + 1) + 2 * max_batch * mb + 2 * max_batch for mb in widths]
+        self._h_stage = torch.zeros(sum(sizes), dtype=torch.int32, pin_memory=True)
+        self._d_stage = torch.zeros(sum(sizes), dtype=torch.int32, device=self.device)
+        base = 0
+        for g, gg in enumerate(geom.groups):
+            tpp = self.spec.groups[g].tokens_per_page
+            max_blocks = widths[g]
+
+            def carve(buf, b0=base, mb=max_blocks):
+                o = b0
+                parts = []
+                for n in (max_batch + 1, 2 * max_batch * mb, max_batch, max_batch):
+                    parts.append(buf[o:o + n])
+                    o += n
+                parts[1] = parts[1].view(max_batch * mb, 2)
+                return parts
+            h_off, h_pg, h_fl, h_ns = carve(self._h_stage)
+            d_off, d_pg, d_fl, d_ns = carve(self._d_stage)
+            base += sizes[g]
             dev = dict(dtype=torch.int32, device=self.device)
             t = GroupTables(
                 geom=gg, slots_per_large=self.addr.slots_per_large(g),
@@ -74,11 +95,8 @@ class DecodeEngine:
                 block_table=torch.full((max_batch, max_blocks), -1, **dev),
                 seq_lens=torch.zeros(max_batch, **dev),
                 slot_mapping=torch.full((max_batch,), -1, dtype=torch.int64, device=self.device),
-                h_offsets=torch.zeros(max_batch + 1, **pin),
-                h_pages=torch.zeros((max_batch * max_blocks, 2), **pin),
-                h_first_live=torch.zeros(max_batch, **pin), h_n_stored=torch.zeros(max_batch, **pin),
-                d_offsets=torch.zeros(max_batch + 1, **dev), d_pages=torch.zeros((max_batch * max_blocks, 2), **dev),
-                d_first_live=torch.zeros(max_batch, **dev), d_n_stored=torch.zeros(max_batch, **dev))
+                h_offsets=h_off, h_pages=h_pg, h_first_live=h_fl, h_n_stored=h_ns,
+                d_offsets=d_off, d_pages=d_pg, d_first_live=d_fl, d_n_stored=d_ns)
             if gg.is_attention:
                 t.workspace = ops.DecodeWorkspace(max_batch, gg.num_q_heads, gg.num_kv_heads, gg.head_dim,
                                                   max_blocks, tpp, self.device)
@@ -134,19 +152,15 @@ class DecodeEngine:
         return totals
 
     def upload_tables(self, groups: Optional[Sequence[int]] = None, totals: Optional[Dict[int, int]] = None) -> None:
-        """Device half: pinned -> device copies and the block-table build.
-        With totals=None the whole table capacity is copied, so the call has a
-        fixed shape and can be captured in a CUDA graph (replayed after
-        pack_tables refilled the pinned buffers)."""
+        """Device half: one pinned -> device copy of the staging buffer (every
+        group's page lists), then the block-table build per group.  Fixed shape,
+        so it can be captured in a CUDA graph (replayed after pack_tables refilled
+        the pinned buffer).  `totals` is accepted for API symmetry with
+        pack_tables; the whole staging buffer is copied either way."""
         n = len(self.requests)
+        self._d_stage.copy_(self._h_stage, non_blocking=True)
         for g in (range(len(self.tables)) if groups is None else groups):
             t = self.tables[g]
-            total = t.h_pages.shape[0] if totals is None else totals[g]
-            t.d_offsets[: n + 1].copy_(t.h_offsets[: n + 1], non_blocking=True)
-            if total:
-                t.d_pages[:total].copy_(t.h_pages[:total], non_blocking=True)
-            t.d_first_live[:n].copy_(t.h_first_live[:n], non_blocking=True)
-            t.d_n_stored[:n].copy_(t.h_n_stored[:n], non_blocking=True)
             tpp = self.spec.groups[g].tokens_per_page
             ops.build_block_tables(t.d_offsets[: n + 1], t.d_pages, t.d_first_live, t.d_n_stored,
                                    t.slots_per_large, tpp, t.max_blocks, t.block_table, t.slot_mapping, t.seq_lens)
