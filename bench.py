@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--tpp", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--unfused", action="store_true",
+                   help="separate reshape_and_cache + paged_decode launches instead of jenga_paged_decode_append")
     p.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly instead of one CUDA graph "
                                                           "per step")
     p.add_argument("--layers-per-group", type=int, default=21)
@@ -278,11 +280,15 @@ def run_ours(a, rank, world, local_rank):
             j = slot[i]
             if hooks is not None:
                 hooks["before"](j)
-            if kind != LayerKind.kCrossAttention:  # cross KV (image tokens) is static during decode
+            fused = kind != LayerKind.kCrossAttention and not a.unfused
+            if kind != LayerKind.kCrossAttention and a.unfused:  # cross KV (image tokens) is static in decode
                 eng.write_kv(g, l, kn[j], vn[j])
             if ev is not None:
                 ev[j][0].record(stream)
-            eng.decode(g, l, q[j], out[j])
+            if fused:  # newest token's K/V appended by the decode launch itself
+                eng.decode_append(g, l, q[j], kn[j], vn[j], out[j])
+            else:
+                eng.decode(g, l, q[j], out[j])
             if ev is not None:
                 ev[j][1].record(stream)
             if hooks is not None:
@@ -479,7 +485,8 @@ def run_ours(a, rank, world, local_rank):
             traffic = json.loads(tf.read_text()).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
-    kname = f"paged_decode_tc_kernel<bf16, D={D}, G={H // Hkv}> (TMA + mma.sync)"
+    kname = (f"paged_decode_tc_kernel<bf16, D={D}, G={H // Hkv}> (TMA + mma.sync" +
+             ("" if a.unfused else ", newest K/V appended in the same launch") + ")")
     res = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",

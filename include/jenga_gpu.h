@@ -335,6 +335,21 @@ int jenga_paged_decode(void* arena_base, jenga_layer_view view, int kind, int dt
                        float scale, float softcap, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* One decode step of one layer in a single launch: the newest token's key/value
+ * rows ([B][Hkv][D], written to slot_mapping[b]; < 0 skips) are appended to the
+ * arena and attended together with the stored ordinals — the reshape_and_cache
+ * + paged_decode pair of SimEngine::decode_one (simulator.cpp:549-566) fused.
+ * seq_lens[b] must already count the new token (it is ordinal seq_lens[b]).
+ * Full / sliding-window groups only (cross-attention KV is static in decode).
+ * The tensor-core kernel patches the row into its staged K/V tile; other
+ * shapes run reshape_and_cache then paged_decode on the same stream. */
+int jenga_paged_decode_append(void* arena_base, jenga_layer_view view, int kind, int dtype,
+                              uint64_t window, const void* q, const void* key, const void* value,
+                              const int64_t* slot_mapping, void* out, const int32_t* block_table,
+                              const int32_t* seq_lens, int batch, int max_blocks, int num_q_heads,
+                              int num_kv_heads, int head_dim, uint32_t tokens_per_page, float scale,
+                              float softcap, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Chunked-prefill paged attention (bf16/fp16, tokens_per_page % 16 == 0):
  * request b's queries are q[cu_q[b] .. cu_q[b+1]) — its newest ordinals
  * (0-based positions seq_lens[b]-C_b .. seq_lens[b]-1), whose K/V were already

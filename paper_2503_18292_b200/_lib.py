@@ -149,6 +149,8 @@ _SIGS = {
     "jenga_paged_decode_workspace_size": (C.c_size_t, [_int, _int, _int, _int, _int, _u32]),
     "jenga_paged_decode": (_int, [_p, LayerViewC, _int, _int, _u64, _p, _p, _p, _p, _int, _int, _int, _int, _int,
                                   _u32, C.c_float, C.c_float, _p, C.c_size_t, _p]),
+    "jenga_paged_decode_append": (_int, [_p, LayerViewC, _int, _int, _u64, _p, _p, _p, _p, _p, _p, _p, _int, _int,
+                                         _int, _int, _int, _u32, C.c_float, C.c_float, _p, C.c_size_t, _p]),
     "jenga_paged_prefill": (_int, [_p, LayerViewC, _int, _int, _u64, _p, _p, _p, _int, _int, _p, _p, _int, _int,
                                    _int, _int, _int, _u32, C.c_float, C.c_float, _p]),
     "jenga_mamba_state_gather": (_int, [_p, LayerViewC, _p, _int, _p, _p]),

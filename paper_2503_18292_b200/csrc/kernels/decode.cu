@@ -372,11 +372,12 @@ JENGA_EXPORT size_t jenga_paged_decode_workspace_size(int batch, int num_q_heads
   return static_cast<size_t>(counters + bh * ms * G * head_dim * 4 + bh * ms * G * 2 * 4);
 }
 
-JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int kind, int dtype, uint64_t window,
-                                    const void* q, void* out, const int32_t* block_table, const int32_t* seq_lens,
-                                    int batch, int max_blocks, int num_q_heads, int num_kv_heads, int head_dim,
-                                    uint32_t tokens_per_page, float scale, float softcap, void* workspace,
-                                    size_t workspace_bytes, void* stream) {
+namespace {
+int paged_decode_impl(void* arena_base, jenga_layer_view view, int kind, int dtype, uint64_t window, const void* q,
+                      void* out, const int32_t* block_table, const int32_t* seq_lens, int batch, int max_blocks,
+                      int num_q_heads, int num_kv_heads, int head_dim, uint32_t tokens_per_page, float scale,
+                      float softcap, void* workspace, size_t workspace_bytes, const void* k_new, const void* v_new,
+                      const int64_t* new_slots, void* stream) {
   using namespace jenga_dev;
   if (batch < 0 || num_kv_heads <= 0 || num_q_heads <= 0 || num_q_heads % num_kv_heads != 0 ||
       tokens_per_page == 0 || max_blocks <= 0 || !arena_base || !q || !out || !block_table || !seq_lens)
@@ -446,8 +447,19 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((dtype == JENGA_BF16 || dtype == JENGA_F16) && tpp % kTile == 0) {
+    prm.k_new = k_new;  // the tensor-core kernel fuses the append
+    prm.v_new = v_new;
+    prm.new_slots = new_slots;
     const int rc = launch_decode_tc(prm, dtype, head_dim, static_cast<int>(G), batch, s);
     if (rc != JENGA_ERR_UNSUPPORTED) return rc;
+    prm.k_new = prm.v_new = nullptr;
+    prm.new_slots = nullptr;
+  }
+  if (k_new != nullptr) {  // CUDA-core kernel: write the new token first, then attend
+    const int rc = jenga_reshape_and_cache(arena_base, view, dtype, num_kv_heads, head_dim, tokens_per_page, k_new,
+                                           v_new, static_cast<int64_t>(num_kv_heads) * head_dim, new_slots, batch,
+                                           stream);
+    if (rc != JENGA_OK) return rc;
   }
   switch (dtype) {
     case JENGA_F32: return dispatch_d<float>(head_dim, static_cast<int>(G), prm, batch, s);
@@ -455,4 +467,31 @@ JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int
     case JENGA_F16: return dispatch_d<__half>(head_dim, static_cast<int>(G), prm, batch, s);
   }
   return set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_decode: unsupported dtype");
+}
+}  // namespace
+
+JENGA_EXPORT int jenga_paged_decode(void* arena_base, jenga_layer_view view, int kind, int dtype, uint64_t window,
+                                    const void* q, void* out, const int32_t* block_table, const int32_t* seq_lens,
+                                    int batch, int max_blocks, int num_q_heads, int num_kv_heads, int head_dim,
+                                    uint32_t tokens_per_page, float scale, float softcap, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  return paged_decode_impl(arena_base, view, kind, dtype, window, q, out, block_table, seq_lens, batch, max_blocks,
+                           num_q_heads, num_kv_heads, head_dim, tokens_per_page, scale, softcap, workspace,
+                           workspace_bytes, nullptr, nullptr, nullptr, stream);
+}
+
+JENGA_EXPORT int jenga_paged_decode_append(void* arena_base, jenga_layer_view view, int kind, int dtype,
+                                           uint64_t window, const void* q, const void* key, const void* value,
+                                           const int64_t* slot_mapping, void* out, const int32_t* block_table,
+                                           const int32_t* seq_lens, int batch, int max_blocks, int num_q_heads,
+                                           int num_kv_heads, int head_dim, uint32_t tokens_per_page, float scale,
+                                           float softcap, void* workspace, size_t workspace_bytes, void* stream) {
+  if (kind == JENGA_KIND_CROSS_ATTENTION)
+    return jenga_dev::set_error(JENGA_ERR_UNSUPPORTED,
+                                "jenga_paged_decode_append: cross-attention KV is static during decode");
+  if (batch > 0 && (key == nullptr || value == nullptr || slot_mapping == nullptr))
+    return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_decode_append: key, value and slot_mapping required");
+  return paged_decode_impl(arena_base, view, kind, dtype, window, q, out, block_table, seq_lens, batch, max_blocks,
+                           num_q_heads, num_kv_heads, head_dim, tokens_per_page, scale, softcap, workspace,
+                           workspace_bytes, key, value, slot_mapping, stream);
 }

@@ -40,6 +40,11 @@ struct DecodeParams {
   float* part_ml;  // [B][Hkv][max_splits][G][2]
   int* counters;   // [B][Hkv]
   int kv_box;      // tensor-core kernel, one head per CTA: tmap is the 4-D K+V box view
+  // Fused append (jenga_paged_decode_append): the newest token's K/V rows
+  // [B][Hkv][D] and slots; nullptr = plain decode (K/V already in the arena).
+  const void* k_new;
+  const void* v_new;
+  const int64_t* new_slots;
 };
 
 // Grid = (Hkv, batch, max_splits) when grid_order == 0 (default);

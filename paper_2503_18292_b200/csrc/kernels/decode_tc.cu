@@ -222,6 +222,36 @@ __device__ __forceinline__ void head_tile(HeadState<D>& st, uint8_t* ks, uint8_t
   }
 }
 
+// Fused append: the warp whose tile holds the newest token (tile row `row`)
+// writes that token's K and V rows of its head into the arena slot AND into
+// the staged tile (the TMA brought the slot's previous bytes), so the
+// reshape_and_cache launch and its dependency disappear from the step.
+// 16-byte unit u of 64-column chunk c sits at c*kBoxBytes + row*128 + ((u ^ (row & 7)) << 4).
+template <typename T, int D>
+__device__ __forceinline__ void patch_newest(const DecodeParams& p, uint8_t* ks, uint8_t* vs, int b, int h, int row,
+                                             int lane) {
+  constexpr int UNITS = D * 2 / 16;  // 16-byte units per row
+  const int64_t slot = p.new_slots[b];
+  if (slot < 0) return;
+  const int64_t page = slot / p.tpp, off = slot - page * p.tpp;
+  uint8_t* dst = const_cast<uint8_t*>(p.arena) + p.start_offset + page * p.page_stride +
+                 (static_cast<int64_t>(2 * h) * p.tpp + off) * (D * 2);
+  const int64_t src = (static_cast<int64_t>(b) * p.hkv + h) * (D * 2);
+  for (int i = lane; i < UNITS; i += 32) {
+    const int c = i >> 3, u = i & 7;
+    const uint4 kx = jenga_dev::ld_nc_v4(static_cast<const uint8_t*>(p.k_new) + src + i * 16);
+    const uint4 vx = jenga_dev::ld_nc_v4(static_cast<const uint8_t*>(p.v_new) + src + i * 16);
+    const int sm = c * kBoxBytes + row * 128 + ((u ^ (row & 7)) << 4);
+    *reinterpret_cast<uint4*>(ks + sm) = kx;
+    *reinterpret_cast<uint4*>(vs + sm) = vx;
+    jenga_dev::st_v4(dst + i * 16, kx);
+    jenga_dev::st_v4(dst + static_cast<int64_t>(p.tpp) * (D * 2) + i * 16, vx);
+  }
+  // generic-proxy writes into a TMA stage: order them before its next refill
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncwarp();
+}
+
 // Reduce the per-lane l partials and write this warp's unnormalised state to
 // the merge area s_acc[warp][G][D] / s_ml[warp][G][2].
 template <int D, int G>
@@ -354,8 +384,8 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
         const int tok0 = (wk.t_begin + it) * kTile;
         const int32_t next = it + 1 < wk.t_count ? tile_row(p, table, h0, tok0 + kTile, D * 2) : 0;
         if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
-        if (!waited && tok0 + kTile >= wk.n) {  // the tile holding the newest token
-          jenga_dev::pdl_wait();
+        if (!waited && tok0 + kTile >= wk.n && p.k_new == nullptr) {  // the tile holding the newest token
+          jenga_dev::pdl_wait();  // (fused append patches that row itself: no wait)
           waited = true;
         }
         load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], row, p.tpp, v_rows, policy, p.kv_box != 0);
@@ -374,8 +404,10 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
     const int st = it % NS;
     jenga_dev::mbar_wait(&full[st], (it / NS) & 1);
     uint8_t* stage = smem + st * STAGE_BYTES;
-    head_tile<T, D>(hs, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, (wk.t_begin + it) * kTile, wk.lo,
-                    wk.n, p, lane);
+    const int tok0 = (wk.t_begin + it) * kTile;
+    if (p.k_new != nullptr && wk.n - 1 >= tok0 && wk.n - 1 < tok0 + kTile)
+      patch_newest<T, D>(p, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, b, h0 + hl, wk.n - 1 - tok0, lane);
+    head_tile<T, D>(hs, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, tok0, wk.lo, wk.n, p, lane);
     __syncwarp();
     if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
   }
@@ -630,7 +662,7 @@ int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaS
   constexpr int STAGE = 2 * HG * kTile * D * 2;
   constexpr int MERGE = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
   constexpr int CTAS_PER_SM = HG >= 4 ? 1 : (HG == 2 ? 2 : 3);
-  if (use_persistent(batch)) {
+  if (use_persistent(batch) && prm.k_new == nullptr) {
     // ring budget net of the separate merge area, a multiple of the rounds
     constexpr int ROUNDS = kConsumerWarps / HG;
     constexpr int BUDGET = ring_budget<HG>() - MERGE;

@@ -183,6 +183,20 @@ class DecodeEngine:
                                 gg.head_dim ** -0.5 if scale is None else scale, window=gg.window,
                                 softcap=self.geom.softcap if softcap is None else softcap, workspace=t.workspace)
 
+    def decode_append(self, g: int, layer: int, q: torch.Tensor, key: torch.Tensor, value: torch.Tensor,
+                      out: torch.Tensor, scale: Optional[float] = None, softcap: Optional[float] = None) -> torch.Tensor:
+        """write_kv + decode of one layer in one launch (the newest token's K/V
+        go to this group's slot_mapping built with the tables)."""
+        t = self.tables[g]
+        gg = t.geom
+        B = q.shape[0]
+        return ops.paged_decode_append(self.arena, self.view(g, layer), int(gg.kind), q, key, value,
+                                       t.slot_mapping[:B], out, t.block_table[:B], t.seq_lens[:B], gg.num_kv_heads,
+                                       self.spec.groups[g].tokens_per_page,
+                                       gg.head_dim ** -0.5 if scale is None else scale, window=gg.window,
+                                       softcap=self.geom.softcap if softcap is None else softcap,
+                                       workspace=t.workspace)
+
     def mamba_page_globals(self, g: int) -> torch.Tensor:
         """int64 global index of each request's working state page (-1: none)."""
         t = self.tables[g]

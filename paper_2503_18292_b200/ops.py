@@ -153,6 +153,40 @@ def paged_decode(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out:
     return out
 
 
+def paged_decode_append(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, key: torch.Tensor,
+                        value: torch.Tensor, slots: torch.Tensor, out: torch.Tensor, block_table: torch.Tensor,
+                        seq_lens: torch.Tensor, num_kv_heads: int, tokens_per_page: int, scale: float,
+                        window: int = 0, softcap: float = 0.0,
+                        workspace: Optional[DecodeWorkspace] = None) -> torch.Tensor:
+    """One fused decode step of a layer: append the newest token's key/value
+    [B, Hkv, D] at `slots` (int64 [B]) and attend (jenga_paged_decode_append)."""
+    if q.dim() != 3 or q.dtype not in DTYPE_CODE:
+        raise ValueError("q must be [B, Hq, D] float32 / bfloat16 / float16")
+    B, hq, d = q.shape
+    _need(q, q.dtype, "q")
+    _need(out, q.dtype, "out")
+    _need(key, q.dtype, "key")
+    _need(value, q.dtype, "value")
+    _need(slots, torch.int64, "slot_mapping")
+    if out.shape != q.shape:
+        raise ValueError(f"out shape {tuple(out.shape)} != q shape {tuple(q.shape)}")
+    if tuple(key.shape) != (B, num_kv_heads, d) or value.shape != key.shape or slots.numel() < B:
+        raise ValueError("key/value must be [B, Hkv, D] with one slot per request")
+    _need(block_table, torch.int32, "block_table")
+    _need(seq_lens, torch.int32, "seq_lens")
+    if block_table.dim() != 2 or block_table.shape[0] < B or seq_lens.numel() < B:
+        raise ValueError("block_table must be [>=B, max_blocks] and seq_lens [>=B]")
+    max_blocks = block_table.shape[-1]
+    if workspace is None:
+        workspace = DecodeWorkspace(B, hq, num_kv_heads, d, max_blocks, tokens_per_page, q.device)
+    check(lib.jenga_paged_decode_append(arena.base, view.c(), int(kind), DTYPE_CODE[q.dtype], int(window), _ptr(q),
+                                        _ptr(key), _ptr(value), _ptr(slots), _ptr(out), _ptr(block_table),
+                                        _ptr(seq_lens), B, max_blocks, hq, num_kv_heads, d, tokens_per_page,
+                                        float(scale), float(softcap), workspace.buf.data_ptr(), workspace.nbytes,
+                                        _stream()))
+    return out
+
+
 def paged_prefill(arena: Arena, view: LayerView, kind: int, q: torch.Tensor, out: torch.Tensor, cu_q: torch.Tensor,
                   max_chunk: int, block_table: torch.Tensor, seq_lens: torch.Tensor, num_kv_heads: int,
                   tokens_per_page: int, scale: float, window: int = 0, softcap: float = 0.0) -> torch.Tensor:

@@ -228,3 +228,44 @@ def test_launch_counter_and_errors():
     with pytest.raises(ValueError):
         ops.paged_decode(eng.arena, eng.view(0, 0), 0, q.cpu(), q.cpu(), eng.tables[0].block_table[:2],
                          eng.tables[0].seq_lens[:2], 8, 16, 1.0)
+
+
+@pytest.mark.parametrize("dtype,hd,hq,hkv,tpp,kind", [
+    (torch.bfloat16, 256, 16, 8, 16, LayerKind.kFullAttention),
+    (torch.bfloat16, 256, 16, 8, 16, LayerKind.kSlidingWindow),
+    (torch.bfloat16, 128, 32, 8, 32, LayerKind.kFullAttention),
+    (torch.float32, 128, 16, 8, 16, LayerKind.kFullAttention),   # CUDA-core kernel: write, then attend
+])
+def test_decode_append_fused(orc, dtype, hd, hq, hkv, tpp, kind):
+    """jenga_paged_decode_append (newest token's K/V patched into the staged
+    tile and written to its slot in the same launch) == reshape_and_cache +
+    paged_decode, bit for bit, in the output and in the arena; and vs the oracle."""
+    window = 300 if kind == LayerKind.kSlidingWindow else 0
+    geom = ModelGeometry("app", [GroupGeometry("g", kind, 2, hkv, hq, hd, dtype, tpp, window=window)])
+    lens = [1, 16, 17, 299, 300, 1025, 2049, 33]
+    eng, ids = make_engine(geom, lens, seed=3)
+    fill_group_kv(eng, 0, [1], seed=5)
+    B = len(lens)
+    gen = torch.Generator(device=eng.device).manual_seed(21)
+    q = torch.randn((B, hq, hd), generator=gen, device=eng.device).to(dtype)
+    k = torch.randn((B, hkv, hd), generator=gen, device=eng.device).to(dtype)
+    v = torch.randn((B, hkv, hd), generator=gen, device=eng.device).to(dtype)
+    at = eng.arena.tensor()
+    saved = at.clone()
+    out_a = torch.empty_like(q)
+    eng.write_kv(0, 1, k, v)
+    eng.decode(0, 1, q, out_a)
+    torch.cuda.synchronize()
+    arena_a = at.clone()
+    at.copy_(saved)
+    out_b = torch.empty_like(q)
+    eng.decode_append(0, 1, q, k, v, out_b)
+    torch.cuda.synchronize()
+    assert torch.equal(at, arena_a), "fused append wrote different arena bytes"
+    assert torch.equal(out_b, out_a), "fused append changed the attention output"
+    t = eng.tables[0]
+    qh = q.view(torch.int16).cpu().numpy() if dtype != torch.float32 else q.cpu().numpy()
+    want = orc.paged_decode(arena_host(eng), tuple(eng.view(0, 1)), int(kind), ORC_DTYPE[dtype], window, qh,
+                            t.block_table[:B].cpu().numpy(), t.seq_lens[:B].cpu().numpy(), hq, hkv, hd, tpp,
+                            hd ** -0.5, 0.0, nthreads=8)
+    assert rel_err(out_b.float().cpu().numpy(), want) <= TOL[dtype]
