@@ -4,7 +4,8 @@ variant, 10 replays each:
 
   decode_only   42 x paged_decode (full / SWA alternating)
   with_kv       42 x (reshape_and_cache + paged_decode)   (bench --unfused)
-  fused         42 x paged_decode_append                 (the bench step's device half)
+  fused         42 x paged_decode_append
+  fused_tables  table upload + builds + 42 x paged_decode_append (the bench step's device half)
 
 Prints one JSON line: ms per step and GB/s (live KV bytes / time) per variant.
 """
@@ -43,9 +44,11 @@ def main(B=32, ctx=8192, reps=10):
     live = sum(int(eng.live_tokens(g).sum()) for g in (0, 1)) * 8192 * L
 
     def step(mode):
+        if mode == "fused_tables":  # + the step's table upload (one H2D copy) and block-table builds
+            eng.upload_tables()
         for i in range(2 * L):
             g, layer = i % 2, i // 2
-            if mode == "fused":
+            if mode in ("fused", "fused_tables"):
                 eng.decode_append(g, layer, q[i], kv[i], kv[i], out[i])
                 continue
             if mode == "with_kv":
@@ -53,7 +56,7 @@ def main(B=32, ctx=8192, reps=10):
             eng.decode(g, layer, q[i], out[i])
 
     res = {}
-    for name in ("decode_only", "with_kv", "fused"):
+    for name in ("decode_only", "with_kv", "fused", "fused_tables"):
         wk = name
         for _ in range(2):
             step(wk)
