@@ -250,15 +250,12 @@ def run_ours(a, rank, world, local_rank):
     for _, g, _ in attn:
         attn_layers_per_group[g] = attn_layers_per_group.get(g, 0) + 1
 
-    # The pinned page-list buffers are reused every step: before packing step s+1
-    # the host waits until step s's H2D copies have read them (an event recorded
-    # right after the table upload, also inside the captured graph), so the host
-    # runs at most one step ahead and every step uploads its own tables.
-    h2d_done = torch.cuda.Event(external=True)
-
+    # The pinned page-list buffer is reused every step: pack_tables waits until the
+    # previous upload's H2D copy has read it (DecodeEngine records an event after
+    # the copy, also inside the captured graph), so the host runs at most one step
+    # ahead and every step uploads its own tables.
     def host_step():
         """Host half of a step: allocator append + CSR pack into pinned memory."""
-        h2d_done.synchronize()
         eng.append()
         return eng.pack_tables()
 
@@ -266,7 +263,6 @@ def run_ours(a, rank, world, local_rank):
         """Device half: table upload/build, then per layer KV write + decode
         (fixed shape when totals is None, so it can be graph-captured)."""
         eng.upload_tables(None, totals)
-        h2d_done.record(torch.cuda.current_stream())  # the capture stream inside graph capture
         pg = {}
         for i, (g, l) in enumerate(wl.layers):
             kind = eng.tables[g].geom.kind

@@ -72,6 +72,10 @@ class DecodeEngine:
         sizes = [(max_batch + 1) + 2 * max_batch * mb + 2 * max_batch for mb in widths]
         self._h_stage = torch.zeros(sum(sizes), dtype=torch.int32, pin_memory=True)
         self._d_stage = torch.zeros(sum(sizes), dtype=torch.int32, device=self.device)
+        # Recorded after each upload's H2D copy (also inside a captured graph):
+        # pack_tables waits on it before rewriting the pinned buffer, so a host
+        # running ahead of the GPU never overwrites page lists not yet copied.
+        self._h2d_done = torch.cuda.Event(external=True)
         base = 0
         for g, gg in enumerate(geom.groups):
             tpp = self.spec.groups[g].tokens_per_page
@@ -137,6 +141,7 @@ class DecodeEngine:
         Returns the page count per group."""
         n = len(self.requests)
         rp = self._req_arr.ctypes.data_as(C.POINTER(C.c_uint64))
+        self._h2d_done.synchronize()  # the previous upload has read the pinned buffer
         totals = {}
         for g in (range(len(self.tables)) if groups is None else groups):
             t = self.tables[g]
@@ -159,6 +164,7 @@ class DecodeEngine:
         pack_tables; the whole staging buffer is copied either way."""
         n = len(self.requests)
         self._d_stage.copy_(self._h_stage, non_blocking=True)
+        self._h2d_done.record(torch.cuda.current_stream())
         for g in (range(len(self.tables)) if groups is None else groups):
             t = self.tables[g]
             tpp = self.spec.groups[g].tokens_per_page

@@ -144,8 +144,7 @@ class Runner:
             eng.sync_tables()
             for layer in range(self.a.layers):
                 for g in (0, 1):
-                    eng.write_kv(g, layer, k, v)
-                    eng.decode(g, layer, q, out)
+                    eng.decode_append(g, layer, q, k, v, out)
             if timed:
                 live += sum(int(x) for g in (0, 1) for x in eng.live_tokens(g)) * self.a.layers
         e1.record()
