@@ -230,17 +230,17 @@ def test_launch_counter_and_errors():
                          eng.tables[0].seq_lens[:2], 8, 16, 1.0)
 
 
-@pytest.mark.parametrize("dtype,hd,hq,hkv,tpp,kind", [
-    (torch.bfloat16, 256, 16, 8, 16, LayerKind.kFullAttention),
-    (torch.bfloat16, 256, 16, 8, 16, LayerKind.kSlidingWindow),
-    (torch.bfloat16, 128, 32, 8, 32, LayerKind.kFullAttention),
-    (torch.float32, 128, 16, 8, 16, LayerKind.kFullAttention),   # CUDA-core kernel: write, then attend
+@pytest.mark.parametrize("dtype,hd,hq,hkv,tpp,kind,window", [
+    (torch.bfloat16, 256, 16, 8, 16, LayerKind.kFullAttention, 0),
+    (torch.bfloat16, 256, 16, 8, 16, LayerKind.kSlidingWindow, 300),
+    (torch.bfloat16, 128, 32, 8, 16, LayerKind.kSlidingWindow, 7),   # window inside the newest tile
+    (torch.bfloat16, 128, 32, 8, 32, LayerKind.kFullAttention, 0),
+    (torch.float32, 128, 16, 8, 16, LayerKind.kFullAttention, 0),    # CUDA-core kernel: write, then attend
 ])
-def test_decode_append_fused(orc, dtype, hd, hq, hkv, tpp, kind):
+def test_decode_append_fused(orc, dtype, hd, hq, hkv, tpp, kind, window):
     """jenga_paged_decode_append (newest token's K/V patched into the staged
     tile and written to its slot in the same launch) == reshape_and_cache +
     paged_decode, bit for bit, in the output and in the arena; and vs the oracle."""
-    window = 300 if kind == LayerKind.kSlidingWindow else 0
     geom = ModelGeometry("app", [GroupGeometry("g", kind, 2, hkv, hq, hd, dtype, tpp, window=window)])
     lens = [1, 16, 17, 299, 300, 1025, 2049, 33]
     eng, ids = make_engine(geom, lens, seed=3)
