@@ -381,17 +381,18 @@ def run_ours(a, rank, world, local_rank):
         hk.copy_(kn)
         hv.copy_(vn)
 
-        # Copies ride a side stream in layer chunks: chunk c+1's inputs land
-        # while chunk c decodes, chunk c's outputs leave as soon as it is done
-        # (one cross-stream wait per chunk keeps PDL chaining inside chunks).
+        # Copies ride a side stream in layer chunks: later inputs land while the
+        # first layers decode, outputs leave while the last layers decode.  Every
+        # cross-stream wait / event record inside the step breaks the PDL chain
+        # (~15 us each: one chunk per layer costs +0.6 ms a step), so only three
+        # chunks each way: inputs [0,1) [1,3) [3,L) and outputs [0,L-3) [L-3,L-1)
+        # [L-1,L).  Measured (Gemma step, 22 MB in / 11 MB out at 55 GB/s): the
+        # e2e step stays ~0.5 ms above the device step however the inputs are
+        # chunked — H2D DMA writes interleaved with the decode's read stream cost
+        # about what they would serialised.
         cs = torch.cuda.Stream(device=dev)
-        # geometric chunks: the first layer waits only for its own inputs, the
-        # last layer's outputs leave alone (short start-up and drain)
-        grow = [0]
-        while grow[-1] < na:
-            grow.append(min(na, 2 * grow[-1] + 1))
-        in_bounds = grow
-        out_bounds = sorted({na - x for x in grow})
+        in_bounds = sorted({0, min(1, na), min(3, na), na})
+        out_bounds = sorted({0, max(na - 3, 0), max(na - 1, 0), na})
         ev_in = [torch.cuda.Event() for _ in range(len(in_bounds) - 1)]
         ev_out = [torch.cuda.Event() for _ in range(len(out_bounds) - 1)]
         in_start = {in_bounds[c]: c for c in range(len(in_bounds) - 1)}
