@@ -20,10 +20,12 @@ from paper_2503_18292_b200.engine import DecodeEngine  # noqa: E402
 from paper_2503_18292_b200.geometry import gemma2_9b  # noqa: E402
 
 
-def run(B, ctx, chunk, iters=10):
+def run(B, ctx, chunk, iters=10, heads=(16, 8, 256)):
+    H, Hkv, D = heads
     geom = gemma2_9b(16)
     for g in geom.groups:
         g.num_layers = 1
+        g.num_q_heads, g.num_kv_heads, g.head_dim = H, Hkv, D
     pages = B * (ctx // 16 + 4) * 2 + 16
     eng = DecodeEngine(geom, pages, B, ctx + 64)
     eng.add_requests(range(B))
@@ -33,7 +35,6 @@ def run(B, ctx, chunk, iters=10):
     for _ in range(ctx):
         eng.append()
     eng.sync_tables()
-    H, Hkv, D = 16, 8, 256
     T = B * chunk
     cu = torch.arange(0, T + 1, chunk, dtype=torch.int32, device="cuda")
     q = torch.randn((T, H, D), device="cuda").to(torch.bfloat16)
@@ -42,7 +43,7 @@ def run(B, ctx, chunk, iters=10):
     out = torch.empty_like(q)
     req = torch.arange(B, dtype=torch.int32, device="cuda").repeat_interleave(chunk)
     ords = (torch.arange(chunk, dtype=torch.int32, device="cuda") + (ctx - chunk + 1)).repeat(B)
-    res = {"B": B, "ctx": ctx, "chunk": chunk}
+    res = {"B": B, "ctx": ctx, "chunk": chunk, "heads": f"Hq={H} Hkv={Hkv} D={D}"}
     for g, name in ((0, "full"), (1, "swa")):
         t = eng.tables[g]
         slots = torch.empty(T, dtype=torch.int64, device="cuda")
@@ -82,3 +83,6 @@ def run(B, ctx, chunk, iters=10):
 if __name__ == "__main__":
     for B, ctx, chunk in ((4, 8192, 2048), (16, 4096, 512), (64, 2048, 256)):
         run(B, ctx, chunk)
+    if "--d128" in sys.argv:  # Llama-3.2 / Jamba attention heads
+        for B, ctx, chunk in ((4, 8192, 2048), (16, 4096, 512)):
+            run(B, ctx, chunk, heads=(32, 8, 128))
