@@ -142,6 +142,23 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
+// Single-CTA 3-D / 4-D TMA loads (box at {0, row, c2[, 0]}).
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int32_t row, int32_t c2, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(0), "r"(row), "r"(c2), "r"(jenga_dev::smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int32_t row, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %2, %2}], [%4], %5;\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(0), "r"(row), "r"(jenga_dev::smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // Warp-cooperative look-ahead over one request's block table for the TMA
 // producer: lane l holds table[base + l] (cur) and table[base + 32 + l] (nxt),
 // so a page lookup is a shuffle instead of a dependent global load per 16-row
@@ -175,11 +192,16 @@ struct PageLookahead {
 // NS = K/V ring stages.
 template <typename T, int D, int G, int KT, int NS>
 __global__ void __launch_bounds__(kT5Threads, 1)
-    paged_prefill_tc5_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap kv_map) {
+    paged_prefill_tc5_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
+                             const __grid_constant__ CUtensorMap v_map) {
+  // Same box layouts as the CTA-pair kernel, whole tile per CTA:
+  //   K: [8-key group][chunk][8 rows][128 B], one 4-D box per 16-key page piece;
+  //   V: [16-key piece][chunk][16 rows][128 B], one 3-D box per piece.
   constexpr int NBOX = D / kBoxCols;          // 64-column chunks of head_dim
   constexpr int QB = kRows / G;               // tokens per query block
-  constexpr int KV_CHUNK = KT * 128;          // one 64-col chunk of a K or V tile
-  constexpr int KV_BYTES = NBOX * KV_CHUNK;   // K (or V) of one tile, one head
+  constexpr int K_GROUP = NBOX * 8 * 128;     // one 8-key group, all chunks
+  constexpr int V_PIECE = NBOX * kTile * 128; // one 16-key piece, all chunks
+  constexpr int KV_BYTES = NBOX * KT * 128;   // K (or V) of one tile, one head
   constexpr int STAGE = 2 * KV_BYTES;
   constexpr int PIECES = KT / kTile;          // 16-row TMA boxes per tile chunk
   constexpr int Q_COL = D;                    // Q: D/2 packed columns after O
@@ -240,7 +262,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
   if (warp == kProducerWarp) {  // the whole warp walks the table; lane 0 issues
-    if (lane == 0) jenga_dev::prefetch_tmap(&kv_map);
+    if (lane == 0) {
+      jenga_dev::prefetch_tmap(&k_map);
+      jenga_dev::prefetch_tmap(&v_map);
+    }
     const uint64_t policy = jenga_dev::l2_policy_evict_first();
     const int64_t row_bytes = D * 2;
     const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
@@ -259,13 +284,8 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         const int32_t row = static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows +
                                                  tok % p.tpp);
         if (lane == 0) {
-#pragma unroll
-          for (int bx = 0; bx < NBOX; ++bx) {
-            jenga_dev::tma_load_2d(ks + bx * KV_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols, row, &kv_full[st],
-                                   policy);
-            jenga_dev::tma_load_2d(ks + KV_BYTES + bx * KV_CHUNK + pc * kTile * 128, &kv_map, bx * kBoxCols,
-                                   row + v_rows, &kv_full[st], policy);
-          }
+          tma_load_4d(ks + pc * 2 * K_GROUP, &k_map, row, &kv_full[st], policy);
+          tma_load_3d(ks + KV_BYTES + pc * V_PIECE, &v_map, row + v_rows, 0, &kv_full[st], policy);
         }
       }
     }
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + KV_BYTES);
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k)
-          umma_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * 16 * 128, KV_CHUNK, 1024), id_o,
+          umma_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o,
                   (jj > 0 || k > 0) ? 1u : 0u);
         umma_commit(&p_empty[sb]);          // O updated
         umma_commit(&kv_empty[jj % NS]);    // K/V stage free
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)   // S = Q K^T: Q from TMEM, K [KT][D] K-major
           umma_ts(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
-                  umma_desc(k_u + (k >> 2) * KV_CHUNK + (k & 3) * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+                  umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
         umma_commit(&s_full[sb]);
         if (j >= 1) issue_pv(j - 1);
       }
@@ -418,7 +438,8 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           const int vrow = idx % KT, chunk = idx / KT;
           const int key = ktok0 + vrow;
           if (key >= key_lo && key <= key_hi) continue;
-          uint4* line = reinterpret_cast<uint4*>(vs + chunk * KV_CHUNK + vrow * 128);
+          uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
+                                                 (vrow % kTile) * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
         }
@@ -855,10 +876,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <typename T, int D, int G, int KT, int NS>
-int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
-  constexpr int NBOX = D / kBoxCols;
-  const int smem = NS * 2 * NBOX * KT * 128 + (1 + 2 * NS + 6) * 8 + 16 + 1024;
+// K as [half][chunk][8 rows] 4-D boxes (one per 16-key page piece) and V as
+// [chunk][16 rows] 3-D boxes of `v_chunks` 64-column chunks, over the arena
+// viewed as [chunk][row][64 columns] (dim1 steps rows, dim2 steps chunks at 128 B).
+int encode_kv_maps(const Prefill5Params& prm, int dtype, int D, int v_chunks, CUtensorMap* k_map,
+                   CUtensorMap* v_map) {
   auto fn = encode_fn();
   if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   uint64_t bytes = 0;
@@ -866,20 +888,36 @@ int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) 
     return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_prefill: arena_base must come from jenga_arena_create");
   const CUtensorMapDataType dt =
       dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap kv_map;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / (D * 2)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * 2};
-  cuuint32_t box[2] = {kBoxCols, kTile};
-  cuuint32_t es[2] = {1, 1};
-  if (fn(&kv_map, dt, 2, const_cast<uint8_t*>(prm.arena), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  const cuuint32_t nbox = static_cast<cuuint32_t>(D / kBoxCols);
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBoxCols), bytes / (D * 2), nbox};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, 128};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  cuuint32_t vbox[3] = {kBoxCols, kTile, static_cast<cuuint32_t>(v_chunks)};
+  if (fn(v_map, dt, 3, const_cast<uint8_t*>(prm.arena), dims, strides, vbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS)
-    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: KV tensor map encode failed");
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: V tensor map encode failed");
+  cuuint64_t kdims[4] = {static_cast<cuuint64_t>(kBoxCols), bytes / (D * 2), nbox, 2};
+  cuuint64_t kstrides[3] = {static_cast<cuuint64_t>(D) * 2, 128, static_cast<cuuint64_t>(D) * 2 * 8};
+  cuuint32_t kbox[4] = {kBoxCols, 8, nbox, 2};
+  if (fn(k_map, dt, 4, const_cast<uint8_t*>(prm.arena), kdims, kstrides, kbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: K tensor map encode failed");
+  return JENGA_OK;
+}
+
+template <typename T, int D, int G, int KT, int NS>
+int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  constexpr int NBOX = D / kBoxCols;
+  const int smem = NS * 2 * NBOX * KT * 128 + (1 + 2 * NS + 6) * 8 + 16 + 1024;
+  CUtensorMap k_map, v_map;
+  if (int rc = encode_kv_maps(prm, dtype, D, NBOX, &k_map, &v_map)) return rc;
   auto kern = paged_prefill_tc5_kernel<T, D, G, KT, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
   dim3 grid(prm.q_blocks, prm.hkv, batch);
-  kern<<<grid, kT5Threads, smem, s>>>(prm, kv_map);
+  kern<<<grid, kT5Threads, smem, s>>>(prm, k_map, v_map);
   return jenga_dev::check_launch("paged_prefill_tc5_kernel");
 }
 
@@ -888,33 +926,8 @@ int launch_tc5_pair(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
   constexpr int NBOX = D / kBoxCols;
   constexpr int STAGE = NBOX * (KT / 2) * 128 + (NBOX / 2) * KT * 128;
   const int smem = NS * STAGE + (1 + 2 * NS + 6) * 8 + 16 + 1024;
-  auto fn = encode_fn();
-  if (fn == nullptr) return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  uint64_t bytes = 0;
-  if (!jenga_dev::arena_extent(prm.arena, &bytes))
-    return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_paged_prefill: arena_base must come from jenga_arena_create");
-  const CUtensorMapDataType dt =
-      dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  // the arena as [chunk][row][64 columns]: dim1 steps rows (D*2 bytes), dim2 steps
-  // 64-column chunks (128 bytes) — so one box spans several chunks of a row run
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBoxCols), bytes / (D * 2), static_cast<cuuint64_t>(NBOX)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, 128};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUtensorMap k_map, v_map;
-  cuuint32_t vbox[3] = {kBoxCols, kTile, NBOX / 2};    // 16 keys x this CTA's half of head_dim (V)
-  if (fn(&v_map, dt, 3, const_cast<uint8_t*>(prm.arena), dims, strides, vbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: V tensor map encode failed");
-  // K: a fourth dimension steps 8 rows, so one box = 16 keys laid out [half][chunk][8 rows]
-  cuuint64_t kdims[4] = {static_cast<cuuint64_t>(kBoxCols), bytes / (D * 2), static_cast<cuuint64_t>(NBOX), 2};
-  cuuint64_t kstrides[3] = {static_cast<cuuint64_t>(D) * 2, 128, static_cast<cuuint64_t>(D) * 2 * 8};
-  cuuint32_t kbox[4] = {kBoxCols, 8, NBOX, 2};
-  cuuint32_t kes[4] = {1, 1, 1, 1};
-  if (fn(&k_map, dt, 4, const_cast<uint8_t*>(prm.arena), kdims, kstrides, kbox, kes, CU_TENSOR_MAP_INTERLEAVE_NONE,
-         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return jenga_dev::set_error(JENGA_ERR_CUDA, "prefill: K tensor map encode failed");
+  CUtensorMap k_map, v_map;  // V: this CTA's half of head_dim per box
+  if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
   auto kern = paged_prefill_tc5_pair_kernel<T, D, G, KT, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
@@ -956,7 +969,11 @@ int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t 
     return e == nullptr || std::atoi(e) != 0;
   }();
   if (pair && D == 256) return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
-  if (pair && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
+  static const bool pair128 = [] {
+    const char* e = std::getenv("JENGA_PREFILL_2SM_D128");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (pair && pair128 && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
   switch (D) {
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
     case 128: return dispatch_g<T, 128, 6>(G, prm, dtype, s, batch);
