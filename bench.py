@@ -512,7 +512,7 @@ def run_ours(a, rank, world, local_rank):
 
 
 # --------------------------------------------------------------------- CPU baselines
-def cpu_sample(a, steps=1, nthreads=None, requests=4):
+def cpu_sample(a, steps=1, nthreads=None, requests=4, single_core=False):
     """The reference CPU path on a bounded sample of the same workload:
     reference KvAllocator page lists (oracle/_ref when built, else the native
     port's restatement) + reference AddressMap views, then the C attention
@@ -582,13 +582,21 @@ def cpu_sample(a, steps=1, nthreads=None, requests=4):
                          nthreads=nthreads)
     t_attn = (time.perf_counter() - t0) / steps
     kv_bytes = B * (ctx + min(4096, ctx)) * bptl
+    extra = {}
+    if single_core:  # the attention oracle on all host cores and on one
+        t1 = time.perf_counter()
+        orc.paged_decode(arena, (0, small, small), FULL, BF16, 0, q, tables[0], seq, H, Hkv, D, tpp, 1 / 16, nthreads=1)
+        orc.paged_decode(arena, (0, small, small), SWA, BF16, 4096, q, tables[1], seq, H, Hkv, D, tpp, 1 / 16,
+                         nthreads=1)
+        t1 = time.perf_counter() - t1
+        extra = {"single_core_GBps": round(kv_bytes / (t1 + t_tables / max(ctx, 1)) / 1e9, 3)}
     return {"value": round(kv_bytes / (t_attn + t_tables / max(ctx, 1)) / 1e9, 3), "unit": "GB/s",
             "cores": nthreads, "kind": kind,
             "sample": f"{B} requests x {ctx} ctx, 1 full + 1 SWA-4096 layer (Gemma-2-9B heads, bf16); page lists "
                       f"from the {'reference' if kind == 'reference' else 'native'} KvAllocator; attention by the "
                       f"C oracle (fp64) on {nthreads} threads",
             "attention_s_per_layer_pair": round(t_attn, 4),
-            "page_table_build_s": round(t_tables, 4)}
+            "page_table_build_s": round(t_tables, 4), **extra}
 
 
 def run_reference(a):
@@ -638,7 +646,7 @@ def main():
     res = run_ours(a, rank, world, local_rank)
     if rank == 0 and world == 1 and not a.no_cpu_baseline and a.workload == "gemma2-9b":
         try:
-            res["cpu_baseline"] = cpu_sample(a, steps=1)
+            res["cpu_baseline"] = cpu_sample(a, steps=1, single_core=True)
         except Exception as e:  # the baseline must not sink the GPU line
             res["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
                                    "sample": f"failed: {e}"}
