@@ -40,6 +40,7 @@ constexpr int kSoftWarps = 4;
 constexpr int kProducerWarp = 4;
 constexpr int kMmaWarp = 5;
 constexpr int kT5Threads = 6 * 32;
+constexpr int kPPThreads = 10 * 32;  // ping-pong pair kernel: 8 softmax warps + producer + MMA
 constexpr int kBoxCols = 64;
 constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescales
 
@@ -863,6 +864,333 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
   }
 }
 
+template <typename T, int D, int G, int KT, int NS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
+    paged_prefill_tc5_pp_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
+                                const __grid_constant__ CUtensorMap v_map) {
+  // Ping-pong variant of the CTA-pair kernel for head_dim <= 128: each CTA holds
+  // TWO 128-row query tiles (A: query blocks 4q + rank, B: 4q + 2 + rank) with
+  // their own O, Q and S in TMEM and their own softmax warpgroup (warps 0-3: A,
+  // 4-7: B).  Every K/V tile feeds both, and the MMA issuer interleaves
+  //   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+  // so one group's softmax runs while the tensor core works on the other's tile.
+  // Shared-memory layouts (all 128-byte swizzled, one TMA box per group / piece):
+  //   K: [8-key group g][chunk c][8 rows][128 B]  (k_map 4-D box {64, 8, NBOX, 2}: one 16-key piece);
+  //      the K-major descriptor walks chunks at 1 KiB, 8-key groups at SBO = NBOX KiB
+  //   V: [16-key piece][chunk c][16 rows][128 B]  (v_map box {64, 16, VB});
+  //      the MN-major descriptor walks chunks at LBO = 2 KiB, 8-key groups at 1 KiB
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int VB = NBOX / 2;                // V column chunks held by each CTA
+  constexpr int QB = kRows / G;
+  constexpr int KH = KT / 2;                  // keys of the K tile held by each CTA
+  constexpr int K_GROUP = NBOX * 8 * 128;     // one 8-key group, all chunks
+  constexpr int K_BYTES = (KH / 8) * K_GROUP;
+  constexpr int V_PIECE = VB * kTile * 128;   // one 16-key piece, this CTA's chunks
+  constexpr int V_BYTES = (KT / kTile) * V_PIECE;
+  constexpr int STAGE = K_BYTES + V_BYTES;
+  // TMEM per CTA: O_A | O_B | Q_A | Q_B | S_A | S_B
+  constexpr int O_COL0 = 0, Q_COL0 = 2 * D, S_COL0 = 3 * D;
+  constexpr uint32_t TMEM_COLS = 512;
+  static_assert(NBOX % 2 == 0 && KT == 64 && 3 * D + 2 * KT <= 512, "ping-pong kernel shape");
+  constexpr int PW = 8, MW = 9;               // producer, MMA warps (0-7 softmax)
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
+  uint64_t* q_full = bars;                    // leader: 16 softmax warps of the pair
+  uint64_t* kv_full = bars + 1;               // leader: both CTAs' TMA bytes
+  uint64_t* kv_empty = kv_full + NS;          // both: multicast commit
+  uint64_t* s_full = kv_empty + NS;           // both: multicast commit
+  uint64_t* p_full = s_full + 2;              // leader: 8 softmax warps of the pair
+  uint64_t* p_empty = p_full + 2;             // both: multicast commit
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int quad = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
+  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
+  const int pt0 = 4 * quad * QB;
+  if (pt0 >= c_len) return;  // uniform over the pair
+  const int n = p.seq_lens[b];
+  const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
+  const int pos0 = n - c_len + pt0;
+  const int pos1 = n - c_len + min(pt0 + 4 * QB, c_len) - 1;  // union of both tiles' keys
+  int key_lo = 0;
+  const int key_hi = cross ? n - 1 : pos1;
+  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
+  const int tile_lo = key_lo / KT;
+  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    jenga_dev::mbar_init(q_full, 2 * 2 * kSoftWarps);
+    for (int i = 0; i < NS; ++i) {
+      jenga_dev::mbar_init(&kv_full[i], 1);
+      jenga_dev::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      jenga_dev::mbar_init(&s_full[i], 1);
+      jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
+      jenga_dev::mbar_init(&p_empty[i], 1);
+    }
+    jenga_dev::fence_mbar_init();
+  }
+  if (warp == MW) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     jenga_dev::smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
+
+  if (warp == PW) {  // the whole warp walks the table; lane 0 issues
+    if (lane == 0) { jenga_dev::prefetch_tmap(&k_map); jenga_dev::prefetch_tmap(&v_map); }
+    const uint64_t policy = jenga_dev::l2_policy_evict_first();
+    const int64_t row_bytes = D * 2;
+    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
+    const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+    PageLookahead pl;
+    pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
+    // pages of one tile (KT / tpp <= 4 for tpp >= 16), looked up once in key order
+    auto row_of = [&](int32_t page, int tok) {
+      return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
+    };
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % NS;
+      if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+      const uint32_t full0 = map_to_cta0(&kv_full[st]);
+      if (rank == 0 && lane == 0) expect_tx_cta0(full0, 2 * STAGE);
+      uint8_t* ks = ring + st * STAGE;
+      uint8_t* vs = ks + K_BYTES;
+      const int ktok0 = (tile_lo + j) * KT;
+      int32_t pages[KT / kTile];
+#pragma unroll
+      for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
+      if (lane == 0) {
+#pragma unroll
+        for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys, a page piece each
+          const int kk = static_cast<int>(rank) * KH + pc * kTile;   // key offset within the tile
+          const int32_t pg = rank ? pages[KH / kTile + pc] : pages[pc];
+          tma_load_4d_pair(ks + pc * 2 * K_GROUP, &k_map, row_of(pg, ktok0 + kk), full0, policy);
+        }
+#pragma unroll
+        for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim
+          const int32_t row = row_of(pages[pc], ktok0 + pc * kTile) + p.tpp;
+          tma_load_3d_pair(vs + pc * V_PIECE, &v_map, row, static_cast<int>(rank) * VB, full0, policy);
+        }
+      }
+    }
+  } else if (warp == MW) {
+    if (rank == 0 && lane == 0) {
+      const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
+      const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
+      auto issue_s = [&](int jj, int g) {  // S_g(jj) = Q_g K_jj^T (K stage already full)
+        const uint32_t k_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          umma2_ts(tmem + S_COL0 + g * KT, tmem + Q_COL0 + g * (D / 2) + k * 8,
+                   umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
+        umma2_commit_both(&s_full[g]);
+      };
+      auto issue_pv = [&](int jj, int g) {  // O_g += P_g(jj) V_jj
+        jenga_dev::mbar_wait(&p_full[g], jj & 1);
+        tc_fence_after();
+        const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + K_BYTES);
+#pragma unroll
+        for (int k = 0; k < KT / 16; ++k)
+          umma2_ts(tmem + O_COL0 + g * D, tmem + S_COL0 + g * KT + k * 8,
+                   umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o, (jj > 0 || k > 0) ? 1u : 0u);
+        umma2_commit_both(&p_empty[g]);
+      };
+      auto wait_kv = [&](int jj) {
+        jenga_dev::mbar_wait(&kv_full[jj % NS], (jj / NS) & 1);
+        tc_fence_after();
+      };
+      jenga_dev::mbar_wait(q_full, 0);
+      if (ntiles > 0) {
+        wait_kv(0);
+        issue_s(0, 0);
+        issue_s(0, 1);
+      }
+      for (int j = 0; j < ntiles; ++j) {
+        // S_g(j+1) overwrites S_g's buffer (P_g(j)): issued after PV_g(j), in order
+        issue_pv(j, 0);
+        if (j + 1 < ntiles) {
+          wait_kv(j + 1);
+          issue_s(j + 1, 0);
+        }
+        issue_pv(j, 1);
+        umma2_commit_both(&kv_empty[j % NS]);  // both groups' PVs of tile j issued
+        if (j + 1 < ntiles) issue_s(j + 1, 1);
+      }
+    }
+  } else {
+    const int grp = warp >> 2;                  // 0: tile A, 1: tile B
+    const int r = threadIdx.x & (kRows - 1);    // query row == TMEM lane
+    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int Q_COL = Q_COL0 + grp * (D / 2), S_COL = S_COL0 + grp * KT, O_COL = O_COL0 + grp * D;
+    const int t0 = pt0 + (2 * grp + static_cast<int>(rank)) * QB;
+    const int tok = t0 + r / G;
+    const bool row_ok = tok < c_len;
+    const int ipos = n - c_len + tok;
+    const uint32_t q_full0 = map_to_cta0(q_full);
+    const uint32_t p_full0 = map_to_cta0(&p_full[grp]);
+    {
+      const uint4* qrow = reinterpret_cast<const uint4*>(
+          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 x = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + i) : make_uint4(0, 0, 0, 0);
+          w[4 * i] = x.x;
+          w[4 * i + 1] = x.y;
+          w[4 * i + 2] = x.z;
+          w[4 * i + 3] = x.w;
+        }
+        tmem_st32u(tmem + lane_addr + Q_COL + c * 32, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cta0(q_full0);
+    }
+    int lo_r = 0, hi_r = cross ? n - 1 : ipos;
+    if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
+      lo_r = static_cast<int>(ipos + 1 - p.window);
+    if (!row_ok || hi_r < lo_r) lo_r = hi_r = 1 << 30;
+    const uint32_t span = static_cast<uint32_t>(hi_r - lo_r);
+    const bool softcap = p.cap_log2 > 0.f;
+    const float sc = softcap ? 1.f : p.qscale;
+    const float qi = p.qscale * p.inv_cap;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int sb = 0;  // one S buffer per group
+      const int ktok0 = (tile_lo + j) * KT;
+      jenga_dev::mbar_wait(&s_full[grp], j & 1);
+      tc_fence_after();
+      float s[KT];
+#pragma unroll
+      for (int c = 0; c < KT; c += 32) {
+        float v[32];
+        tmem_ld32(tmem + lane_addr + S_COL + sb * KT + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c + i] = v[i];
+      }
+      if (softcap) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
+      }
+      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
+      }
+      float mt = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) mt = fmaxf(mt, s[i]);
+      mt *= sc;
+      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+        const float m_new = fmaxf(m_used, mt);
+        if (j >= 1) {
+          const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
+          jenga_dev::mbar_wait(&p_empty[grp], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + O_COL + c, v);
+            uint32_t u[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
+            tmem_st32u(tmem + lane_addr + O_COL + c, u);
+          }
+          tmem_st_wait();
+          l *= alpha;
+        }
+        m_used = m_new;
+      }
+      uint32_t pk[KT / 2];
+      float rs0 = 0.f, rs1 = 0.f;
+      const float neg = m_used == -INFINITY ? 0.f : -m_used;
+#pragma unroll
+      for (int i = 0; i < KT; i += 2) {
+        const float a = jenga_dev::fast_exp2(fmaf(s[i], sc, neg));
+        const float bb = jenga_dev::fast_exp2(fmaf(s[i + 1], sc, neg));
+        rs0 += a;
+        rs1 += bb;
+        pk[i / 2] = pack2<T>(a, bb);
+      }
+      l += rs0 + rs1;
+#pragma unroll
+      for (int c = 0; c < KT / 2; c += 32) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
+        tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
+      }
+      tmem_st_wait();
+      // zero this CTA's V columns of keys outside the pair's range
+      // boundary V rows: zeroed by group A only (PV_B(j) is issued after PV_A(j))
+      const bool boundary = grp == 0 && (ktok0 < key_lo || ktok0 + KT - 1 > key_hi);
+      if (boundary) {
+        uint8_t* vs = ring + (j % NS) * STAGE + K_BYTES;
+        for (int idx = r; idx < KT * VB; idx += kRows) {
+          const int vrow = idx % KT, chunk = idx / KT;
+          const int key = ktok0 + vrow;
+          if (key >= key_lo && key <= key_hi) continue;
+          uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
+                                                 (vrow % kTile) * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (boundary)
+          arrive_cta0_release(p_full0);
+        else
+          arrive_cta0(p_full0);
+      }
+    }
+    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[grp], (ntiles - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      float v[32];
+      if (ntiles > 0) {
+        tmem_ld32(tmem + lane_addr + O_COL + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
+                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
+                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
+                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's last remote arrivals and MMAs are done
+  if (warp == MW) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -936,6 +1264,32 @@ int launch_tc5_pair(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
   return jenga_dev::check_launch("paged_prefill_tc5_pair_kernel");
 }
 
+template <typename T, int D, int G, int KT, int NS>
+int launch_tc5_pp(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int STAGE = NBOX * (KT / 2) * 128 + (NBOX / 2) * KT * 128;
+  const int smem = NS * STAGE + (1 + 2 * NS + 6) * 8 + 16 + 1024;
+  CUtensorMap k_map, v_map;
+  if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
+  auto kern = paged_prefill_tc5_pp_kernel<T, D, G, KT, NS>;
+  static std::atomic<uint64_t> configured{0};
+  if (int rc = configure_smem(kern, smem, configured)) return rc;
+  dim3 grid((prm.q_blocks + 3) / 4 * 2, prm.hkv, batch);  // a CTA pair per 4 query blocks
+  kern<<<grid, kPPThreads, smem, s>>>(prm, k_map, v_map);
+  return jenga_dev::check_launch("paged_prefill_tc5_pp_kernel");
+}
+
+template <typename T, int D, int NS>
+int dispatch_pp(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  switch (G) {
+    case 1: return launch_tc5_pp<T, D, 1, 64, NS>(prm, dtype, s, batch);
+    case 2: return launch_tc5_pp<T, D, 2, 64, NS>(prm, dtype, s, batch);
+    case 4: return launch_tc5_pp<T, D, 4, 64, NS>(prm, dtype, s, batch);
+    case 8: return launch_tc5_pp<T, D, 8, 64, NS>(prm, dtype, s, batch);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
 template <typename T, int D, int NS>
 int dispatch_pair(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (G) {
@@ -973,6 +1327,12 @@ int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t 
     const char* e = std::getenv("JENGA_PREFILL_2SM_D128");
     return e == nullptr || std::atoi(e) != 0;
   }();
+  static const bool pp = [] {
+    const char* e = std::getenv("JENGA_PREFILL_PP");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  // head_dim 128: two query tiles per CTA, ping-ponged (TMEM: 2 x (O 128 + Q 64 + S 64))
+  if (pair && pair128 && pp && D == 128) return dispatch_pp<T, 128, 8>(G, prm, dtype, s, batch);
   if (pair && pair128 && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
   switch (D) {
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
