@@ -24,14 +24,15 @@ def run_prefill(orc, eng, g, layer, chunks, seed=5):
     out = torch.full_like(q, float("nan"))
     cu_d = torch.from_numpy(cu).to(eng.device)
     scale = gg.head_dim ** -0.5
+    softcap = eng.geom.softcap
     ops.paged_prefill(eng.arena, eng.view(g, layer), int(gg.kind), q, out, cu_d, int(max(chunks)),
                       t.block_table[:B], t.seq_lens[:B], gg.num_kv_heads, eng.spec.groups[g].tokens_per_page, scale,
-                      window=gg.window)
+                      window=gg.window, softcap=softcap)
     torch.cuda.synchronize()
     want = orc.paged_prefill(arena_host(eng), tuple(eng.view(g, layer)), int(gg.kind), ORC_DTYPE[gg.dtype],
                              gg.window, q.view(torch.int16).cpu().numpy(), cu, t.block_table[:B].cpu().numpy(),
                              t.seq_lens[:B].cpu().numpy(), gg.num_q_heads, gg.num_kv_heads, gg.head_dim,
-                             eng.spec.groups[g].tokens_per_page, scale)
+                             eng.spec.groups[g].tokens_per_page, scale, softcap)
     got = out.float().cpu().numpy()
     assert np.isfinite(got).all()
     tol = TOL[gg.dtype]
@@ -62,6 +63,19 @@ def test_prefill_gemma_long_chunk_softcap(orc):
     for g in range(2):
         fill_group_kv(eng, g, [0], seed=g, all_live=True)
         run_prefill(orc, eng, g, 0, [512, 1024])
+
+
+def test_prefill_d128_long_chunk_pingpong(orc):
+    """Llama / Jamba heads (D=128, G=4: the ping-pong pair kernel) on long chunks
+    at a 5k context, full and SWA-1000 with soft-capping."""
+    geom = ModelGeometry("llama-p", [
+        GroupGeometry("full", LayerKind.kFullAttention, 1, 8, 32, 128, torch.bfloat16, 16),
+        GroupGeometry("window", LayerKind.kSlidingWindow, 1, 8, 32, 128, torch.bfloat16, 16, window=1000)],
+        softcap=30.0)
+    eng, ids = make_engine(geom, [5000, 1100, 700], seed=13, defer_window=True)
+    for g in range(2):
+        fill_group_kv(eng, g, [0], seed=g + 3, all_live=True)
+        run_prefill(orc, eng, g, 0, [1500, 1100, 77])
 
 
 def test_prefill_cross_attention(orc):
