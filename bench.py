@@ -512,7 +512,7 @@ def run_ours(a, rank, world, local_rank):
 
 
 # --------------------------------------------------------------------- CPU baselines
-def cpu_sample(a, steps=1, nthreads=None, requests=4, single_core=False):
+def cpu_sample(a, steps=1, nthreads=None, requests=16, single_core=False):
     """The reference CPU path on a bounded sample of the same workload:
     reference KvAllocator page lists (oracle/_ref when built, else the native
     port's restatement) + reference AddressMap views, then the C attention
