@@ -269,3 +269,64 @@ def test_decode_append_fused(orc, dtype, hd, hq, hkv, tpp, kind, window):
                             t.block_table[:B].cpu().numpy(), t.seq_lens[:B].cpu().numpy(), hq, hkv, hd, tpp,
                             hd ** -0.5, 0.0, nthreads=8)
     assert rel_err(out_b.float().cpu().numpy(), want) <= TOL[dtype]
+
+
+def test_fused_append_graph_steps_match_unfused():
+    """Twenty decode steps of a full + SWA model captured as one CUDA graph per
+    step (host append + pack between replays, as bench.py runs it), fused
+    append vs eager reshape_and_cache + paged_decode on an identical engine:
+    every step's outputs and the final arenas are bit-identical, across page
+    boundaries and SWA frees."""
+    from paper_2503_18292_b200.engine import DecodeEngine
+    geom = ModelGeometry("g2", [
+        GroupGeometry("full", LayerKind.kFullAttention, 2, 8, 16, 256, torch.bfloat16, 16),
+        GroupGeometry("window", LayerKind.kSlidingWindow, 2, 8, 16, 256, torch.bfloat16, 16, window=40)])
+    lens = [15, 31, 100]
+    B, steps = len(lens), 20
+    engines = []
+    for _ in range(2):
+        eng = DecodeEngine(geom, 64, B, 160)
+        eng.add_requests(range(B))
+        eng.arena.tensor().zero_()
+        for pos in range(max(lens)):
+            eng.append([r for r in range(B) if pos < lens[r]])
+        engines.append(eng)
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    layers = [(g, l) for l in range(2) for g in (0, 1)]
+    q = torch.randn((steps, len(layers), B, 16, 256), generator=gen, device="cuda").to(torch.bfloat16)
+    kv = torch.randn((steps, len(layers), 2, B, 8, 256), generator=gen, device="cuda").to(torch.bfloat16)
+    outs = [torch.zeros((len(layers), B, 16, 256), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    qs = torch.empty_like(q[0])
+    kvs = torch.empty_like(kv[0])
+    fused, eager = engines
+
+    def fused_device():
+        fused.upload_tables()
+        for i, (g, l) in enumerate(layers):
+            fused.decode_append(g, l, qs[i], kvs[i, 0], kvs[i, 1], outs[0][i])
+
+    fused.append()
+    fused.pack_tables()
+    qs.copy_(q[0])
+    kvs.copy_(kv[0])
+    fused_device()  # warm-up (tensor maps, smem attributes) outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    fused.pack_tables()
+    with torch.cuda.graph(graph):
+        fused_device()
+    for s in range(steps):
+        if s > 0:
+            fused.append()
+        fused.pack_tables()
+        qs.copy_(q[s])
+        kvs.copy_(kv[s])
+        graph.replay()
+        eager.append()
+        eager.sync_tables()
+        for i, (g, l) in enumerate(layers):
+            eager.write_kv(g, l, kv[s, i, 0], kv[s, i, 1])
+            eager.decode(g, l, q[s, i], outs[1][i])
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), f"step {s}: fused graph output differs"
+    assert torch.equal(fused.arena.tensor(), eager.arena.tensor())
