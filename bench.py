@@ -180,7 +180,7 @@ class Workload:
             elif gg.kind == LayerKind.kCrossAttention:
                 smalls = self.B * (math.ceil(self.image_tokens / tpp) + 1)
             elif gg.kind == LayerKind.kSlidingWindow:
-                smalls = self.B * (math.ceil(gg.window / tpp) + 2)
+                smalls = self.B * (math.ceil(min(gg.window, self.ctx + steps + 16) / tpp) + 2)
             else:
                 smalls = self.B * (math.ceil((self.ctx + steps + 16) / tpp) + 1)
             total += math.ceil(smalls / addr.slots_per_large(g)) + self.B  # request-aware units
