@@ -3,11 +3,15 @@
 // CUDA-core kernel in decode.cu; the differences are the data movement and
 // the math:
 //
-//  * K/V tiles move with 2-D TMA tensor loads (cp.async.bulk.tensor -> UTMALDG)
-//    over the whole arena viewed as a [rows][D] matrix, rows = one token of
-//    one (page, layer, K|V, head): row index = (start_offset + global*
-//    page_stride + ((2h + kv)*tpp + off)*D*e) / (D*e).  Boxes of 64 x 16 land in
-//    shared memory with the 128-byte swizzle, so ldmatrix is conflict-free.
+//  * K/V tiles move with TMA tensor loads (cp.async.bulk.tensor -> UTMALDG) over
+//    the whole arena viewed as rows of D elements, row = one token of one
+//    (page, layer, K|V, head): row index = (start_offset + global*page_stride +
+//    ((2h + kv)*tpp + off)*D*e) / (D*e).  One head per CTA (default): ONE 4-D
+//    box {64 cols, 16 rows, D/64 chunks, K|V} per 16-token tile; several heads:
+//    64 x 16 2-D boxes.  Tiles land with the 128-byte swizzle, so ldmatrix is
+//    conflict-free.
+//  * Fused append (jenga_paged_decode_append): the warp whose tile holds the
+//    newest token writes that token's K/V to its slot and into the staged tile.
 //  * One CTA serves HG KV heads of a request: a pipeline stage holds the same
 //    16-token tile of all HG heads, which are adjacent in the head-major
 //    page-layer slice ([Hkv][K|V][tpp][D]), so each stage is one contiguous
