@@ -2,23 +2,33 @@
 // (tcgen05.mma + TMEM), bf16/fp16.  Same contract as prefill.cu (which keeps
 // the mma.sync path for comparison, JENGA_PREFILL_TC5=0).
 //
-// One CTA = (128 query rows, KV head, request); rows are (token, query head)
-// pairs r = t*G + g as in prefill.cu.  Six warps:
-//   warps 0-3  softmax / correction / epilogue: thread r owns query row r,
-//              i.e. TMEM lane r of the S and O accumulators (32x32b loads);
-//              scores are masked with the reference liveness rule
+// Three kernels share the algorithm; rows are (token, query head) pairs
+// r = t*G + g as in prefill.cu, 128 rows per query block:
+//  * paged_prefill_tc5_pair_kernel (head_dim 256, default): a cluster of 2 CTAs,
+//    tcgen05.mma.cta_group::2 with M = 256 over two adjacent query blocks; each
+//    SM holds half of every K/V tile (its half of the keys for K, its half of
+//    head_dim for V).
+//  * paged_prefill_tc5_pp_kernel (head_dim 128, default): the same pair, each
+//    CTA holding TWO query blocks (A, B) with their own O / Q / S in TMEM and
+//    their own softmax warpgroup; the MMA issuer ping-pongs between them.
+//  * paged_prefill_tc5_kernel (head_dim 64, or JENGA_PREFILL_2SM=0): one CTA
+//    per query block, cta_group::1.
+// Warp roles (pair / single: 6 warps; ping-pong: 10):
+//   softmax    thread r owns query row r = TMEM lane r of S and O (32x32b
+//              tcgen05.ld); scores masked with the reference liveness rule
 //              (layer_policies.cpp:105-120), exponentiated against a lazily
-//              updated row max (O is rescaled in TMEM only when the max grows
-//              by more than 2^8), and P is written to shared memory in the
-//              128-byte-swizzled K-major layout the MMA reads.
-//   warp 4     TMA producer: the Q block once (3-D box), then KT-token K/V
-//              tiles of the paged arena (2-D boxes, one per page piece).
-//   warp 5     MMA issuer (one elected thread) and TMEM owner:
-//                S[j%2]  = Q . K_j^T   M=128, N=KT, K=D   (A, B K-major)
-//                O      += P_j . V_j    M=128, N=D,  K=KT  (B MN-major)
-//              software-pipelined: S_{j+1} is issued before O += P_j V_j;
-//              tcgen05.commit releases K/V stages and P buffers.
-// TMEM: O in columns [0, D), S double buffer after it (512 allocated).
+//              updated row max (O rescaled in TMEM only when the max grows by
+//              more than 2^8); P written back over its S columns (tcgen05.st) —
+//              the TMEM A operand of O += P V.
+//   producer   one warp walks the block table (warp-shuffled look-ahead); lane 0
+//              issues one 4-D TMA box per 16-key page piece of K and one 3-D box
+//              per piece of V (128-byte swizzle) into a ring of K/V stages.
+//   MMA        one elected thread, TMEM owner:
+//                S = Q . K_j^T   (A = Q from TMEM, B = K K-major)
+//                O += P_j . V_j  (A = P from TMEM, B = V MN-major)
+//              S_{j+1} issued before O += P_j V_j; tcgen05.commit releases K/V
+//              stages and S/P buffers.
+// TMEM: O in columns [0, D), Q after it (D/2 packed columns), then S buffers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
