@@ -216,7 +216,11 @@ def run_ours(a, rank, world, local_rank):
     dev = torch.device(f"cuda:{local_dev}")
     wl = Workload(a)
     B = wl.B
-    total_steps = a.warmup + a.steps + (0 if a.no_e2e else a.warmup + a.steps) + 2
+    # every host append of the run: warm-up + timed steps, the per-launch event pass
+    # (k_steps below), graph warm-up / capture steps, and the e2e leg (pipelined one
+    # step ahead) — the tables and the arena are sized for all of them
+    total_steps = (a.warmup + a.steps + max(2, a.steps // 4) + 8 +
+                   (0 if a.no_e2e else a.warmup + a.steps + 4))
     eng = DecodeEngine(wl.geom, wl.arena_large_pages(total_steps), B, wl.max_tokens(total_steps), dev,
                        group_max_tokens=wl.group_max_tokens(total_steps))
     ids = shard_requests(list(range(B * world)), rank, world)  # this GPU's requests; its pool is private
