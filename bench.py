@@ -65,7 +65,8 @@ def peaks():
 
 def workload_desc(a):
     return (f"gemma2-9b decode: {a.batch_per_gpu or 32} req/GPU x {a.ctx} ctx, {2 * a.layers_per_group} layers "
-            f"({a.layers_per_group} full + {a.layers_per_group} SWA-4096), Hq=16 Hkv=8 D=256, tpp={a.tpp}")
+            f"({a.layers_per_group} full + {a.layers_per_group} SWA-4096), Hq=16 Hkv=8 D=256, tpp={a.tpp}, "
+            f"logit softcap 50")
 
 
 # --------------------------------------------------------------------- clocks
@@ -129,7 +130,7 @@ class Workload:
             L = a.layers_per_group
             self.layers = [(g, l) for l in range(L) for g in (0, 1)]  # alternating full / SWA
             self.desc = (f"gemma2-9b decode: {self.B} req/GPU x {a.ctx} ctx, {2 * L} layers ({L} full + {L} "
-                         f"SWA-4096), Hq=16 Hkv=8 D=256, tpp={a.tpp}")
+                         f"SWA-4096), Hq=16 Hkv=8 D=256, tpp={a.tpp}, logit softcap {self.geom.softcap:g}")
         elif a.workload == "jamba-style":
             self.geom = jamba_style(a.tpp)
             self.B = a.batch_per_gpu or 64
@@ -581,17 +582,18 @@ def cpu_sample(a, steps=1, nthreads=None, requests=16, single_core=False):
     t0 = time.perf_counter()
     for _ in range(steps):
         orc.paged_decode(arena, (0, small, small), FULL, BF16, 0, q, tables[0], seq, H, Hkv, D, tpp, 1 / 16,
-                         nthreads=nthreads)
+                         50.0, nthreads=nthreads)
         orc.paged_decode(arena, (0, small, small), SWA, BF16, 4096, q, tables[1], seq, H, Hkv, D, tpp, 1 / 16,
-                         nthreads=nthreads)
+                         50.0, nthreads=nthreads)
     t_attn = (time.perf_counter() - t0) / steps
     kv_bytes = B * (ctx + min(4096, ctx)) * bptl
     extra = {}
     if single_core:  # the attention oracle on all host cores and on one
         t1 = time.perf_counter()
-        orc.paged_decode(arena, (0, small, small), FULL, BF16, 0, q, tables[0], seq, H, Hkv, D, tpp, 1 / 16, nthreads=1)
-        orc.paged_decode(arena, (0, small, small), SWA, BF16, 4096, q, tables[1], seq, H, Hkv, D, tpp, 1 / 16,
+        orc.paged_decode(arena, (0, small, small), FULL, BF16, 0, q, tables[0], seq, H, Hkv, D, tpp, 1 / 16, 50.0,
                          nthreads=1)
+        orc.paged_decode(arena, (0, small, small), SWA, BF16, 4096, q, tables[1], seq, H, Hkv, D, tpp, 1 / 16,
+                         50.0, nthreads=1)
         t1 = time.perf_counter() - t1
         extra = {"single_core_GBps": round(kv_bytes / (t1 + t_tables / max(ctx, 1)) / 1e9, 3)}
     return {"value": round(kv_bytes / (t_attn + t_tables / max(ctx, 1)) / 1e9, 3), "unit": "GB/s",

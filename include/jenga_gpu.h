@@ -271,10 +271,15 @@ int jenga_pages_blocks(const jenga_pages* pl, uint64_t request, int g,
  * jenga_build_block_tables:
  *   offsets[n_req+1], pages[offsets[n_req]], first_live_block[n_req],
  *   n_stored[n_req] (stored ordinals; for mamba groups 1 page = working).
- * Pass pages=NULL to query offsets only. */
+ * Pass pages=NULL to query offsets only.  Everything is validated before
+ * anything is written: a request holding more than max_blocks blocks (the
+ * block-table width; <= 0 = unchecked) or a total above pages_capacity
+ * (entries of `pages`) fails with JENGA_ERR_CONFIG, a dead block after the
+ * first live one (the table encodes dead blocks as a leading prefix) or a
+ * pool whose global page indices overflow int32 with JENGA_ERR_INVARIANT. */
 int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64_t* requests,
-                         int n_req, int32_t* offsets, jenga_small_page* pages,
-                         int32_t* first_live_block, int32_t* n_stored);
+                         int n_req, int max_blocks, int64_t pages_capacity, int32_t* offsets,
+                         jenga_small_page* pages, int32_t* first_live_block, int32_t* n_stored);
 
 /* ------------------------------------------------------------------------
  * Device API (sm_100a).  One arena per GPU: num_large_pages x large_page_bytes

@@ -138,7 +138,7 @@ _SIGS = {
     "jenga_pages_seq_len": (_int, [_p, _u64, _pu64]),
     "jenga_pages_group_state": (_int, [_p, _u64, _int, _pu64, _pu64, _pu64, _pu64, _pint, C.POINTER(SmallPage)]),
     "jenga_pages_blocks": (_int, [_p, _u64, _int, C.POINTER(SmallPage), C.POINTER(C.c_uint8), _u64, _pu64]),
-    "jenga_pages_pack_csr": (_int, [_p, _int, _pu64, _int, _pi32, C.POINTER(SmallPage), _pi32, _pi32]),
+    "jenga_pages_pack_csr": (_int, [_p, _int, _pu64, _int, _int, C.c_int64, _pi32, C.POINTER(SmallPage), _pi32, _pi32]),
     "jenga_arena_create": (_int, [_int, _u64, _u64, C.POINTER(_p)]),
     "jenga_arena_destroy": (None, [_p]),
     "jenga_arena_base": (_p, [_p]),

@@ -595,11 +595,19 @@ JENGA_EXPORT int jenga_pages_blocks(const jenga_pages* pl, uint64_t request, int
 }
 
 JENGA_EXPORT int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64_t* requests,
-                                      int n_req, int32_t* offsets, jenga_small_page* pages,
-                                      int32_t* first_live, int32_t* n_stored) {
+                                      int n_req, int max_blocks, int64_t pages_capacity, int32_t* offsets,
+                                      jenga_small_page* pages, int32_t* first_live, int32_t* n_stored) {
   ARG_CHECK(pl != nullptr && requests != nullptr && offsets != nullptr && n_req >= 0 && g >= 0);
+  ARG_CHECK(pages == nullptr || pages_capacity >= 0);
   return guarded([&] {
+    JENGA_CHECK(static_cast<size_t>(g) < pl->kv->num_groups(), "group index out of range");
     const bool mamba = pl->kv->group(g).kind == jenga::LayerKind::kMamba;
+    // Block tables hold int32 AddressMap global indices (large*slots_per_large + slot).
+    JENGA_CHECK(uint64_t{pl->kv->pool().num_pages()} * pl->kv->type_allocator(g).geometry().slots_per_large <=
+                    uint64_t{INT32_MAX},
+                "pool too large for int32 global page indices");
+    // Pass 1: count and validate everything before writing a byte, so an
+    // undersized caller buffer is rejected instead of overrun.
     int64_t off = 0;
     offsets[0] = 0;
     for (int i = 0; i < n_req; ++i) {
@@ -607,18 +615,35 @@ JENGA_EXPORT int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64
       JENGA_CHECK(static_cast<size_t>(g) < r.groups.size(), "group index out of range");
       const auto& rt = r.groups[g];
       const int64_t cnt = mamba ? (rt.working_page ? 1 : 0) : static_cast<int64_t>(rt.blocks.size());
+      if (max_blocks > 0 && cnt > max_blocks)
+        throw jenga::ConfigError("request " + std::to_string(requests[i]) + " holds " + std::to_string(cnt) +
+                                 " blocks; the block table is " + std::to_string(max_blocks) + " wide");
+      if (!mamba) {
+        // the device table marks blocks [0, freed_blocks) dead and every later one
+        // live: a hole after the first live block would hand a freed page to a kernel
+        for (int64_t b = static_cast<int64_t>(rt.freed_blocks); b < cnt; ++b)
+          JENGA_CHECK(rt.blocks[b].live, "dead block after the first live block");
+      }
+      off += cnt;
+      JENGA_CHECK(off <= INT32_MAX, "page list too long for int32 offsets");
+      offsets[i + 1] = static_cast<int32_t>(off);
+    }
+    if (pages != nullptr && off > pages_capacity)
+      throw jenga::ConfigError("page lists need " + std::to_string(off) + " entries; the buffer holds " +
+                               std::to_string(pages_capacity));
+    // Pass 2: write.
+    for (int i = 0; i < n_req; ++i) {
+      const auto& rt = pl->pl->request(requests[i]).groups[g];
+      const int64_t o = offsets[i];
       if (pages) {
         if (mamba) {
-          if (rt.working_page) pages[off] = to_c(*rt.working_page);
+          if (rt.working_page) pages[o] = to_c(*rt.working_page);
         } else {
-          for (int64_t b = 0; b < cnt; ++b) pages[off + b] = to_c(rt.blocks[b].page);
+          for (int64_t b = 0, cnt = offsets[i + 1] - o; b < cnt; ++b) pages[o + b] = to_c(rt.blocks[b].page);
         }
       }
       if (first_live) first_live[i] = mamba ? 0 : static_cast<int32_t>(rt.freed_blocks);
       if (n_stored) n_stored[i] = static_cast<int32_t>(rt.stored);
-      off += cnt;
-      JENGA_CHECK(off <= INT32_MAX, "page list too long for int32 offsets");
-      offsets[i + 1] = static_cast<int32_t>(off);
     }
   });
 }

@@ -21,12 +21,28 @@ int set(int code, const char* msg);
 namespace jenga_dev {
 int set_error(int code, const std::string& msg) { return jenga_host_err::set(code, msg.c_str()); }
 
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("JENGA_PDL");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  return on;
+namespace {
+std::mutex g_stream_mu;
+std::map<std::pair<int, uintptr_t>, bool> g_pdl_writer_pending;  // (device, stream) -> early-trigger writer in chain
+
+std::pair<int, uintptr_t> stream_key(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return {dev, reinterpret_cast<uintptr_t>(s)};
+}
+}  // namespace
+
+void note_launch(cudaStream_t stream, LaunchClass c) {
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  if (c == kLaunchArenaWriterPdl)
+    g_pdl_writer_pending[stream_key(stream)] = true;
+  else
+    g_pdl_writer_pending.erase(stream_key(stream));
+}
+
+bool early_kv_ok(cudaStream_t stream) {
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  return g_pdl_writer_pending.count(stream_key(stream)) == 0;
 }
 
 int num_sms() {

@@ -90,8 +90,11 @@ __global__ void __launch_bounds__(256) reshape_and_cache_kernel(
 // cp.async.bulk shared->global).  The thread refills the stage of the
 // previous chunk as soon as its store has finished reading shared memory, so
 // kCopyStages-1 loads stay in flight; items with a negative index are skipped.
-// Default 16 KiB x 6 stages, 2 CTAs per SM (2 x 96 KiB rings per SM);
-// JENGA_COPY_CFG="chunk_kib,stages,ctas_per_sm" selects another instantiation (A/B runs).
+// 16 KiB x 6 stages, 2 CTAs per SM (2 x 96 KiB rings per SM): the fastest of
+// the chunk / depth / occupancy sweep in profiles/r01_copy_sweep.jsonl.
+constexpr int kCopyChunkBytes = 16384;
+constexpr int kCopyStages = 6;
+constexpr int kCopyCtasPerSm = 2;
 
 struct CopyArgs {
   const uint8_t* src_base;
@@ -246,6 +249,7 @@ int launch_token_rows(bool scatter, void* arena_base, jenga_layer_view view, uin
   kern<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<uint8_t*>(arena_base), view.start_offset, view.exec_page_size, view.page_stride, tpp,
       pieces_per_layer, piece_bytes / 16, row_chunks, static_cast<uint8_t*>(rows), row_stride_bytes, slots, n_tokens);
+  note_launch(static_cast<cudaStream_t>(stream), kLaunchSerializing);
   return check_launch(scatter ? "token_rows_kernel<scatter>" : "token_rows_kernel<gather>");
 }
 
@@ -260,6 +264,7 @@ int launch_copy(const CopyArgs& args, int ctas_per_sm, void* stream, const char*
   const int grid = static_cast<int>(
       std::min<uint64_t>(chunks, static_cast<uint64_t>(jenga_dev::num_sms()) * std::max(1, ctas_per_sm)));
   jenga_dev::launch_maybe_pdl(kern, dim3(grid), dim3(32), smem, static_cast<cudaStream_t>(stream), args);
+  jenga_dev::note_launch(static_cast<cudaStream_t>(stream), jenga_dev::kLaunchArenaWriterPdl);
   return jenga_dev::check_launch(what);
 }
 
@@ -271,29 +276,10 @@ int launch_paged_copy(const void* src_base, uint64_t src_off, uint64_t src_strid
   if (bytes % 16 != 0 || src_off % 16 != 0 || dst_off % 16 != 0 || src_stride % 16 != 0 ||
       dst_stride % 16 != 0 || reinterpret_cast<uintptr_t>(src_base) % 16 || reinterpret_cast<uintptr_t>(dst_base) % 16)
     return set_error(JENGA_ERR_UNSUPPORTED, std::string(what) + ": sizes/offsets must be 16-byte multiples");
-  static const bool keep_ok = [] {  // JENGA_COPY_L2_KEEP=0: no evict_last hints (A/B runs)
-    const char* e = std::getenv("JENGA_COPY_L2_KEEP");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  if (!keep_ok) src_keep = dst_keep = 0;
-  static const std::array<int, 3> cfg = [] {
-    std::array<int, 3> c{16, 6, 2};
-    if (const char* e = std::getenv("JENGA_COPY_CFG")) std::sscanf(e, "%d,%d,%d", &c[0], &c[1], &c[2]);
-    return c;
-  }();
   const CopyArgs args{static_cast<const uint8_t*>(src_base), src_off, src_stride, src_idx,
                       static_cast<uint8_t*>(dst_base), dst_off, dst_stride, dst_idx, bytes / 16, n,
                       src_keep, dst_keep};
-  const int key = cfg[0] * 100 + cfg[1];
-  switch (key) {
-    case 806: return launch_copy<8192, 6>(args, cfg[2], stream, what);
-    case 812: return launch_copy<8192, 12>(args, cfg[2], stream, what);
-    case 1606: return launch_copy<16384, 6>(args, cfg[2], stream, what);
-    case 1612: return launch_copy<16384, 12>(args, cfg[2], stream, what);
-    case 3206: return launch_copy<32768, 6>(args, cfg[2], stream, what);
-    case 3203: return launch_copy<32768, 3>(args, cfg[2], stream, what);
-  }
-  return set_error(JENGA_ERR_ARG, "JENGA_COPY_CFG: unsupported chunk/stages");
+  return launch_copy<kCopyChunkBytes, kCopyStages>(args, kCopyCtasPerSm, stream, what);
 }
 
 }  // namespace
@@ -329,6 +315,7 @@ JENGA_EXPORT int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view
                      k8 + static_cast<int64_t>(t0) * kv_token_stride * e, v8 + static_cast<int64_t>(t0) * kv_token_stride * e,
                      kv_token_stride * e, slot_mapping + t0, total);
   }
+  note_launch(static_cast<cudaStream_t>(stream), kLaunchArenaWriterPdl);
   return check_launch("reshape_and_cache_kernel");
 }
 

@@ -207,10 +207,24 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-bool pdl_enabled();  // JENGA_PDL=0 disables (A/B runs)
-int num_sms();       // SMs of the current device (cached per device)
+int num_sms();  // SMs of the current device (cached per device)
 
-// Launch with the programmatic-stream-serialization attribute when enabled.
+// PDL ordering contract.  Kernels launched with the programmatic attribute may
+// start before their predecessor in the stream has finished; every kernel
+// reads the previous kernels' outputs only after griddepcontrol.wait — except
+// the decode producer, which streams K/V tiles early.  That is safe only when
+// no kernel still in the PDL chain writes arena bytes a later decode reads.
+// The arena writers that trigger their dependents early (reshape_and_cache,
+// the page copies) mark the stream; a launch without the attribute (table
+// builds, prefill, token rows) fully serialises the stream and clears the
+// mark; decode launches leave it as it is (their only arena write is the
+// newest token's row, which the consumer itself patches or waits for).  The
+// decode launcher asks early_kv_ok(): false -> its producer waits first.
+enum LaunchClass { kLaunchArenaWriterPdl = 0, kLaunchSerializing = 1 };
+void note_launch(cudaStream_t stream, LaunchClass c);
+bool early_kv_ok(cudaStream_t stream);
+
+// Launch with the programmatic-stream-serialization attribute.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                              Args&&... args) {
@@ -223,7 +237,7 @@ cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -305,23 +305,9 @@ int splits_for(int max_blocks, int tpp, int tiles_per_split) {
 // it should stream ~512-768 KiB of one head's K+V.  head_dim 256: 32 tiles
 // (512 KiB); head_dim <= 128: 96 * 128/D tiles (768 KiB) — measured +7% (Llama
 // vision) and +10% (Jamba attention) over 32 tiles at D=128
-// (profiles/r01_sweeps.md).  JENGA_DECODE_TILES_PER_SPLIT overrides for sweeps.
+// (profiles/r01_sweeps.md).
 int tiles_per_split(int head_dim) {
-  static const int forced = [] {
-    const char* e = std::getenv("JENGA_DECODE_TILES_PER_SPLIT");
-    const int x = e ? std::atoi(e) : 0;
-    return x >= kMinTilesPerSplit ? x : 0;
-  }();
-  if (forced) return forced;
   return head_dim >= 256 ? kTilesPerSplit : 96 * 128 / std::max(head_dim, 16);
-}
-
-int grid_order() {
-  static const int v = [] {
-    const char* e = std::getenv("JENGA_DECODE_GRID_ORDER");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
 }
 
 template <typename T, int D, int G>
@@ -336,6 +322,7 @@ int launch_typed(const DecodeParams& prm, int batch, cudaStream_t stream) {
   if (int rc = configure_smem(kern, smem, configured)) return rc;
   const dim3 grid = decode_grid(prm, batch);
   kern<<<grid, kThreads, smem, stream>>>(prm);
+  jenga_dev::note_launch(stream, jenga_dev::kLaunchSerializing);
   return jenga_dev::check_launch("paged_decode_kernel");
 }
 
@@ -417,7 +404,6 @@ int paged_decode_impl(void* arena_base, jenga_layer_view view, int kind, int dty
   prm.hkv = num_kv_heads;
   prm.tpp = tpp;
   prm.tiles_per_split = tiles_per_split(head_dim);
-  prm.grid_order = grid_order();
   prm.batch = batch;
   prm.max_splits = splits_for(max_blocks, tpp, prm.tiles_per_split);
   if (kind == JENGA_KIND_SLIDING_WINDOW) {
@@ -441,7 +427,6 @@ int paged_decode_impl(void* arena_base, jenga_layer_view view, int kind, int dty
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const int64_t counters = ((bh * 4 + 16 + 255) / 256) * 256;
   prm.counters = reinterpret_cast<int*>(ws);
-  prm.work = prm.counters + bh;  // two ints after the split tickets
   prm.part_acc = reinterpret_cast<float*>(ws + counters);
   prm.part_ml = prm.part_acc + bh * prm.max_splits * G * head_dim;
 
@@ -450,6 +435,7 @@ int paged_decode_impl(void* arena_base, jenga_layer_view view, int kind, int dty
     prm.k_new = k_new;  // the tensor-core kernel fuses the append
     prm.v_new = v_new;
     prm.new_slots = new_slots;
+    prm.early_kv = jenga_dev::early_kv_ok(s) ? 1 : 0;
     const int rc = launch_decode_tc(prm, dtype, head_dim, static_cast<int>(G), batch, s);
     if (rc != JENGA_ERR_UNSUPPORTED) return rc;
     prm.k_new = prm.v_new = nullptr;

@@ -30,16 +30,16 @@ struct DecodeParams {
   int tpp;
   int tiles_per_split;
   int max_splits;
-  int grid_order;      // 0: (head, request, split); 1: (head, split, request)
   int batch;
-  int* work;           // persistent kernel: [0] next work item, [1] CTAs finished
   float qscale;    // scale*log2e, or scale when soft-capping
   float cap_log2;  // softcap*log2e (0: off)
   float inv_cap;   // 1/softcap
   float* part_acc; // [B][Hkv][max_splits][G][D]
   float* part_ml;  // [B][Hkv][max_splits][G][2]
   int* counters;   // [B][Hkv]
-  int kv_box;      // tensor-core kernel, one head per CTA: tmap is the 4-D K+V box view
+  // 1: the producer may stream K/V before griddepcontrol.wait (no early-
+  // triggering arena writer is still in the PDL chain, common.cuh)
+  int early_kv;
   // Fused append (jenga_paged_decode_append): the newest token's K/V rows
   // [B][Hkv][D] and slots; nullptr = plain decode (K/V already in the arena).
   const void* k_new;
@@ -47,18 +47,10 @@ struct DecodeParams {
   const int64_t* new_slots;
 };
 
-// Grid = (Hkv, batch, max_splits) when grid_order == 0 (default);
-// (Hkv, max_splits, batch) when 1 (JENGA_DECODE_GRID_ORDER, A/B runs).
-__device__ __forceinline__ int grid_request(const DecodeParams& p) {
-  return p.grid_order == 0 ? blockIdx.y : blockIdx.z;
-}
-__device__ __forceinline__ int grid_split(const DecodeParams& p) {
-  return p.grid_order == 0 ? blockIdx.z : blockIdx.y;
-}
-inline dim3 decode_grid(const DecodeParams& p, int batch, int heads_per_cta = 1) {
-  const int hx = p.hkv / heads_per_cta;
-  return p.grid_order == 0 ? dim3(hx, batch, p.max_splits) : dim3(hx, p.max_splits, batch);
-}
+// Grid = (Hkv, batch, max_splits).
+__device__ __forceinline__ int grid_request(const DecodeParams&) { return blockIdx.y; }
+__device__ __forceinline__ int grid_split(const DecodeParams&) { return blockIdx.z; }
+inline dim3 decode_grid(const DecodeParams& p, int batch) { return dim3(p.hkv, batch, p.max_splits); }
 
 // Live ordinals of request b (LayerPolicy::needs_token, layer_policies.cpp:
 // 105-120) cut into splits of whole 16-token tiles.
@@ -68,7 +60,9 @@ struct Work {
 
 __device__ __forceinline__ Work assign_work(const DecodeParams& p, int b, int split) {
   Work w;
-  w.n = p.seq_lens[b];
+  // a length beyond the table width is clamped to the blocks the table holds,
+  // so no kernel ever indexes past the request's row
+  w.n = min(p.seq_lens[b], p.max_blocks * p.tpp);
   w.lo = 0;
   if (p.kind == JENGA_KIND_SLIDING_WINDOW && w.n > p.window) w.lo = static_cast<int>(w.n - p.window);
   const int tile_lo = w.lo / kTile;

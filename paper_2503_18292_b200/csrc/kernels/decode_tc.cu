@@ -6,19 +6,16 @@
 //  * K/V tiles move with TMA tensor loads (cp.async.bulk.tensor -> UTMALDG) over
 //    the whole arena viewed as rows of D elements, row = one token of one
 //    (page, layer, K|V, head): row index = (start_offset + global*page_stride +
-//    ((2h + kv)*tpp + off)*D*e) / (D*e).  One head per CTA (default): ONE 4-D
-//    box {64 cols, 16 rows, D/64 chunks, K|V} per 16-token tile; several heads:
-//    64 x 16 2-D boxes.  Tiles land with the 128-byte swizzle, so ldmatrix is
-//    conflict-free.
+//    ((2h + kv)*tpp + off)*D*e) / (D*e).  ONE 4-D box {64 cols, 16 rows, D/64
+//    chunks, K|V} per 16-token tile brings a head's K and V tiles of a page
+//    (the head-major page-layer slice [Hkv][K|V][tpp][D] makes them one
+//    contiguous 2*16*D*e run).  Tiles land with the 128-byte swizzle, so
+//    ldmatrix is conflict-free.
 //  * Fused append (jenga_paged_decode_append): the warp whose tile holds the
 //    newest token writes that token's K/V to its slot and into the staged tile.
-//  * One CTA serves HG KV heads of a request: a pipeline stage holds the same
-//    16-token tile of all HG heads, which are adjacent in the head-major
-//    page-layer slice ([Hkv][K|V][tpp][D]), so each stage is one contiguous
-//    HG x 16 KiB run of K and V.  Long contiguous runs keep DRAM row locality high under the
-//    page-layer layout, where one layer is only a 128 KiB slice of every
-//    2.75 MiB page (measured: the busiest DRAM channels idle ~18% with 8 KiB
-//    runs).
+//  * One CTA per (KV head, request, split); three CTAs per SM overlap each
+//    other's prologue and merge (multi-head CTAs measured 9% slower on the
+//    Gemma shard, profiles/r01_sweeps.md).
 //  * S^T = K . Q^T and O^T += V^T . P^T run on the tensor cores with
 //    mma.sync m16n8k16 (fp32 accumulate): tokens on M (16 per tile), the G
 //    query heads of one KV head on N (padded to 8), head_dim as K for QK and
@@ -92,22 +89,15 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
-// Shared-memory budget per CTA for the stage ring: 1 CTA/SM when a CTA owns
-// 4 heads, 2 when it owns 2, 3 when it owns 1 (~192 KiB in flight per SM).
-template <int HG>
-constexpr int ring_budget() {
-  return HG >= 4 ? 196608 : (HG == 2 ? 98304 : 65536);
-}
-
-// Ring depth: a multiple of the rounds (kConsumerWarps / HG) so each slot is
-// always consumed by the same warps — a warp that skipped a use of a slot
-// could otherwise wait on a parity two phases ahead and pass early.
-template <int D, int HG>
+// Stage ring: ~64 KiB per CTA (three CTAs per SM, ~192 KiB in flight per SM),
+// a multiple of the four consumer warps so each slot is always consumed by the
+// same warp — a warp that skipped a use of a slot could otherwise wait on a
+// parity two phases ahead and pass early.
+template <int D>
 constexpr int stages() {
-  constexpr int rounds = kConsumerWarps / HG;
-  constexpr int stage = 2 * HG * kTile * D * 2;
-  constexpr int ns = (ring_budget<HG>() / stage) / rounds * rounds;
-  return ns < rounds ? rounds : (ns > 12 ? 12 : ns);
+  constexpr int stage = 2 * kTile * D * 2;
+  constexpr int ns = (65536 / stage) / kConsumerWarps * kConsumerWarps;
+  return ns < kConsumerWarps ? kConsumerWarps : (ns > 12 ? 12 : ns);
 }
 
 // ------------------------------------------------------------ per-warp math
@@ -291,54 +281,36 @@ __device__ __forceinline__ void head_store(HeadState<D>& st, float* s_acc, float
   }
 }
 
-// TMA loads of one tile (16 tokens) of HG heads into a stage: K of heads
-// h0..h0+HG-1, then their V (head-major slice: head h's K rows at 2*h*tpp,
-// its V rows tpp later).
-template <int D, int HG>
+// TMA load of one 16-token tile of one head into a stage: ONE 4-D box
+// {64 cols, 16 rows, D/64 chunks, K|V} = the head's K and V tiles of the page,
+// landing [K|V][chunk][16 rows][128 B] — the ldmatrix layout.
+template <int D>
 __device__ __forceinline__ void load_stage(const CUtensorMap* tmap, uint8_t* stage, uint64_t* bar, int32_t row,
-                                           int tpp, int v_rows, uint64_t policy, bool kv_box) {
-  constexpr int NBOX = D / kBoxCols;
-  constexpr int TILE_BYTES = NBOX * kBoxBytes;
-  jenga_dev::mbar_arrive_expect_tx(bar, 2 * HG * TILE_BYTES);
-  if (HG == 1 && kv_box) {
-    // one 4-D box = the head's K and V tiles of the page: {64 cols, 16 rows, NBOX
-    // chunks, K|V}, landing [K|V][chunk][16 rows][128 B] — the ldmatrix layout
-    jenga_dev::tma_load_4d_row(stage, tmap, row, bar, policy);
-    return;
-  }
-#pragma unroll
-  for (int hl = 0; hl < HG; ++hl)
-#pragma unroll
-    for (int bx = 0; bx < NBOX; ++bx)
-      jenga_dev::tma_load_2d(stage + hl * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols, row + hl * 2 * tpp,
-                             bar, policy);
-#pragma unroll
-  for (int hl = 0; hl < HG; ++hl)
-#pragma unroll
-    for (int bx = 0; bx < NBOX; ++bx)
-      jenga_dev::tma_load_2d(stage + (HG + hl) * TILE_BYTES + bx * kBoxBytes, tmap, bx * kBoxCols,
-                             row + v_rows + hl * 2 * tpp, bar, policy);
+                                           uint64_t policy) {
+  constexpr int TILE_BYTES = (D / kBoxCols) * kBoxBytes;
+  jenga_dev::mbar_arrive_expect_tx(bar, 2 * TILE_BYTES);
+  jenga_dev::tma_load_4d_row(stage, tmap, row, bar, policy);
 }
 
-// Arena row of the first K row of (page of token tok0, head h0).
-__device__ __forceinline__ int32_t tile_row(const DecodeParams& p, const int32_t* table, int h0, int tok0,
+// Arena row of the first K row of (page of token tok0, head h).  tok0 is below
+// max_blocks*tpp (assign_work clamps n), so the table index stays in the row.
+__device__ __forceinline__ int32_t tile_row(const DecodeParams& p, const int32_t* table, int h, int tok0,
                                             int64_t row_bytes) {
-  const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h0) * 2 * p.tpp;
+  const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
   const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
   return static_cast<int32_t>(base_row + static_cast<int64_t>(table[tok0 / p.tpp]) * page_rows + tok0 % p.tpp);
 }
 
 // ------------------------------------------------------------ grid kernel
-// One CTA per (KV-head group, request, split).
-template <typename T, int D, int G, int HG, int NS>
-__global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
+// One CTA per (KV head, request, split).
+template <typename T, int D, int G, int NS>
+__global__ void __launch_bounds__(kThreads, 3)
     paged_decode_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
   static_assert(D % kBoxCols == 0, "head_dim must be a multiple of 64");
   static_assert(G <= 8, "at most 8 query heads per KV head (N = 8)");
-  static_assert(kConsumerWarps % HG == 0, "heads per CTA must divide the consumer warps");
+  static_assert(NS % kConsumerWarps == 0, "slots must map to fixed consumer warps");
   constexpr int TILE_BYTES = (D / kBoxCols) * kBoxBytes;  // 16 tokens x D x 2 B, one head
-  constexpr int STAGE_BYTES = 2 * HG * TILE_BYTES;
-  constexpr int ROUNDS = kConsumerWarps / HG;            // warps per head
+  constexpr int STAGE_BYTES = 2 * TILE_BYTES;
   constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
   constexpr int RING = NS * STAGE_BYTES;
   constexpr int BAR_OFFSET = RING > MERGE_BYTES ? RING : MERGE_BYTES;
@@ -353,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int b = grid_request(p);
-  const int h0 = blockIdx.x * HG;  // first KV head of this CTA
+  const int h = blockIdx.x;
   const int split = grid_split(p);
   const Work wk = assign_work(p, b, split);
   if (split >= wk.nsplit) return;
@@ -361,14 +333,14 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       jenga_dev::mbar_init(&full[i], 1);
-      jenga_dev::mbar_init(&empty[i], HG);  // every head's warp releases the stage
+      jenga_dev::mbar_init(&empty[i], 1);
     }
     jenga_dev::fence_mbar_init();
   }
   __syncthreads();
   // PDL: the next kernel in the stream may become resident now.  Block
-  // tables / seq_lens come from a non-PDL kernel and are complete; q, the
-  // newest token's K/V (reshape_and_cache) and the reused workspace are only
+  // tables / seq_lens come from a kernel launched without the attribute and
+  // are complete; q, the newest token's K/V and the reused workspace are only
   // touched after pdl_wait().
   jenga_dev::pdl_launch_dependents();
 
@@ -378,40 +350,40 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
     if (lane == 0) {  // producer: one elected lane
       jenga_dev::prefetch_tmap(&tmap);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int v_rows = p.tpp;
-      bool waited = false;
+      // an arena writer that let us start early may still be running: wait
+      // for it before the first load (common.cuh, PDL ordering contract)
+      bool waited = p.early_kv == 0;
+      if (waited) jenga_dev::pdl_wait();
       // the next tile's arena row is read one iteration ahead, so the block-table
       // load is off the empty-slot -> refill path
-      int32_t row = wk.t_count > 0 ? tile_row(p, table, h0, wk.t_begin * kTile, D * 2) : 0;
+      int32_t row = wk.t_count > 0 ? tile_row(p, table, h, wk.t_begin * kTile, D * 2) : 0;
       for (int it = 0; it < wk.t_count; ++it) {
         const int st = it % NS;
         const int tok0 = (wk.t_begin + it) * kTile;
-        const int32_t next = it + 1 < wk.t_count ? tile_row(p, table, h0, tok0 + kTile, D * 2) : 0;
+        const int32_t next = it + 1 < wk.t_count ? tile_row(p, table, h, tok0 + kTile, D * 2) : 0;
         if (it >= NS) jenga_dev::mbar_wait(&empty[st], ((it / NS) & 1) ^ 1);
         if (!waited && tok0 + kTile >= wk.n && p.k_new == nullptr) {  // the tile holding the newest token
           jenga_dev::pdl_wait();  // (fused append patches that row itself: no wait)
           waited = true;
         }
-        load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], row, p.tpp, v_rows, policy, p.kv_box != 0);
+        load_stage<D>(&tmap, smem + st * STAGE_BYTES, &full[st], row, policy);
         row = next;
       }
     }
     return;
   }
 
-  const int hl = warp % HG;      // local head of this warp
-  const int round = warp / HG;   // which of the ROUNDS stage streams
   HeadState<D> hs;
   jenga_dev::pdl_wait();  // q and the workspace belong to the previous kernels until here
-  head_begin<T, D, G>(hs, p, b, h0 + hl, lane);
-  for (int it = round; it < wk.t_count; it += ROUNDS) {
+  head_begin<T, D, G>(hs, p, b, h, lane);
+  for (int it = warp; it < wk.t_count; it += kConsumerWarps) {
     const int st = it % NS;
     jenga_dev::mbar_wait(&full[st], (it / NS) & 1);
     uint8_t* stage = smem + st * STAGE_BYTES;
     const int tok0 = (wk.t_begin + it) * kTile;
     if (p.k_new != nullptr && wk.n - 1 >= tok0 && wk.n - 1 < tok0 + kTile)
-      patch_newest<T, D>(p, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, b, h0 + hl, wk.n - 1 - tok0, lane);
-    head_tile<T, D>(hs, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, tok0, wk.lo, wk.n, p, lane);
+      patch_newest<T, D>(p, stage, stage + TILE_BYTES, b, h, wk.n - 1 - tok0, lane);
+    head_tile<T, D>(hs, stage, stage + TILE_BYTES, tok0, wk.lo, wk.n, p, lane);
     __syncwarp();
     if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
   }
@@ -419,172 +391,7 @@ __global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
   float* s_acc = reinterpret_cast<float*>(smem);  // [4][G][D] (the ring is drained)
   float* s_ml = s_acc + kConsumerWarps * G * D;   // [4][G][2]
   head_store<D, G>(hs, s_acc, s_ml, warp, lane);
-  merge_epilogue<T, G, D, HG>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h0);
-}
-
-// ------------------------------------------------------------ persistent kernel
-// gridDim.x CTAs (a few per SM) pull work items (request, head group, split)
-// from a global atomic queue.  The producer keeps streaming tiles across item
-// boundaries, so the TMA ring never drains between items and there is no
-// wave-quantisation tail; the consumers merge each item while the next one's
-// tiles are already landing.  Items are enumerated request by request from a
-// per-CTA prefix over the requests' split counts (needs batch <= kMaxPersistB).
-constexpr int kMaxPersistB = 2048;
-constexpr int kItemSlots = 4;
-
-struct ItemDesc {
-  int b, h0, split, n, lo, nsplit, t_begin, t_count, seq0, stop;
-};
-
-template <typename T, int D, int G, int HG, int NS>
-__global__ void __launch_bounds__(kThreads, HG >= 4 ? 1 : (HG == 2 ? 2 : 3))
-    paged_decode_tc_persistent(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
-  constexpr int TILE_BYTES = (D / kBoxCols) * kBoxBytes;
-  constexpr int STAGE_BYTES = 2 * HG * TILE_BYTES;
-  constexpr int ROUNDS = kConsumerWarps / HG;
-  constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
-  constexpr int RING = NS * STAGE_BYTES;
-  static_assert(NS % ROUNDS == 0, "slots must map to fixed consumer warps");
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
-  float* s_acc = reinterpret_cast<float*>(smem + RING);     // separate from the ring:
-  float* s_ml = s_acc + kConsumerWarps * G * D;             // the producer keeps filling it
-  ItemDesc* items = reinterpret_cast<ItemDesc*>(smem + RING + MERGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(items + kItemSlots);
-  uint64_t* empty = full + NS;
-  uint64_t* item_full = empty + NS;
-  uint64_t* item_empty = item_full + kItemSlots;
-  int* s_flag = reinterpret_cast<int*>(item_empty + kItemSlots);
-  int* s_prefix = s_flag + 4;  // [batch + 1] item prefix over requests
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int groups = p.hkv / HG;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) {
-      jenga_dev::mbar_init(&full[i], 1);
-      jenga_dev::mbar_init(&empty[i], HG);
-    }
-    for (int i = 0; i < kItemSlots; ++i) {
-      jenga_dev::mbar_init(&item_full[i], 1);
-      jenga_dev::mbar_init(&item_empty[i], kConsumerWarps);
-    }
-    jenga_dev::fence_mbar_init();
-  }
-  if (warp == 0) {  // items per request -> exclusive prefix (one warp scan)
-    const int per = (p.batch + 31) / 32;
-    int local = 0;
-    for (int i = 0; i < per; ++i) {
-      const int bb = lane * per + i;
-      if (bb < p.batch) local += assign_work(p, bb, 0).nsplit * groups;
-    }
-    int incl = local;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += v;
-    }
-    int run = incl - local;
-    for (int i = 0; i < per; ++i) {
-      const int bb = lane * per + i;
-      if (bb < p.batch) {
-        s_prefix[bb] = run;
-        run += assign_work(p, bb, 0).nsplit * groups;
-      }
-    }
-    if (lane == 31) s_prefix[p.batch] = incl;
-  }
-  __syncthreads();
-  const int total = s_prefix[p.batch];
-
-  if (warp == kConsumerWarps) {
-    if (lane == 0) {  // producer: fetch items, stream their tiles
-      jenga_dev::prefetch_tmap(&tmap);
-      const uint64_t policy = jenga_dev::l2_policy_evict_first();
-      const int v_rows = p.tpp;
-      int seq = 0;
-      for (int ic = 0;; ++ic) {
-        const int j = ic % kItemSlots;
-        if (ic >= kItemSlots) jenga_dev::mbar_wait(&item_empty[j], ((ic / kItemSlots) & 1) ^ 1);
-        const int item = atomicAdd(&p.work[0], 1);
-        ItemDesc d{};
-        if (item >= total) {
-          d.stop = 1;
-          items[j] = d;
-          jenga_dev::mbar_arrive(&item_full[j]);
-          break;
-        }
-        int lo_b = 0, hi_b = p.batch - 1;  // last request with prefix <= item
-        while (lo_b < hi_b) {
-          const int mid = (lo_b + hi_b + 1) >> 1;
-          if (s_prefix[mid] <= item) lo_b = mid;
-          else hi_b = mid - 1;
-        }
-        const int r = item - s_prefix[lo_b];
-        d.b = lo_b;
-        d.split = r / groups;
-        d.h0 = (r % groups) * HG;
-        const Work wk = assign_work(p, d.b, d.split);
-        d.n = wk.n;
-        d.lo = wk.lo;
-        d.nsplit = wk.nsplit;
-        d.t_begin = wk.t_begin;
-        d.t_count = wk.t_count;
-        d.seq0 = seq;
-        items[j] = d;
-        jenga_dev::mbar_arrive(&item_full[j]);  // release: the descriptor is visible to its waiters
-        const int32_t* table = p.table + static_cast<int64_t>(d.b) * p.max_blocks;
-        for (int it = 0; it < d.t_count; ++it, ++seq) {
-          const int st = seq % NS;
-          if (seq >= NS) jenga_dev::mbar_wait(&empty[st], ((seq / NS) & 1) ^ 1);
-          const int tok0 = (d.t_begin + it) * kTile;
-          load_stage<D, HG>(&tmap, smem + st * STAGE_BYTES, &full[st], tile_row(p, table, d.h0, tok0, D * 2), p.tpp,
-                            v_rows, policy, p.kv_box != 0);
-        }
-      }
-    }
-  } else {
-    const int hl = warp % HG;
-    const int round = warp / HG;
-    HeadState<D> hs;
-    for (int ic = 0;; ++ic) {
-      const int j = ic % kItemSlots;
-      jenga_dev::mbar_wait(&item_full[j], (ic / kItemSlots) & 1);
-      const ItemDesc d = items[j];
-      __syncwarp();
-      if (lane == 0) jenga_dev::mbar_arrive(&item_empty[j]);
-      if (d.stop) break;
-      head_begin<T, D, G>(hs, p, d.b, d.h0 + hl, lane);
-      // this warp owns the global tiles seq with seq % ROUNDS == round (NS % ROUNDS == 0,
-      // so every use of a slot is consumed by the same warps)
-      int it = (round - d.seq0 % ROUNDS + ROUNDS) % ROUNDS;
-      for (; it < d.t_count; it += ROUNDS) {
-        const int seq = d.seq0 + it;
-        const int st = seq % NS;
-        jenga_dev::mbar_wait(&full[st], (seq / NS) & 1);
-        uint8_t* stage = smem + st * STAGE_BYTES;
-        head_tile<T, D>(hs, stage + hl * TILE_BYTES, stage + (HG + hl) * TILE_BYTES, (d.t_begin + it) * kTile, d.lo,
-                        d.n, p, lane);
-        __syncwarp();
-        if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
-      }
-      consumers_sync();  // the previous item's merge has finished reading s_acc
-      head_store<D, G>(hs, s_acc, s_ml, warp, lane);
-      merge_epilogue<T, G, D, HG>(p, s_acc, s_ml, s_flag, d.nsplit, d.split, d.b, d.h0);
-    }
-  }
-  // the last CTA out re-arms the queue for the next launch / graph replay
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&p.work[1], 1) == static_cast<int>(gridDim.x) - 1) {
-      p.work[0] = 0;
-      p.work[1] = 0;
-      __threadfence();
-    }
-  }
+  merge_epilogue<T, G, D>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h);
 }
 
 // ------------------------------------------------------------ host side
@@ -601,19 +408,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Views of the arena, encoded once per (arena, D, dtype, tpp, kind):
-//  * 2-D [rows][D] with 64 x 16 boxes (several heads per CTA);
-//  * 4-D {64 cols, rows, D/64 chunks at 128 B, K|V at tpp rows} with one box =
-//    a whole head's K and V tile of a page (one head per CTA): 1 TMA op per 16 KiB
-//    instead of 2*D/64 (measured on the prefill producer: TMA op count, not bytes,
-//    bounded delivery).
-int tensor_map(const void* base, int D, int dtype, int tpp, bool kv_box, CUtensorMap* out) {
+// The arena as a 4-D tensor {64 cols, rows, D/64 chunks at 128 B, K|V at tpp
+// rows}: one box = a whole head's K and V tile of a page, 1 TMA op per
+// 2*16*D*e bytes (op count, not bytes, bounded delivery in the prefill
+// producer; the 2-D 64 x 16 box variant measured 1% / 4.5% slower on the
+// Gemma / Llama-vision decode steps).  Encoded once per (arena, D, dtype, tpp).
+int tensor_map(const void* base, int D, int dtype, int tpp, CUtensorMap* out) {
   static std::mutex mu;
-  static std::map<std::tuple<uintptr_t, uint64_t, int, int, int, bool>, CUtensorMap> cache;
+  static std::map<std::tuple<uintptr_t, uint64_t, int, int, int>, CUtensorMap> cache;
   uint64_t bytes = 0;
   if (!jenga_dev::arena_extent(base, &bytes)) return JENGA_ERR_UNSUPPORTED;  // not a jenga arena
   // keyed by the extent too: a new arena may reuse a freed arena's address
-  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), bytes, D, dtype, kv_box ? tpp : 0, kv_box);
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(base), bytes, D, dtype, tpp);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -626,24 +432,15 @@ int tensor_map(const void* base, int D, int dtype, int tpp, bool kv_box, CUtenso
   const CUtensorMapDataType dt =
       dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap m;
-  CUresult r;
-  if (kv_box) {
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(kBoxCols), bytes / row_bytes, static_cast<cuuint64_t>(D / kBoxCols),
-                          2};
-    cuuint64_t strides[3] = {row_bytes, 128, static_cast<cuuint64_t>(tpp) * row_bytes};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile),
-                         static_cast<cuuint32_t>(D / kBoxCols), 2};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    r = fn(&m, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  } else {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), bytes / row_bytes};
-    cuuint64_t strides[1] = {row_bytes};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile)};
-    cuuint32_t estr[2] = {1, 1};
-    r = fn(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  }
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(kBoxCols), bytes / row_bytes, static_cast<cuuint64_t>(D / kBoxCols),
+                        2};
+  cuuint64_t strides[3] = {row_bytes, 128, static_cast<cuuint64_t>(tpp) * row_bytes};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(kBoxCols), static_cast<cuuint32_t>(kTile),
+                       static_cast<cuuint32_t>(D / kBoxCols), 2};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = fn(&m, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return jenga_dev::set_error(JENGA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   cache[key] = m;
@@ -651,101 +448,38 @@ int tensor_map(const void* base, int D, int dtype, int tpp, bool kv_box, CUtenso
   return JENGA_OK;
 }
 
-// Persistent scheduling only with JENGA_DECODE_PERSISTENT=1: measured slower
-// than three grid CTAs per SM on the bench shapes (profiles/r01_sweeps.md).
-bool use_persistent(int batch) {
-  static const int v = [] {
-    const char* e = std::getenv("JENGA_DECODE_PERSISTENT");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v != 0 && batch <= kMaxPersistB;
-}
-
-template <typename T, int D, int G, int HG>
+template <typename T, int D, int G>
 int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaStream_t stream) {
-  constexpr int STAGE = 2 * HG * kTile * D * 2;
+  constexpr int STAGE = 2 * kTile * D * 2;
   constexpr int MERGE = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
-  constexpr int CTAS_PER_SM = HG >= 4 ? 1 : (HG == 2 ? 2 : 3);
-  if (use_persistent(batch) && prm.k_new == nullptr) {
-    // ring budget net of the separate merge area, a multiple of the rounds
-    constexpr int ROUNDS = kConsumerWarps / HG;
-    constexpr int BUDGET = ring_budget<HG>() - MERGE;
-    constexpr int NSR = (BUDGET / STAGE) / ROUNDS * ROUNDS;
-    constexpr int NS = NSR < ROUNDS ? ROUNDS : (NSR > 12 ? 12 : NSR);
-    const int smem = NS * STAGE + MERGE + kItemSlots * static_cast<int>(sizeof(ItemDesc)) +
-                     (2 * NS + 2 * kItemSlots) * 8 + 16 + (batch + 1) * 4 + 1024;
-    auto kern = paged_decode_tc_persistent<T, D, G, HG, NS>;
-    static std::atomic<uint64_t> configured{0};
-    if (int rc = configure_smem(kern, smem, configured)) return rc;
-    int per_sm = 0;  // resident CTAs per SM at this shared-memory size
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
-    kern<<<jenga_dev::num_sms() * std::min(per_sm, CTAS_PER_SM), kThreads, smem, stream>>>(prm, tmap);
-    return jenga_dev::check_launch("paged_decode_tc_persistent");
-  }
-  constexpr int NS = stages<D, HG>();
+  constexpr int NS = stages<D>();
   const int smem = std::max(NS * STAGE, MERGE) + 2 * NS * 8 + 16 + 1024;
-  auto kern = paged_decode_tc_kernel<T, D, G, HG, NS>;
+  auto kern = paged_decode_tc_kernel<T, D, G, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  const dim3 grid = decode_grid(prm, batch, HG);
-  jenga_dev::launch_maybe_pdl(kern, grid, dim3(kThreads), smem, stream, prm, tmap);
+  jenga_dev::launch_maybe_pdl(kern, decode_grid(prm, batch), dim3(kThreads), smem, stream, prm, tmap);
   return jenga_dev::check_launch("paged_decode_tc_kernel");
 }
 
-template <typename T, int D, int G>
-int dispatch_hg(int hg, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
-  switch (hg) {
-    case 1: return launch_tc<T, D, G, 1>(prm, m, batch, s);
-    case 2: return launch_tc<T, D, G, 2>(prm, m, batch, s);
-    case 4: return launch_tc<T, D, G, 4>(prm, m, batch, s);
-  }
-  return JENGA_ERR_UNSUPPORTED;
-}
-
 template <typename T, int D>
-int dispatch_g(int G, int hg, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+int dispatch_g(int G, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
   switch (G) {
-    case 1: return dispatch_hg<T, D, 1>(hg, prm, m, batch, s);
-    case 2: return dispatch_hg<T, D, 2>(hg, prm, m, batch, s);
-    case 4: return dispatch_hg<T, D, 4>(hg, prm, m, batch, s);
-    case 8: return dispatch_hg<T, D, 8>(hg, prm, m, batch, s);
+    case 1: return launch_tc<T, D, 1>(prm, m, batch, s);
+    case 2: return launch_tc<T, D, 2>(prm, m, batch, s);
+    case 4: return launch_tc<T, D, 4>(prm, m, batch, s);
+    case 8: return launch_tc<T, D, 8>(prm, m, batch, s);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
 
 template <typename T>
-int dispatch_d(int D, int G, int hg, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
+int dispatch_d(int D, int G, const DecodeParams& prm, const CUtensorMap& m, int batch, cudaStream_t s) {
   switch (D) {
-    case 64: return dispatch_g<T, 64>(G, hg, prm, m, batch, s);
-    case 128: return dispatch_g<T, 128>(G, hg, prm, m, batch, s);
-    case 256: return dispatch_g<T, 256>(G, hg, prm, m, batch, s);
+    case 64: return dispatch_g<T, 64>(G, prm, m, batch, s);
+    case 128: return dispatch_g<T, 128>(G, prm, m, batch, s);
+    case 256: return dispatch_g<T, 256>(G, prm, m, batch, s);
   }
   return JENGA_ERR_UNSUPPORTED;
-}
-
-// One 4-D box per (page, head) K+V tile (default); JENGA_DECODE_KV_BOX=0 selects
-// the 2-D boxes for A/B runs.
-bool use_kv_box() {
-  static const bool v = [] {
-    const char* e = std::getenv("JENGA_DECODE_KV_BOX");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  return v;
-}
-
-// KV heads per CTA: 1 by default — three 1-head CTAs per SM overlap each
-// other's prologue/epilogue and measured fastest on the Gemma shard
-// (profiles/r01_sweeps.md); JENGA_DECODE_HEADS_PER_CTA=2|4 selects the
-// multi-head variants.
-int heads_per_cta(int hkv) {
-  static const int forced = [] {
-    const char* e = std::getenv("JENGA_DECODE_HEADS_PER_CTA");
-    return e ? std::atoi(e) : 0;
-  }();
-  for (int hg : {forced, 1})
-    if ((hg == 1 || hg == 2 || hg == 4) && hkv % hg == 0) return hg;
-  return 1;
 }
 
 }  // namespace
@@ -755,14 +489,11 @@ namespace jenga_decode {
 int launch_decode_tc(const DecodeParams& prm, int dtype, int head_dim, int G, int batch, cudaStream_t stream) {
   if (prm.tpp % kTile != 0 || head_dim % kBoxCols != 0 || G > 8) return JENGA_ERR_UNSUPPORTED;
   if (prm.start_offset % (head_dim * 2) || prm.page_stride % (head_dim * 2)) return JENGA_ERR_UNSUPPORTED;
-  const int hg = heads_per_cta(prm.hkv);
   CUtensorMap m;
-  DecodeParams p2 = prm;
-  p2.kv_box = hg == 1 && use_kv_box();
-  const int rc = tensor_map(prm.arena, head_dim, dtype, prm.tpp, p2.kv_box != 0, &m);
+  const int rc = tensor_map(prm.arena, head_dim, dtype, prm.tpp, &m);
   if (rc != JENGA_OK) return rc;
-  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, hg, p2, m, batch, stream);
-  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, hg, p2, m, batch, stream);
+  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, m, batch, stream);
+  if (dtype == JENGA_F16) return dispatch_d<__half>(head_dim, G, prm, m, batch, stream);
   return JENGA_ERR_UNSUPPORTED;
 }
 

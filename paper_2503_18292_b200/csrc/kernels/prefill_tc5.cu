@@ -1322,74 +1322,79 @@ int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int 
   return JENGA_ERR_UNSUPPORTED;
 }
 
-// 64-token K/V tiles; ring depth sized to ~192 KB of shared memory (96 KB for
-// head_dim 64, so two CTAs share an SM: 256 TMEM columns each).
+// Kernel per head_dim: CTA pairs (cta_group::2, M = 256) at 256 — each SM streams
+// half of every K/V tile; ping-ponged CTA pairs at 128 (two query tiles per CTA,
+// TMEM: 2 x (O 128 + Q 64 + S 64)); one CTA per query block at 64, whose single
+// 64-column chunk is too narrow to split V across a pair.  64-token K/V tiles.
 template <typename T>
 int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
-  // CTA pairs (cta_group::2) halve the K/V bytes each SM streams; head_dim 64
-  // has a single 64-column chunk, too few to split V between the pair.
-  static const bool pair = [] {
-    const char* e = std::getenv("JENGA_PREFILL_2SM");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  if (pair && D == 256) return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
-  static const bool pair128 = [] {
-    const char* e = std::getenv("JENGA_PREFILL_2SM_D128");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  static const bool pp = [] {
-    const char* e = std::getenv("JENGA_PREFILL_PP");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  // head_dim 128: two query tiles per CTA, ping-ponged (TMEM: 2 x (O 128 + Q 64 + S 64))
-  if (pair && pair128 && pp && D == 128) return dispatch_pp<T, 128, 8>(G, prm, dtype, s, batch);
-  if (pair && pair128 && D == 128) return dispatch_pair<T, 128, 8>(G, prm, dtype, s, batch);
   switch (D) {
+    case 256: return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
+    case 128: return dispatch_pp<T, 128, 8>(G, prm, dtype, s, batch);
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
-    case 128: return dispatch_g<T, 128, 6>(G, prm, dtype, s, batch);
-    case 256: return dispatch_g<T, 256, 3>(G, prm, dtype, s, batch);
   }
-  return JENGA_ERR_UNSUPPORTED;
+  return jenga_dev::set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: head_dim must be 64, 128 or 256");
 }
 
 }  // namespace
 
-namespace jenga_decode {
-
-// Prefill on tcgen05; JENGA_ERR_UNSUPPORTED lets the caller use prefill.cu.
-int launch_prefill_tc5(const void* arena, uint64_t start_offset, uint64_t page_stride, void* out, const int32_t* cu_q,
-                       const int32_t* table, const int32_t* seq_lens, int kind, int64_t window, int max_blocks,
-                       int hq, int hkv, int tpp, int q_blocks_128, float qscale, float cap_log2, float inv_cap,
-                       int dtype, int head_dim, int batch, int total_tokens, const void* q, cudaStream_t s) {
-  static const bool enabled = [] {
-    const char* e = std::getenv("JENGA_PREFILL_TC5");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  if (!enabled || (head_dim != 64 && head_dim != 128 && head_dim != 256)) return JENGA_ERR_UNSUPPORTED;
+// Chunked-prefill paged attention (the reference's
+// prefill_some stores a chunk of positions per step, simulator.cpp:504-547).
+// Request b contributes C_b query tokens — its newest ordinals, 0-based
+// positions n_b - C_b .. n_b - 1 — whose K/V were already scattered into the
+// arena by reshape_and_cache.  Query position i attends key j iff j <= i
+// (causal), additionally j + W > i for sliding windows (needs_token at length
+// i + 1, layer_policies.cpp:105-120); cross attention attends all n_b image keys.
+JENGA_EXPORT int jenga_paged_prefill(void* arena_base, jenga_layer_view view, int kind, int dtype, uint64_t window,
+                                     const void* q, void* out, const int32_t* cu_q, int total_tokens,
+                                     int max_chunk, const int32_t* block_table, const int32_t* seq_lens, int batch,
+                                     int max_blocks, int num_q_heads, int num_kv_heads, int head_dim,
+                                     uint32_t tokens_per_page, float scale, float softcap, void* stream) {
+  using namespace jenga_dev;
+  if (batch < 0 || num_kv_heads <= 0 || num_q_heads <= 0 || num_q_heads % num_kv_heads != 0 ||
+      tokens_per_page == 0 || max_blocks <= 0 || total_tokens < 0 || max_chunk < 0 || !arena_base || !q || !out ||
+      !cu_q || !block_table || !seq_lens)
+    return set_error(JENGA_ERR_ARG, "jenga_paged_prefill: invalid arguments");
+  if (kind != JENGA_KIND_FULL && kind != JENGA_KIND_SLIDING_WINDOW && kind != JENGA_KIND_CROSS_ATTENTION)
+    return set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: kind must be full, sliding_window or cross");
+  if (kind == JENGA_KIND_SLIDING_WINDOW && window == 0)
+    return set_error(JENGA_ERR_CONFIG, "jenga_paged_prefill: sliding window needs window >= 1");
+  if (dtype != JENGA_BF16 && dtype != JENGA_F16)
+    return set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: bf16 / fp16 KV only (tensor-core path)");
+  if (view.exec_page_size != 2ull * num_kv_heads * tokens_per_page * head_dim * 2)
+    return set_error(JENGA_ERR_CONFIG, "jenga_paged_prefill: exec_page_size != 2*Hkv*tpp*D*dtype");
+  if (tokens_per_page % kTile != 0 || view.start_offset % (head_dim * 2) || view.page_stride % (head_dim * 2))
+    return set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: tokens_per_page must be a multiple of 16");
+  const int G = num_q_heads / num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: query heads per kv head must be 1, 2, 4 or 8");
+  if (batch == 0 || total_tokens == 0) return JENGA_OK;
   Prefill5Params prm{};
-  prm.arena = static_cast<const uint8_t*>(arena);
-  prm.start_offset = start_offset;
-  prm.page_stride = page_stride;
+  prm.arena = static_cast<const uint8_t*>(arena_base);
+  prm.start_offset = view.start_offset;
+  prm.page_stride = view.page_stride;
   prm.out = out;
   prm.cu_q = cu_q;
-  prm.table = table;
+  prm.table = block_table;
   prm.seq_lens = seq_lens;
   prm.kind = kind;
-  prm.window = window;
+  prm.window = static_cast<int64_t>(window);
   prm.max_blocks = max_blocks;
-  prm.hq = hq;
-  prm.hkv = hkv;
-  prm.tpp = tpp;
-  prm.q_blocks = q_blocks_128;
-
-  prm.qscale = qscale;
-  prm.cap_log2 = cap_log2;
-  prm.inv_cap = inv_cap;
-  const int G = hq / hkv;
+  prm.hq = num_q_heads;
+  prm.hkv = num_kv_heads;
+  prm.tpp = static_cast<int>(tokens_per_page);
+  prm.q_blocks = (max_chunk + kRows / G - 1) / (kRows / G);  // 128 (token, query head) rows per block
+  if (softcap > 0.f) {
+    prm.qscale = scale;
+    prm.cap_log2 = softcap * kLog2e;
+    prm.inv_cap = 1.f / softcap;
+  } else {
+    prm.qscale = scale * kLog2e;
+  }
   prm.q = q;
-  (void)total_tokens;
-  if (dtype == JENGA_BF16) return dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, s, batch);
-  return dispatch_d<__half>(head_dim, G, prm, dtype, s, batch);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int rc = dtype == JENGA_BF16 ? dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, s, batch)
+                                     : dispatch_d<__half>(head_dim, G, prm, dtype, s, batch);
+  if (rc == JENGA_OK) note_launch(s, kLaunchSerializing);
+  return rc;
 }
-
-}  // namespace jenga_decode

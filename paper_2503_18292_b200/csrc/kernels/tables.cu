@@ -83,6 +83,7 @@ JENGA_EXPORT int jenga_build_block_tables(const int32_t* offsets, const jenga_sm
   build_tables_kernel<<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(
       offsets, pages, first_live_block, n_stored, batch, slots_per_large, tokens_per_page, max_blocks,
       block_table, slot_mapping, seq_lens);
+  note_launch(static_cast<cudaStream_t>(stream), kLaunchSerializing);
   return check_launch("build_tables_kernel");
 }
 
@@ -95,5 +96,6 @@ JENGA_EXPORT int jenga_slot_mapping(const int32_t* block_table, int max_blocks, 
   if (n_tokens == 0) return JENGA_OK;
   slot_mapping_kernel<<<(n_tokens + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       block_table, max_blocks, req, ord, n_tokens, tokens_per_page, slot_mapping);
+  note_launch(static_cast<cudaStream_t>(stream), kLaunchSerializing);
   return check_launch("slot_mapping_kernel");
 }

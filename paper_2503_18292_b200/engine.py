@@ -145,14 +145,14 @@ class DecodeEngine:
         totals = {}
         for g in (range(len(self.tables)) if groups is None else groups):
             t = self.tables[g]
+            # the C side validates widths and capacity before writing the pinned buffer
             check(lib.jenga_pages_pack_csr(
-                self.pages.h, g, rp, n, C.cast(t.h_offsets.data_ptr(), C.POINTER(C.c_int32)),
+                self.pages.h, g, rp, n, t.max_blocks, t.h_pages.shape[0],
+                C.cast(t.h_offsets.data_ptr(), C.POINTER(C.c_int32)),
                 C.cast(t.h_pages.data_ptr(), C.POINTER(_lib.SmallPage)),
                 C.cast(t.h_first_live.data_ptr(), C.POINTER(C.c_int32)),
                 C.cast(t.h_n_stored.data_ptr(), C.POINTER(C.c_int32))))
             total = int(t.h_offsets[n])
-            if total > t.h_pages.shape[0]:
-                raise OverflowError("page lists exceed the table capacity (raise max_tokens)")
             totals[g] = total
         return totals
 

@@ -74,9 +74,10 @@ def toy(tokens_per_page: int = 16) -> ModelGeometry:
     ])
 
 
-def gemma2_9b(tokens_per_page: int = 16, softcap: float = 0.0) -> ModelGeometry:
+def gemma2_9b(tokens_per_page: int = 16, softcap: float = 50.0) -> ModelGeometry:
     """configs[1]: Gemma-2-9B — 42 layers alternating full / SWA-4096,
-    Hq=16, Hkv=8, D=256, bf16."""
+    Hq=16, Hkv=8, D=256, bf16, attention-logit soft-capping at 50 (the
+    model's attn_logit_softcapping)."""
     bf = torch.bfloat16
     return ModelGeometry("gemma2-9b", [
         GroupGeometry("full", LayerKind.kFullAttention, 21, 8, 16, 256, bf, tokens_per_page),

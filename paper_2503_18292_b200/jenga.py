@@ -525,19 +525,21 @@ class PageLists:
         check(lib.jenga_pages_blocks(self.h, request, g, pages, live, cap, C.byref(n)))
         return [(SmallPageId(pages[i].large, pages[i].slot), bool(live[i])) for i in range(cap)]
 
-    def pack_csr(self, g: int, requests: Sequence[int]):
-        """CSR page lists (numpy) for jenga_build_block_tables."""
+    def pack_csr(self, g: int, requests: Sequence[int], max_blocks: int = 0):
+        """CSR page lists (numpy) for jenga_build_block_tables; max_blocks > 0
+        rejects a request longer than that block-table width."""
         req = np.ascontiguousarray(np.asarray(requests, dtype=np.uint64))
         nreq = len(req)
         offsets = np.zeros(nreq + 1, dtype=np.int32)
         rp = req.ctypes.data_as(C.POINTER(C.c_uint64))
-        check(lib.jenga_pages_pack_csr(self.h, g, rp, nreq, offsets.ctypes.data_as(C.POINTER(C.c_int32)),
-                                       None, None, None))
+        check(lib.jenga_pages_pack_csr(self.h, g, rp, nreq, max_blocks, 0,
+                                       offsets.ctypes.data_as(C.POINTER(C.c_int32)), None, None, None))
         total = int(offsets[-1])
         pages = np.zeros((max(1, total), 2), dtype=np.uint32)
         first_live = np.zeros(nreq, dtype=np.int32)
         n_stored = np.zeros(nreq, dtype=np.int32)
-        check(lib.jenga_pages_pack_csr(self.h, g, rp, nreq, offsets.ctypes.data_as(C.POINTER(C.c_int32)),
+        check(lib.jenga_pages_pack_csr(self.h, g, rp, nreq, max_blocks, pages.shape[0],
+                                       offsets.ctypes.data_as(C.POINTER(C.c_int32)),
                                        pages.ctypes.data_as(C.POINTER(_lib.SmallPage)),
                                        first_live.ctypes.data_as(C.POINTER(C.c_int32)),
                                        n_stored.ctypes.data_as(C.POINTER(C.c_int32))))

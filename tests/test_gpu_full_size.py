@@ -105,7 +105,7 @@ def test_gemma_shard_full_size(orc):
             rows = t.block_table[:B].cpu().numpy()[sample]
             host, ctable, cview = _compact(eng, g, layer, rows)
             want = orc.paged_decode(host, cview, int(gg.kind), BF16, gg.window, q[sample].view(torch.int16).cpu().numpy(),
-                                    ctable, seq[sample], 16, 8, 256, tpp, 256 ** -0.5, 0.0, nthreads=8)
+                                    ctable, seq[sample], 16, 8, 256, tpp, 256 ** -0.5, eng.geom.softcap, nthreads=8)
             got = out[sample].float().cpu().numpy()
             tol = TOL[torch.bfloat16]
             err = rel_err(got, want)
@@ -129,7 +129,7 @@ def _sampled_decode_check(orc, eng, g, layer, q, sample, tol):
     host, ctable, cview = _compact(eng, g, layer, rows)
     want = orc.paged_decode(host, cview, int(gg.kind), BF16, gg.window, q[sample].view(torch.int16).cpu().numpy(),
                             ctable, seq, gg.num_q_heads, gg.num_kv_heads, gg.head_dim,
-                            eng.spec.groups[g].tokens_per_page, gg.head_dim ** -0.5, 0.0, nthreads=8)
+                            eng.spec.groups[g].tokens_per_page, gg.head_dim ** -0.5, eng.geom.softcap, nthreads=8)
     err = rel_err(out[sample].float().cpu().numpy(), want)
     print(f"[full-size] group {g} layer {layer}: seq {seq.tolist()} relative error {err:.3g}")
     assert err <= tol, f"group {g} layer {layer}: relative error {err:.3g} > {tol}"

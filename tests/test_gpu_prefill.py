@@ -87,15 +87,3 @@ def test_prefill_cross_attention(orc):
     fill_group_kv(eng, 1, [0], seed=1)
     run_prefill(orc, eng, 1, 0, [33, 70])  # text-token queries over all image keys
 
-
-
-def test_single_cta_kernel_all_head_dims():
-    """The single-CTA tcgen05 kernel (default for head_dim 64) on every head_dim:
-    the bf16 shape sweep again in a process with CTA pairs disabled."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, JENGA_PREFILL_2SM="0")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
-                        "test_prefill_shapes and bf16"], env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
