@@ -10,9 +10,12 @@ reads every live K/V byte through the layer view of the HBM arena.
 
 The headline 256 x 8k batch holds 541 GB of KV and does not fit one GPU, so
 each GPU owns a 32-request shard (67.6 GB, the G=8 shard of the headline
-batch); `--gpus N` shards N x 32 requests with no inter-GPU traffic on the
-hot path ("scaling": "weak"); NCCL only gathers outputs for verification
-after the timed region.
+batch).  `--gpus N` runs N ranks, one process per GPU — started here through
+torch.distributed.run (127.0.0.1) unless a launcher already set WORLD_SIZE —
+each owning N x 32 / N requests, its own allocator and arena, with no
+inter-GPU traffic on the hot path ("scaling": "weak").  After the timed
+region NCCL gathers sampled requests' outputs and layer slices to rank 0,
+which checks them against the C oracle ("verified").
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -220,7 +223,7 @@ def run_ours(a, rank, world, local_rank):
     # every host append of the run: warm-up + timed steps, the per-launch event pass
     # (k_steps below), graph warm-up / capture steps, and the e2e leg (pipelined one
     # step ahead) — the tables and the arena are sized for all of them
-    total_steps = (a.warmup + a.steps + max(2, a.steps // 4) + 8 +
+    total_steps = (a.warmup + a.steps + max(3, a.steps // 4) + 8 +
                    (0 if a.no_e2e else a.warmup + a.steps + 4))
     eng = DecodeEngine(wl.geom, wl.arena_large_pages(total_steps), B, wl.max_tokens(total_steps), dev,
                        group_max_tokens=wl.group_max_tokens(total_steps))
@@ -264,13 +267,16 @@ def run_ours(a, rank, world, local_rank):
         eng.append()
         return eng.pack_tables()
 
-    def device_step(totals=None, ev=None, hooks=None):
-        """Device half: table upload/build, then per layer KV write + decode
-        (fixed shape when totals is None, so it can be graph-captured)."""
+    def device_step(totals=None, ev=None, hooks=None, attention=True):
+        """Device half: table upload, then per layer KV write + decode (fixed
+        shape, so it can be graph-captured).  attention=False: everything but
+        the attention launches (the roofline's subtrahend)."""
         eng.upload_tables(None, totals)
         pg = {}
         for i, (g, l) in enumerate(wl.layers):
             kind = eng.tables[g].geom.kind
+            if kind != LayerKind.kMamba and not attention:
+                continue
             if kind == LayerKind.kMamba:
                 if g not in pg:
                     pg[g] = eng.mamba_page_globals(g)
@@ -353,18 +359,39 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
     launches = ops.kernel_launch_count() - launches0 + (a.steps * per_replay if graph is not None else 0)
     ms = start.elapsed_time(end)
-    # per-launch decode durations: a short pass right after, with events
-    # bracketing every paged-decode launch on its stream
-    k_steps = max(2, a.steps // 4)
+    ms_local = ms
+    # Attention launches' own time inside the PDL-chained graph: the same step
+    # without them (table upload + Mamba copies) is captured and timed alone,
+    # decode time = step time - that.  (Events between launches would break
+    # the PDL overlap the timed step runs with.)
+    k_steps = max(3, a.steps // 4)
+    rest_graph = None
+    if graph is not None:
+        rest_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(rest_graph):
+            device_step(attention=False)
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    r0.record(stream)
+    for _ in range(k_steps):
+        if rest_graph is not None:
+            rest_graph.replay()
+        else:
+            device_step(attention=False)
+    r1.record(stream)
+    torch.cuda.synchronize()
+    rest_ms = r0.elapsed_time(r1) / k_steps
+    # secondary evidence: CUDA events around every attention launch of a few
+    # eager steps (no graph, no PDL overlap across the events)
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in attn]
            for _ in range(k_steps)]
     kv_prof = 0
-    for s in range(k_steps):
-        step(evs[s])
+    for s_ in range(k_steps):
+        step(evs[s_])
         kv_prof += step_bytes()[0]
     torch.cuda.synchronize()
     clocks = clk.stop()
-    dec_ms = sum(e0.elapsed_time(e1) for st in evs for e0, e1 in st)
+    ev_ms = sum(e0.elapsed_time(e1) for st in evs for e0, e1 in st)
     kv_local = kv_bytes
     moved = kv_bytes + st_bytes
     if world > 1:
@@ -372,7 +399,9 @@ def run_ours(a, rank, world, local_rank):
         moved = int(sum_over_ranks(moved, dev))        # whole-job bytes
     ms_per_step = ms / a.steps
     qo_step = 2 * na * B * H * D * 2                   # q read + out write of one step's decode launches
-    dec_gbs = (kv_prof + qo_step * k_steps) / (dec_ms * 1e-3) / 1e9
+    dec_ms_step = ms_local / a.steps - rest_ms         # attention launches per step, in the graph
+    dec_gbs = (kv_local / a.steps + qo_step) / (dec_ms_step * 1e-3) / 1e9
+    ev_gbs = (kv_prof + qo_step * k_steps) / (ev_ms * 1e-3) / 1e9
     qo = qo_step * a.steps
 
     # ---------------- e2e: host buffers through the public API each step
@@ -434,7 +463,7 @@ def run_ours(a, rank, world, local_rank):
             e2e_graph.replay()
             torch.cuda.synchronize()
 
-        pending = {"totals": None}
+        pending = {"totals": None, "pl_bytes": 0}
 
         def e2e_step():
             """Launch this step (its tables were packed during the previous
@@ -443,6 +472,7 @@ def run_ours(a, rank, world, local_rank):
             if pending["totals"] is None:
                 pending["totals"] = host_step()
             nbytes = sum(step_bytes())
+            pending["pl_bytes"] += eng.upload_bytes(pending["totals"])  # page lists the device reads this step
             if e2e_graph is None:
                 e2e_device(pending["totals"])
             else:
@@ -456,6 +486,7 @@ def run_ours(a, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
         e_bytes = 0
+        pending["pl_bytes"] = 0
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
@@ -468,23 +499,27 @@ def run_ours(a, rank, world, local_rank):
             e_ms = max_over_ranks(e_ms, dev)
             e_bytes = int(sum_over_ranks(e_bytes, dev))
         e2e = {"value": round(e_bytes / (e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
-               "h2d_bytes_per_step": int(q.nbytes + kn.nbytes + vn.nbytes), "d2h_bytes_per_step": int(out.nbytes),
+               "h2d_bytes_per_step": int(q.nbytes + kn.nbytes + vn.nbytes + pending["pl_bytes"] / a.steps),
+               "d2h_bytes_per_step": int(out.nbytes),
+               "page_list_bytes_per_step": int(pending["pl_bytes"] / a.steps),
                "ms_per_step": round(e_ms / a.steps, 3),
                "tokens_per_s": round(B * world * a.steps / (e_ms * 1e-3), 1)}
 
-    # ---------------- verification gather (NCCL, outside the timed region)
+    # ---------------- verification (outside the timed region): sampled requests'
+    # outputs + their layer slices gathered to rank 0 (NCCL), checked there
+    # against the C oracle
     finite = bool(torch.isfinite(out.float()).all().item())
-    if world > 1:
-        gathered = gather_rows(out[-1])        # NCCL all-gather of the last layer's outputs
-        finite = finite and bool(torch.isfinite(gathered.float()).all().item())
+    verification = verify_outputs(eng, q, out, attn, rank, world, dev)
 
     pk, src = peaks()
     value = moved / (ms * 1e-3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "decode_traffic.json"
-    if tf.exists() and a.workload == "gemma2-9b":
+    if tf.exists():  # ncu --set full capture of this exact workload (profiles/run_ncu.sh), else null
         try:
-            traffic = json.loads(tf.read_text()).get("traffic_bytes_per_launch")
+            tj = json.loads(tf.read_text())
+            if tj.get("workload") == wl.desc and tj.get("kernel_launches_per_step") == na:
+                traffic = tj.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
     kname = (f"paged_decode_tc_kernel<bf16, D={D}, G={H // Hkv}> (TMA + mma.sync" +
@@ -503,17 +538,83 @@ def run_ours(a, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(dec_gbs, 1),
                      "peak": pk["hbm_gbs"], "peak_source": src, "unit": "GB/s",
                      "frac": round(dec_gbs / pk["hbm_gbs"], 4), "traffic": traffic,
-                     "decode_share_of_step": round(dec_ms / k_steps / ms_per_step, 4),
-                     "timing": f"CUDA events around each decode launch over {k_steps} steps run right after "
-                               f"the event-free timed region",
+                     "decode_share_of_step": round(dec_ms_step / (ms_local / a.steps), 4),
+                     "timing": f"attention launches' time inside the timed graph = step time - the same step "
+                               f"without them (table upload{' + Mamba copies' if mamba else ''}: "
+                               f"{rest_ms * 1e3:.1f} us, its own graph timed over {k_steps} replays)",
+                     "eager_events_gbs": round(ev_gbs, 1),
                      "algorithmic_bytes_per_step": int((kv_local + qo) / a.steps),
                      "algorithmic_bytes_per_launch": int((kv_local + qo) / a.steps / na)},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "setup_s": round(setup_s, 1), "outputs_finite": finite,
     }
+    if verification is not None:
+        res["verification"] = verification
+        res["verified"] = verification["verified"] and finite
     if st_bytes:
         res["mamba_state_bytes_per_step"] = int(st_bytes / a.steps)
     return res
+
+
+# --------------------------------------------------------------------- verification
+def verify_outputs(eng, q, out, attn, rank, world, dev):
+    """Every rank exports, for the last layer of each attention group, one
+    sampled request (a different one per rank): its q and output rows, its
+    block-table row remapped onto a compact copy of its live pages' layer
+    slices, and its seq_len.  One all-gather per group (NCCL over NVLink)
+    brings them to rank 0, which recomputes each row with the C oracle (fp64)
+    and checks the bf16 tolerance of north_star (1e-2, normwise per row:
+    max|got - want| / max|want|).  Returns the summary on rank 0, else None."""
+    import torch
+
+    from paper_2503_18292_b200.distributed import gather_padded
+
+    B = len(eng.requests)
+    last = {}
+    for j, (_, g, l) in enumerate(attn):
+        last[g] = (j, l)
+    b = rank % B
+    gathered = []
+    for g, (j, l) in sorted(last.items()):
+        data, table, seq = eng.export_request_layer(g, l, b)
+        head = torch.tensor([g, l, b, rank, table.numel(), data.numel()], dtype=torch.int64, device=dev)
+        payload = torch.cat([head.view(torch.uint8), table.contiguous().view(torch.uint8), seq.view(torch.uint8),
+                             q[j, b].contiguous().view(torch.uint8).reshape(-1),
+                             out[j, b].contiguous().view(torch.uint8).reshape(-1), data])
+        gathered.append(gather_padded(payload).cpu().numpy())
+    if rank != 0:
+        return None
+    from oracle import c_oracle
+    from oracle.oracle import BF16
+    orc = c_oracle()
+    errs = []
+    for rows in gathered:
+        for r in range(rows.shape[0]):
+            buf = rows[r]
+            g, l, bb, rk, nt, nd = (int(x) for x in buf[:48].view(np.int64))
+            gg = eng.tables[g].geom
+            H, Hkv, D = gg.num_q_heads, gg.num_kv_heads, gg.head_dim
+            o = 48
+            table = buf[o:o + 4 * nt].view(np.int32).reshape(1, nt)
+            o += 4 * nt
+            seq = buf[o:o + 4].view(np.int32).copy()
+            o += 4
+            qrow = buf[o:o + 2 * H * D].view(np.int16).reshape(1, H, D)
+            o += 2 * H * D
+            got = (buf[o:o + 2 * H * D].view(np.uint16).astype(np.uint32) << 16).view(np.float32).reshape(1, H, D)
+            o += 2 * H * D
+            data = np.ascontiguousarray(buf[o:o + nd])
+            ex = eng.view(g, l).exec_page_size
+            want = orc.paged_decode(data, (0, ex, ex), int(gg.kind), BF16, gg.window, np.ascontiguousarray(qrow),
+                                    table, seq, H, Hkv, D, eng.spec.groups[g].tokens_per_page, D ** -0.5,
+                                    eng.geom.softcap, nthreads=os.cpu_count() or 1)
+            errs.append(float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-30)))
+    tol = 1e-2
+    return {"verified": bool(errs) and max(errs) <= tol, "samples": len(errs), "max_rel_err": max(errs),
+            "tolerance": tol,
+            "how": "rank 0 gathers (NCCL all-gather) one sampled request per rank and attention group - q/out rows, "
+                   "block-table row and a compact copy of its live layer slices - and recomputes the last layer's "
+                   "decode with the C oracle (fp64); error normwise per row"}
 
 
 # --------------------------------------------------------------------- CPU baselines
@@ -631,6 +732,10 @@ def run_reference(a):
 
 def main():
     a = parse()
+    if a.impl == "ours" and a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-run this script as a.gpus ranks (torch.distributed.run, 127.0.0.1)
+        from paper_2503_18292_b200.distributed import launch_local_ranks
+        sys.exit(launch_local_ranks(str(Path(__file__).resolve()), sys.argv[1:], a.gpus))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -641,6 +746,8 @@ def main():
             a.warmup = min(a.warmup, 1)
             print(json.dumps(run_reference(a)), flush=True)
         return
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but the launcher started {world} ranks")
     import torch
     import torch.distributed as dist
     if world > 1:

@@ -282,6 +282,35 @@ int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64_t* requests,
                          jenga_small_page* pages, int32_t* first_live_block, int32_t* n_stored);
 
 /* ------------------------------------------------------------------------
+ * Delta page-list upload (the CSR path above re-packs
+ * every list).  A decode step changes at most two entries of a (request,
+ * group) row — the block store_position appended (simulator.cpp:248-253) and
+ * a sliding-window block it freed (:272-280).  A table mirror remembers what
+ * one group's device block table [max_batch][max_blocks] holds; each pack
+ * diffs the page lists of requests[0..n_req) (row i = requests[i]) against it
+ * and writes only the changed entries, plus every row's seq_len and newest-
+ * token slot, into `delta`.  Rows whose list changed in any other way
+ * (rollback, prefix adoption, release, a different request) are resent in
+ * full; rows beyond n_req that held a request are cleared.  Each packed
+ * buffer must be applied to the device table exactly once, in order
+ * (jenga_upload_page_list_deltas); reset the mirror after rebuilding the
+ * table any other way.  Validation happens before anything is written:
+ * JENGA_ERR_CONFIG for a batch or request wider than the mirror or a buffer
+ * smaller than *used_bytes (reported either way).
+ * ---------------------------------------------------------------------- */
+typedef struct jenga_table_mirror jenga_table_mirror;
+/* Bytes a delta buffer needs in the worst case (every row rewritten). */
+size_t jenga_delta_buffer_bytes(int max_batch, int max_blocks);
+int jenga_table_mirror_create(const jenga_pages* pl, int g, int max_batch, int max_blocks,
+                              jenga_table_mirror** out);
+void jenga_table_mirror_destroy(jenga_table_mirror* mirror);
+/* The device table is all -1 again (e.g. freshly filled). */
+int jenga_table_mirror_reset(jenga_table_mirror* mirror);
+int jenga_pages_pack_deltas(jenga_table_mirror* mirror, const uint64_t* requests, int n_req,
+                            void* delta, size_t capacity_bytes, size_t* used_bytes,
+                            int* n_records);
+
+/* ------------------------------------------------------------------------
  * Device API (sm_100a).  One arena per GPU: num_large_pages x large_page_bytes
  * (= LargePagePool sizing, lcm_allocator.cpp:12-18), 4 KiB aligned.
  * All launches are async on `stream` (cudaStream_t). Pointers are device
@@ -305,6 +334,22 @@ int jenga_build_block_tables(const int32_t* offsets, const jenga_small_page* pag
                              int batch, uint32_t slots_per_large, uint32_t tokens_per_page,
                              int max_blocks, int32_t* block_table, int64_t* slot_mapping,
                              int32_t* seq_lens, void* stream);
+
+/* Apply a delta buffer from jenga_pages_pack_deltas to one group's table:
+ * block_table[max_batch][max_blocks] entries, seq_lens[] and slot_mapping[]
+ * (the newest stored ordinal's slot; -1 none) of the rows it describes.  The
+ * kernel reads `delta` in place — pinned host memory (device-accessible
+ * through unified addressing) or device memory — so no host->device copy is
+ * issued, the record count may change every step, and the launch can be
+ * captured in a CUDA graph that is replayed after each pack.  The launch
+ * writes the buffer's sequence number back into its header; the next pack
+ * reads it, and if its predecessor never reached the device (a buffer packed
+ * and overwritten, or packed before a graph capture and not replayed) it
+ * rewrites every row over the full table width.  The caller must not rewrite
+ * `delta` before this launch has completed (record an event). */
+int jenga_upload_page_list_deltas(void* delta, int max_batch, int max_blocks,
+                                  int32_t* block_table, int32_t* seq_lens,
+                                  int64_t* slot_mapping, void* stream);
 
 /* Slot mapping for a run of new tokens (prefill chunk):
  *   token t of request req[t] at 1-based ordinal ord[t] ->

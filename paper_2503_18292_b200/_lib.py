@@ -139,6 +139,12 @@ _SIGS = {
     "jenga_pages_group_state": (_int, [_p, _u64, _int, _pu64, _pu64, _pu64, _pu64, _pint, C.POINTER(SmallPage)]),
     "jenga_pages_blocks": (_int, [_p, _u64, _int, C.POINTER(SmallPage), C.POINTER(C.c_uint8), _u64, _pu64]),
     "jenga_pages_pack_csr": (_int, [_p, _int, _pu64, _int, _int, C.c_int64, _pi32, C.POINTER(SmallPage), _pi32, _pi32]),
+    "jenga_delta_buffer_bytes": (C.c_size_t, [_int, _int]),
+    "jenga_table_mirror_create": (_int, [_p, _int, _int, _int, C.POINTER(_p)]),
+    "jenga_table_mirror_destroy": (None, [_p]),
+    "jenga_table_mirror_reset": (_int, [_p]),
+    "jenga_pages_pack_deltas": (_int, [_p, _pu64, _int, _p, C.c_size_t, C.POINTER(C.c_size_t), _pint]),
+    "jenga_upload_page_list_deltas": (_int, [_p, _int, _int, _p, _p, _p, _p]),
     "jenga_arena_create": (_int, [_int, _u64, _u64, C.POINTER(_p)]),
     "jenga_arena_destroy": (None, [_p]),
     "jenga_arena_base": (_p, [_p]),

@@ -647,3 +647,191 @@ JENGA_EXPORT int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64
     }
   });
 }
+
+// ------------------------------------------------------------------------
+// Delta page-list upload.  A decode step changes at most
+// two entries of a (request, group) row — the block store_position appended
+// (simulator.cpp:248-253) and a sliding-window block it freed (:272-280) — so
+// instead of re-packing every list, a host mirror of what the device table
+// holds diffs each row against the page lists and emits only the changed
+// entries, plus every row's seq_len and newest-token slot.
+struct jenga_table_mirror {
+  const jenga_pages* pl = nullptr;
+  int g = 0;
+  int max_batch = 0, max_blocks = 0;
+  uint32_t slots_per_large = 1, tpp = 1;
+  bool mamba = false;
+  struct Row {
+    uint64_t request = UINT64_MAX;  // none
+    uint64_t epoch = 0;
+    int64_t count = 0, first_live = 0;
+  };
+  std::vector<Row> rows;
+  int n_rows = 0;  // rows the last pack described
+  std::vector<int32_t> rec;  // staging: (flat index, value) pairs
+  // The last packed buffer and its sequence number: the device writes the
+  // number back (header word 4) when it applies the buffer, so a pack whose
+  // predecessor was never applied (overwritten, or packed before a graph
+  // capture and never replayed) knows the device table is not what the
+  // mirror says, and rewrites every row over the full width instead.
+  const volatile int32_t* last_buf = nullptr;
+  int32_t last_seq = 0;
+  void invalidate() {
+    for (auto& r : rows) r = Row{UINT64_MAX - 1, 0, max_blocks, 0};
+    n_rows = max_batch;
+  }
+};
+
+namespace {
+// int32 n_records, n_rows, max_blocks, seq, ack (device-written), 3 x reserved
+constexpr size_t kDeltaHeader = 32;
+size_t delta_bytes(int n_rows, size_t n_records) {
+  return kDeltaHeader + static_cast<size_t>(n_rows) * 12 + n_records * 8;
+}
+}  // namespace
+
+JENGA_EXPORT size_t jenga_delta_buffer_bytes(int max_batch, int max_blocks) {
+  if (max_batch < 0 || max_blocks < 0) return 0;
+  // worst case: every row rewritten in full, twice its width (old + new length)
+  return delta_bytes(max_batch, 2 * static_cast<size_t>(max_batch) * static_cast<size_t>(max_blocks));
+}
+
+JENGA_EXPORT int jenga_table_mirror_create(const jenga_pages* pl, int g, int max_batch, int max_blocks,
+                                           jenga_table_mirror** out) {
+  ARG_CHECK(pl != nullptr && out != nullptr && g >= 0 && max_batch >= 0 && max_blocks > 0);
+  return guarded([&] {
+    JENGA_CHECK(static_cast<size_t>(g) < pl->kv->num_groups(), "group index out of range");
+    JENGA_CHECK(int64_t{max_batch} * max_blocks <= INT32_MAX, "block table too large for int32 entry indices");
+    const auto& geo = pl->kv->type_allocator(g).geometry();
+    JENGA_CHECK(uint64_t{pl->kv->pool().num_pages()} * geo.slots_per_large <= uint64_t{INT32_MAX},
+                "pool too large for int32 global page indices");
+    auto m = std::make_unique<jenga_table_mirror>();
+    m->pl = pl;
+    m->g = g;
+    m->max_batch = max_batch;
+    m->max_blocks = max_blocks;
+    m->slots_per_large = geo.slots_per_large;
+    m->tpp = pl->kv->group(g).tokens_per_page;
+    m->mamba = pl->kv->group(g).kind == jenga::LayerKind::kMamba;
+    m->rows.assign(max_batch, jenga_table_mirror::Row{});
+    *out = m.release();
+  });
+}
+
+JENGA_EXPORT void jenga_table_mirror_destroy(jenga_table_mirror* m) { delete m; }
+
+JENGA_EXPORT int jenga_table_mirror_reset(jenga_table_mirror* m) {
+  ARG_CHECK(m != nullptr);
+  // the device table is assumed all -1 again (a freshly filled table)
+  for (auto& r : m->rows) r = jenga_table_mirror::Row{};
+  m->n_rows = 0;
+  m->last_buf = nullptr;
+  m->last_seq = 0;
+  return JENGA_OK;
+}
+
+JENGA_EXPORT int jenga_pages_pack_deltas(jenga_table_mirror* m, const uint64_t* requests, int n_req, void* delta,
+                                         size_t capacity_bytes, size_t* used_bytes, int* n_records) {
+  ARG_CHECK(m != nullptr && (n_req == 0 || requests != nullptr) && n_req >= 0 && delta != nullptr);
+  return guarded([&] {
+    if (n_req > m->max_batch)
+      throw jenga::ConfigError("batch of " + std::to_string(n_req) + " exceeds the mirror's " +
+                               std::to_string(m->max_batch) + " rows");
+    const int g = m->g;
+    const int64_t W = m->max_blocks;
+    if (m->last_buf != nullptr && m->last_buf[4] != m->last_seq) m->invalidate();
+    m->rec.clear();
+    auto global_of = [&](const jenga::SmallPageId& p) {
+      return static_cast<int32_t>(uint64_t{p.large.index} * m->slots_per_large + p.slot);
+    };
+    struct RowOut {
+      int32_t seq;
+      int64_t slot;
+      jenga_table_mirror::Row next;
+    };
+    std::vector<RowOut> outs(std::max(n_req, m->n_rows));
+    // Pass 1: diff every row into the staging records; the mirror itself is only
+    // updated once the caller's buffer is known to be large enough.
+    for (int i = 0; i < n_req; ++i) {
+      const auto& r = m->pl->pl->request(requests[i]);
+      JENGA_CHECK(static_cast<size_t>(g) < r.groups.size(), "group index out of range");
+      const auto& rt = r.groups[g];
+      const int64_t cnt = m->mamba ? (rt.working_page ? 1 : 0) : static_cast<int64_t>(rt.blocks.size());
+      const int64_t fl = m->mamba ? 0 : static_cast<int64_t>(rt.freed_blocks);
+      if (cnt > W)
+        throw jenga::ConfigError("request " + std::to_string(requests[i]) + " holds " + std::to_string(cnt) +
+                                 " blocks; the block table is " + std::to_string(W) + " wide");
+      if (!m->mamba)
+        for (int64_t b = fl; b < cnt; ++b) JENGA_CHECK(rt.blocks[b].live, "dead block after the first live block");
+      auto value = [&](int64_t b) -> int32_t {
+        if (b < fl || b >= cnt) return -1;
+        return global_of(m->mamba ? *rt.working_page : rt.blocks[b].page);
+      };
+      const auto& old = m->rows[i];
+      const int64_t base = static_cast<int64_t>(i) * W;
+      const bool full = old.request != r.id || old.epoch != rt.epoch || cnt < old.count || fl < old.first_live;
+      if (full) {
+        for (int64_t b = 0, end = std::max(cnt, old.count); b < end; ++b) {
+          m->rec.push_back(static_cast<int32_t>(base + b));
+          m->rec.push_back(value(b));
+        }
+      } else {
+        for (int64_t b = old.first_live, end = std::min(fl, old.count); b < end; ++b) {  // newly dead
+          m->rec.push_back(static_cast<int32_t>(base + b));
+          m->rec.push_back(-1);
+        }
+        for (int64_t b = old.count; b < cnt; ++b) {  // appended
+          m->rec.push_back(static_cast<int32_t>(base + b));
+          m->rec.push_back(value(b));
+        }
+      }
+      // newest stored ordinal's slot (exactly jenga_build_block_tables' rule)
+      int64_t slot = -1;
+      const int64_t n = static_cast<int64_t>(rt.stored);
+      if (n > 0) {
+        const int64_t blk = (n - 1) / m->tpp;
+        if (blk < cnt && blk >= fl) slot = int64_t{value(blk)} * m->tpp + (n - 1) % m->tpp;
+      }
+      JENGA_CHECK(n <= INT32_MAX, "sequence too long for int32 seq_lens");
+      outs[i] = RowOut{static_cast<int32_t>(n), slot, jenga_table_mirror::Row{r.id, rt.epoch, cnt, fl}};
+    }
+    for (int i = n_req; i < m->n_rows; ++i) {  // rows that left the batch: clear them
+      const auto& old = m->rows[i];
+      for (int64_t b = 0; b < old.count; ++b) {
+        m->rec.push_back(static_cast<int32_t>(int64_t{i} * W + b));
+        m->rec.push_back(-1);
+      }
+      outs[i] = RowOut{0, -1, jenga_table_mirror::Row{}};
+    }
+    const int rows_out = static_cast<int>(outs.size());
+    const size_t nrec = m->rec.size() / 2;
+    const size_t need = delta_bytes(rows_out, nrec);
+    if (used_bytes) *used_bytes = need;
+    if (n_records) *n_records = static_cast<int>(nrec);
+    if (need > capacity_bytes)
+      throw jenga::ConfigError("delta needs " + std::to_string(need) + " bytes; the buffer holds " +
+                               std::to_string(capacity_bytes));
+    JENGA_CHECK(nrec <= static_cast<size_t>(INT32_MAX), "too many delta records");
+    // Pass 2: write the buffer, then commit the mirror.
+    auto* w = static_cast<uint8_t*>(delta);
+    int64_t* slots = reinterpret_cast<int64_t*>(w + kDeltaHeader);
+    int32_t* seqs = reinterpret_cast<int32_t*>(w + kDeltaHeader + 8 * static_cast<size_t>(rows_out));
+    int32_t* recs = seqs + rows_out;
+    for (int i = 0; i < rows_out; ++i) {
+      slots[i] = outs[i].slot;
+      seqs[i] = outs[i].seq;
+    }
+    if (nrec) std::memcpy(recs, m->rec.data(), nrec * 8);
+    int32_t* hdr = reinterpret_cast<int32_t*>(w);
+    m->last_seq = m->last_seq == INT32_MAX ? 1 : m->last_seq + 1;
+    hdr[0] = static_cast<int32_t>(nrec);
+    hdr[1] = rows_out;
+    hdr[2] = m->max_blocks;
+    hdr[3] = m->last_seq;
+    hdr[4] = 0;  // ack: the applying kernel writes seq here
+    hdr[5] = hdr[6] = hdr[7] = 0;
+    for (int i = 0; i < rows_out; ++i) m->rows[i] = outs[i].next;
+    m->n_rows = n_req;
+    m->last_buf = reinterpret_cast<const volatile int32_t*>(w);
+  });
+}

@@ -408,6 +408,10 @@ class PageLists {
     uint64_t checkpoints = 0;
     uint64_t consumed_held = 0;      // vision: consumed ordinals still held
     uint64_t consumed_ordinals = 0;  // vision: ordinals consumed by prefill
+    // Bumped (to a PageLists-wide unique value) whenever the list changes other
+    // than by appending blocks at the tail or freeing its leading live block:
+    // a table mirror (jenga_pages_pack_deltas) then resends the whole row.
+    uint64_t epoch = 0;
   };
   struct ImageSpan {
     uint64_t begin = 0, end = 0;  // prompt positions, inclusive
@@ -495,6 +499,10 @@ class PageLists {
   void free_block(Request& r, size_t g, uint64_t b, bool allow_cache, uint64_t now);
   void finish_prefill(Request& r, uint64_t now);
   uint64_t adopt_prefix(Request& r, uint64_t now);
+  void reset_groups(Request& r);  // fresh GroupRuntimes, new epochs
+  void bump(GroupRuntime& rt) { rt.epoch = ++epoch_counter_; }
+
+  uint64_t epoch_counter_ = 0;
 
   KvAllocator* kv_;
   bool prefix_caching_;

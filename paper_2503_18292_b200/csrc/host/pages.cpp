@@ -19,9 +19,14 @@ void PageLists::add_request(uint64_t id) {
   index_[id] = requests_.size();
   Request r;
   r.id = id;
-  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  reset_groups(r);
   r.restore.assign(kv_->num_groups(), std::nullopt);
   requests_.push_back(std::move(r));
+}
+
+void PageLists::reset_groups(Request& r) {
+  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  for (GroupRuntime& rt : r.groups) bump(rt);
 }
 
 PageLists::Request& PageLists::req(uint64_t id) {
@@ -210,7 +215,7 @@ uint64_t PageLists::admit(uint64_t id, const std::vector<uint64_t>& tokens, cons
   r.image_ordinal = image_ordinals.size() == tokens.size() ? image_ordinals : std::vector<uint64_t>(tokens.size(), 0);
   r.prompt_len = tokens.size();
   r.consumed = 0;
-  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  reset_groups(r);
   r.restore.assign(kv_->num_groups(), std::nullopt);
   r.needs_release = false;
   r.suppress_window_free = false;
@@ -380,6 +385,7 @@ void PageLists::rollback_newest(uint64_t id, size_t g, uint64_t count, uint64_t 
         rt.blocks[bidx].live = false;
         rt.live_blocks--;
         rt.blocks.pop_back();
+        bump(rt);
       }
     }
   }
@@ -481,7 +487,7 @@ void PageLists::release(uint64_t id, bool allow_cache, uint64_t now) {
       rt.working_page.reset();
     }
   }
-  r.groups.assign(kv_->num_groups(), GroupRuntime{});
+  reset_groups(r);
   r.needs_release = false;
   r.draft_len = 0;
   r.suppress_window_free = false;

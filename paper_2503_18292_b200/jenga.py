@@ -544,3 +544,44 @@ class PageLists:
                                        first_live.ctypes.data_as(C.POINTER(C.c_int32)),
                                        n_stored.ctypes.data_as(C.POINTER(C.c_int32))))
         return offsets, pages[:total], first_live, n_stored
+
+
+class TableMirror:
+    """Host mirror of one group's device block table (jenga_table_mirror):
+    pack() diffs the page lists against what the device holds and writes only
+    the changed entries (+ seq_lens / newest slots) into a delta buffer that
+    jenga_upload_page_list_deltas applies on the device."""
+
+    HEADER = 32
+
+    def __init__(self, pages: PageLists, g: int, max_batch: int, max_blocks: int):
+        self.pages, self.g, self.max_batch, self.max_blocks = pages, g, max_batch, max_blocks
+        self.h = C.c_void_p()
+        check(lib.jenga_table_mirror_create(pages.h, g, max_batch, max_blocks, C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.jenga_table_mirror_destroy(self.h)
+            self.h = None
+
+    @staticmethod
+    def buffer_bytes(max_batch: int, max_blocks: int) -> int:
+        return int(lib.jenga_delta_buffer_bytes(max_batch, max_blocks))
+
+    def reset(self) -> None:
+        check(lib.jenga_table_mirror_reset(self.h))
+
+    def pack(self, requests, buf_ptr: int, capacity: int):
+        """Diff rows requests[i] into the buffer at buf_ptr; returns (bytes used, records)."""
+        req = np.ascontiguousarray(np.asarray(requests, dtype=np.uint64))
+        used = C.c_size_t()
+        nrec = C.c_int()
+        check(lib.jenga_pages_pack_deltas(self.h, req.ctypes.data_as(C.POINTER(C.c_uint64)), len(req),
+                                          C.c_void_p(buf_ptr), capacity, C.byref(used), C.byref(nrec)))
+        return int(used.value), int(nrec.value)
+
+    @staticmethod
+    def seq_lens_view(buf: np.ndarray, rows: int) -> np.ndarray:
+        """int32 seq_lens of the last pack, inside the (uint8) buffer."""
+        o = TableMirror.HEADER + 8 * rows
+        return buf[o:o + 4 * rows].view(np.int32)

@@ -70,7 +70,8 @@ def fill_group_kv(eng: DecodeEngine, g: int, layers, seed=0, all_live=False):
     n = t.h_n_stored[:B].numpy().astype(np.int64)
     lo = np.zeros(B, dtype=np.int64)
     if all_live:
-        lo = t.h_first_live[:B].numpy().astype(np.int64) * eng.spec.groups[g].tokens_per_page
+        tpp = eng.spec.groups[g].tokens_per_page
+        lo = np.array([eng.pages.group_state(r, g)["freed_blocks"] * tpp for r in eng.requests], dtype=np.int64)
     elif gg.window:
         lo = np.maximum(0, n - gg.window)
     req = np.concatenate([np.full(n[b] - lo[b], b, dtype=np.int32) for b in range(B)]) if n.sum() else \

@@ -330,3 +330,42 @@ def test_fused_append_graph_steps_match_unfused():
         torch.cuda.synchronize()
         assert torch.equal(outs[0], outs[1]), f"step {s}: fused graph output differs"
     assert torch.equal(fused.arena.tensor(), eager.arena.tensor())
+
+
+def test_delta_upload_matches_full_rebuild():
+    """Delta page-list upload (table mirror -> jenga_upload_page_list_deltas,
+    the kernel reading the pinned delta buffer in place) vs the CSR rebuild
+    (jenga_build_block_tables) on two engines fed the same appends: block
+    tables, seq_lens and newest slots bit-identical after every step — SWA
+    frees, Mamba working pages, uneven appends, eager and graph-replayed."""
+    from paper_2503_18292_b200.engine import DecodeEngine
+    geom = ModelGeometry("d", [
+        GroupGeometry("full", LayerKind.kFullAttention, 2, 8, 16, 128, torch.bfloat16, 16),
+        GroupGeometry("window", LayerKind.kSlidingWindow, 2, 8, 16, 128, torch.bfloat16, 16, window=70),
+        GroupGeometry("ssm", LayerKind.kMamba, 3, state_bytes=4096)])
+    B = 6
+    engs = [DecodeEngine(geom, 400, B, 700, upload=u) for u in ("delta", "full")]
+    for e in engs:
+        e.add_requests(range(B))
+    rng = np.random.default_rng(5)
+    graph = None
+    for step in range(260):
+        ids = [r for r in range(B) if rng.random() < 0.8]
+        for e in engs:
+            e.append(ids)
+            e.pack_tables()
+        if step == 100:  # from here on the delta engine's device half is a replayed graph
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                engs[0].upload_tables()
+        if graph is None:
+            engs[0].upload_tables()
+        else:
+            graph.replay()
+        engs[1].upload_tables()
+        torch.cuda.synchronize()
+        for g in range(3):
+            a, b = engs[0].tables[g], engs[1].tables[g]
+            assert torch.equal(a.block_table, b.block_table), (step, g)
+            assert torch.equal(a.seq_lens, b.seq_lens) and torch.equal(a.slot_mapping, b.slot_mapping), (step, g)
+            assert torch.equal(a.h_n_stored, b.h_n_stored)
