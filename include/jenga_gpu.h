@@ -249,6 +249,24 @@ int jenga_pages_restore_pending(const jenga_pages* pl, uint64_t request, int g, 
                                 jenga_small_page* checkpoint);
 int jenga_pages_finish_restore(jenga_pages* pl, uint64_t request, int g, uint64_t now_step);
 int jenga_pages_set_fix_mamba_restore(jenga_pages* pl, int on);
+/* Mamba checkpoint snapshots.  store_position allocates a checkpoint page
+ * every checkpoint_interval stored positions and frees it straight into the
+ * prefix cache (simulator.cpp:231-242); the reference models bytes only.  On
+ * the device the working state at that ordinal must be copied into the page
+ * (jenga_page_copy working -> checkpoint) before a later prefix hit restores
+ * from it.  Each such page is queued; this drains up to `capacity` entries,
+ * skipping pages evicted from the cache since (they may already belong to
+ * another request).  Call it after the host half of a step and issue the
+ * copies before the step's device work can overwrite the pages. */
+typedef struct jenga_checkpoint_copy {
+  uint64_t request;
+  int32_t group;
+  int32_t reserved;
+  uint64_t ordinal;              /* stored ordinal the state corresponds to */
+  jenga_small_page working;      /* source: the request's working page */
+  jenga_small_page checkpoint;   /* destination: the cached checkpoint page */
+} jenga_checkpoint_copy;
+int jenga_pages_take_checkpoint_copies(jenga_pages* pl, jenga_checkpoint_copy* out, int capacity, int* n);
 /* Defer sliding-window frees across a prefill chunk (the reference's
  * suppress_window_free, simulator.cpp:466-500): while on, stored positions
  * never free out-of-window blocks; apply performs the pending frees once the

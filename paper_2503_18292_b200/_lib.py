@@ -53,6 +53,11 @@ class SmallPage(C.Structure):
     _fields_ = [("large", C.c_uint32), ("slot", C.c_uint32)]
 
 
+class CheckpointCopyC(C.Structure):
+    _fields_ = [("request", C.c_uint64), ("group", C.c_int32), ("reserved", C.c_int32), ("ordinal", C.c_uint64),
+                ("working", SmallPage), ("checkpoint", SmallPage)]
+
+
 class ByteRangeC(C.Structure):
     _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64)]
 
@@ -128,6 +133,7 @@ _SIGS = {
     "jenga_pages_restore_pending": (_int, [_p, _u64, _int, _pint, C.POINTER(SmallPage)]),
     "jenga_pages_finish_restore": (_int, [_p, _u64, _int, _u64]),
     "jenga_pages_set_fix_mamba_restore": (_int, [_p, _int]),
+    "jenga_pages_take_checkpoint_copies": (_int, [_p, C.POINTER(CheckpointCopyC), _int, _pint]),
     "jenga_pages_set_defer_window_free": (_int, [_p, _u64, _int]),
     "jenga_pages_apply_window_free": (_int, [_p, _u64, _u64]),
     "jenga_pages_set_vision_mode": (_int, [_p, _int]),

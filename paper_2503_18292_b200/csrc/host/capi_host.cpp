@@ -57,6 +57,7 @@ struct jenga_addr {
 struct jenga_pages {
   std::unique_ptr<jenga::PageLists> pl;
   jenga::KvAllocator* kv;
+  std::vector<jenga_checkpoint_copy> pending_copies;  // drained, not yet handed out
 };
 
 #define ARG_CHECK(cond) \
@@ -533,6 +534,21 @@ JENGA_EXPORT int jenga_pages_finish_restore(jenga_pages* pl, uint64_t request, i
   return guarded([&] { pl->pl->finish_restore(request, static_cast<size_t>(g), now); });
 }
 
+JENGA_EXPORT int jenga_pages_take_checkpoint_copies(jenga_pages* pl, jenga_checkpoint_copy* out, int capacity,
+                                                   int* n) {
+  ARG_CHECK(pl != nullptr && n != nullptr && capacity >= 0 && (capacity == 0 || out != nullptr));
+  return guarded([&] {
+    auto& pending = pl->pending_copies;
+    auto fresh = pl->pl->take_checkpoint_copies();
+    for (auto& c : fresh)
+      pending.push_back(jenga_checkpoint_copy{c.request, c.g, 0, c.ordinal, to_c(c.working), to_c(c.checkpoint)});
+    const int take = std::min<int>(capacity, static_cast<int>(pending.size()));
+    for (int i = 0; i < take; ++i) out[i] = pending[i];
+    pending.erase(pending.begin(), pending.begin() + take);
+    *n = take;
+  });
+}
+
 JENGA_EXPORT int jenga_pages_set_fix_mamba_restore(jenga_pages* pl, int on) {
   ARG_CHECK(pl != nullptr);
   pl->pl->fix_mamba_restore = on != 0;
@@ -685,9 +701,10 @@ struct jenga_table_mirror {
 namespace {
 // int32 n_records, n_rows, max_blocks, seq, ack (device-written), 3 x reserved
 constexpr size_t kDeltaHeader = 32;
-size_t delta_bytes(int n_rows, size_t n_records) {
-  return kDeltaHeader + static_cast<size_t>(n_rows) * 12 + n_records * 8;
-}
+// header | int64 slots[n_rows] | int32 seq_lens[n_rows] (+4 B pad when n_rows is
+// odd, so the (int32, int32) records are 8-byte aligned) | records
+size_t records_offset(int n_rows) { return kDeltaHeader + static_cast<size_t>(n_rows) * 12 + (n_rows & 1) * 4; }
+size_t delta_bytes(int n_rows, size_t n_records) { return records_offset(n_rows) + n_records * 8; }
 }  // namespace
 
 JENGA_EXPORT size_t jenga_delta_buffer_bytes(int max_batch, int max_blocks) {
@@ -816,7 +833,7 @@ JENGA_EXPORT int jenga_pages_pack_deltas(jenga_table_mirror* m, const uint64_t* 
     auto* w = static_cast<uint8_t*>(delta);
     int64_t* slots = reinterpret_cast<int64_t*>(w + kDeltaHeader);
     int32_t* seqs = reinterpret_cast<int32_t*>(w + kDeltaHeader + 8 * static_cast<size_t>(rows_out));
-    int32_t* recs = seqs + rows_out;
+    int32_t* recs = reinterpret_cast<int32_t*>(w + records_offset(rows_out));
     for (int i = 0; i < rows_out; ++i) {
       slots[i] = outs[i].slot;
       seqs[i] = outs[i].seq;

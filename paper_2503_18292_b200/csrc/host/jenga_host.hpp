@@ -492,6 +492,22 @@ class PageLists {
   void apply_window_free(uint64_t id, uint64_t now);
   bool fix_mamba_restore = true;  // false: keep the reference's pinned-page leak
 
+  // Mamba checkpoint snapshots: store_position allocates a checkpoint page
+  // every k stored positions and frees it straight into the prefix cache
+  // (simulator.cpp:231-242) — a byte model with no bytes.  On the device the
+  // working state at that ordinal must be copied into the page before anyone
+  // can hit it; each allocation is queued here and drained by the caller
+  // (take_checkpoint_copies), which drops copies whose page was evicted from
+  // the cache in the meantime (it may already belong to another request).
+  struct CheckpointCopy {
+    uint64_t request = 0;
+    uint32_t g = 0;
+    uint64_t ordinal = 0;          // stored ordinal the state corresponds to
+    SmallPageId working, checkpoint;
+    BlockContent key;              // cache key the page was registered under
+  };
+  std::vector<CheckpointCopy> take_checkpoint_copies();
+
  private:
   Request& req(uint64_t id);
   std::vector<GroupLookupInput> build_lookup_inputs(const Request& r) const;
@@ -503,6 +519,7 @@ class PageLists {
   void bump(GroupRuntime& rt) { rt.epoch = ++epoch_counter_; }
 
   uint64_t epoch_counter_ = 0;
+  std::vector<CheckpointCopy> checkpoint_copies_;
 
   KvAllocator* kv_;
   bool prefix_caching_;

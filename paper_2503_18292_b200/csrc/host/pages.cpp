@@ -95,6 +95,8 @@ bool PageLists::store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now
       ta.touch(res->page, now);
       rt.checkpoints = rt.stored / k;
       kv_->free(g, res->page, rt.chain[rt.checkpoints - 1]);
+      checkpoint_copies_.push_back(CheckpointCopy{id, static_cast<uint32_t>(g), rt.stored, *rt.working_page,
+                                                  res->page, rt.chain[rt.checkpoints - 1]});
     }
     return true;
   }
@@ -471,6 +473,17 @@ void PageLists::finish_restore(uint64_t id, size_t g, uint64_t now) {
   kv_->type_allocator(g).touch(page, now);
   kv_->free(g, page, rt.chain[rt.checkpoints - 1]);  // back to the cache as the same checkpoint
   r.restore[g].reset();
+}
+
+std::vector<PageLists::CheckpointCopy> PageLists::take_checkpoint_copies() {
+  std::vector<CheckpointCopy> out;
+  for (CheckpointCopy& c : checkpoint_copies_) {
+    // still registered under its key <=> not evicted (and so not re-allocated)
+    const auto page = kv_->cache().find(c.g, c.key);
+    if (page.has_value() && *page == c.checkpoint) out.push_back(std::move(c));
+  }
+  checkpoint_copies_.clear();
+  return out;
 }
 
 // reference simulator.cpp:314-327

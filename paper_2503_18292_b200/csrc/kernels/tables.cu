@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(256) slot_mapping_kernel(const int32_t* __rest
 // of its own, and a step that captures this launch in a CUDA graph replays it
 // with whatever the host packed last.
 //   [0] n_records [1] n_rows [2] max_blocks [3] seq [4] ack [5..7] 0 |
-//   int64 slots[n_rows] | int32 seq_lens[n_rows] | int32 (flat entry, value)[n_records]
+//   int64 slots[n_rows] | int32 seq_lens[n_rows] (+1 pad if n_rows is odd) |
+//   int32 (flat entry, value)[n_records] (8-byte aligned)
 // The launch acknowledges the buffer by writing seq into word 4, which tells
 // the next pack that its predecessor reached the device.
 __global__ void __launch_bounds__(256) apply_deltas_kernel(int32_t* __restrict__ delta, int max_batch,
@@ -85,8 +86,9 @@ __global__ void __launch_bounds__(256) apply_deltas_kernel(int32_t* __restrict__
   if (blockIdx.x == 0 && threadIdx.x == 0) __stcg(delta + 4, __ldcv(delta + 3));  // ack
   const int64_t entries = static_cast<int64_t>(max_batch) * max_blocks;
   const int64_t* slots = reinterpret_cast<const int64_t*>(delta + 8);
-  const int32_t* seqs = delta + 8 + 2 * __ldcv(delta + 1);
-  const int2* rec = reinterpret_cast<const int2*>(seqs + __ldcv(delta + 1));
+  const int rows_packed = __ldcv(delta + 1);
+  const int32_t* seqs = delta + 8 + 2 * rows_packed;
+  const int2* rec = reinterpret_cast<const int2*>(seqs + rows_packed + (rows_packed & 1));
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += stride) {
     if (seq_lens) seq_lens[i] = __ldcv(seqs + i);

@@ -205,7 +205,7 @@ class DecodeEngine:
         """Host->device page-list bytes of one upload (the bytes the device reads)."""
         n = len(self.requests)
         if self.upload == "delta":
-            return sum(32 + 12 * n + 8 * nrec for nrec in totals.values())
+            return sum(32 + 12 * n + 4 * (n & 1) + 8 * nrec for nrec in totals.values())
         return int(self._h_stage.numel() * 4)
 
     # ------------------------------------------------------------ per layer ops

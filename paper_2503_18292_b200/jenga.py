@@ -461,6 +461,22 @@ class PageLists:
     def finish_restore(self, request: int, g: int, now: int = 0) -> None:
         check(lib.jenga_pages_finish_restore(self.h, request, g, now))
 
+    def take_checkpoint_copies(self, capacity: int = 4096):
+        """Drain the queued Mamba checkpoint snapshots: list of dicts with
+        request, group, ordinal, working (source) and checkpoint (destination)."""
+        buf = (_lib.CheckpointCopyC * max(1, capacity))()
+        out = []
+        while True:
+            n = C.c_int()
+            check(lib.jenga_pages_take_checkpoint_copies(self.h, buf, capacity, C.byref(n)))
+            for i in range(n.value):
+                c = buf[i]
+                out.append({"request": c.request, "group": c.group, "ordinal": c.ordinal,
+                            "working": SmallPageId(c.working.large, c.working.slot),
+                            "checkpoint": SmallPageId(c.checkpoint.large, c.checkpoint.slot)})
+            if n.value < capacity:
+                return out
+
     def set_fix_mamba_restore(self, on: bool) -> None:
         check(lib.jenga_pages_set_fix_mamba_restore(self.h, 1 if on else 0))
 

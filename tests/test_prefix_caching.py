@@ -177,3 +177,32 @@ def test_prefix_hit_splices_cached_pages():
     win = pl.blocks(2, 1)
     assert sum(lv for _, lv in win) == 2 and all(not lv for _, lv in win[:5])  # only the window's blocks pinned
     kv.check_invariants()
+
+
+def test_mamba_checkpoint_copies_are_queued_and_dropped_when_evicted():
+    """Every checkpoint page store_position allocates (simulator.cpp:231-242)
+    is reported once as a working -> checkpoint copy for the device; a page
+    evicted from the cache before the copy was taken is not reported."""
+    spec = ModelSpec("hyb", [LayerGroupSpec("attn", LayerKind.kFullAttention, 2, 64, tokens_per_page=2),
+                             LayerGroupSpec("ssm", LayerKind.kMamba, 3, 256, checkpoint_interval_tokens=16)])
+    kv = KvAllocator(spec, 1 << 22)
+    pl = PageLists(kv, prefix_caching=True)
+    toks = [mix64(i) for i in range(40)]
+    pl.add_request(1)
+    pl.admit(1, toks)
+    assert pl.prefill(1, 100) == (40, False)
+    copies = pl.take_checkpoint_copies()
+    wp = pl.group_state(1, 1)["working_page"]
+    assert [c["ordinal"] for c in copies] == [16, 32]
+    assert all(c["group"] == 1 and c["request"] == 1 and c["working"] == wp for c in copies)
+    assert len({c["checkpoint"] for c in copies}) == 2 and wp not in {c["checkpoint"] for c in copies}
+    for c in copies:
+        assert kv.record(1, c["checkpoint"])["state"] == 1  # cached (evictable)
+    assert pl.take_checkpoint_copies() == []  # drained
+    # decode 16 more tokens -> one more checkpoint, then evict everything evictable
+    for i in range(16):
+        assert pl.append(1, mix64(1000 + i))
+    while kv.evict_lru_large_page() is not None:
+        pass
+    assert pl.take_checkpoint_copies() == []  # its page left the cache: nothing to copy into
+    kv.check_invariants()

@@ -22,7 +22,8 @@ def apply_delta(buf, table, seq, slots):
     hdr[4] = hdr[3]  # ack, as the kernel does
     sl = buf[32:32 + 8 * rows].view(np.int64)
     sq = buf[32 + 8 * rows:32 + 12 * rows].view(np.int32)
-    rec = buf[32 + 12 * rows:32 + 12 * rows + 8 * nrec].view(np.int32).reshape(-1, 2)
+    r0 = 32 + 12 * rows + 4 * (rows & 1)  # records are 8-byte aligned
+    rec = buf[r0:r0 + 8 * nrec].view(np.int32).reshape(-1, 2)
     seq[:rows] = sq
     slots[:rows] = sl
     flat = table.reshape(-1)
