@@ -45,7 +45,10 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="gemma2-9b", choices=["gemma2-9b", "jamba-style", "llama-3.2-11b-vision"])
+    p.add_argument("--workload", default="gemma2-9b",
+                   choices=["gemma2-9b", "jamba-style", "llama-3.2-11b-vision", "prefix-mix"])
+    p.add_argument("--article", type=int, default=1024, help="prefix-mix: shared article tokens")
+    p.add_argument("--question", type=int, default=32, help="prefix-mix: question tokens (+U[0,16])")
     p.add_argument("--batch-per-gpu", type=int, default=0, help="0: the workload's default")
     p.add_argument("--ctx", type=int, default=8192)
     p.add_argument("--tpp", type=int, default=16)
@@ -125,7 +128,26 @@ class Workload:
         self.name = a.workload
         self.ctx = a.ctx
         self.image_tokens = 0
-        if a.workload == "gemma2-9b":
+        self.prefix_caching = False
+        if a.workload == "prefix-mix":
+            # BASELINE configs[4]: the reference's multi-article shape (trace.cpp:144-169) on the
+            # Gemma-2-9B geometry — every request's prompt = a shared article + a question;
+            # round 0 prefills cold and is released into the prefix cache, round 1 asks the
+            # next question of every article and adopts the cached article pages
+            self.geom = gemma2_9b(a.tpp)
+            for gg in self.geom.groups:
+                gg.num_layers = a.layers_per_group
+            self.B = a.batch_per_gpu or 256
+            L = a.layers_per_group
+            self.layers = [(g, l) for l in range(L) for g in (0, 1)]
+            self.prefix_caching = True
+            self.article, self.question, self.round0_output = a.article, a.question, 4
+            self.ctx = a.article + a.question + 16
+            self.desc = (f"prefix-mix (config 5) decode on gemma2-9b geometry: {self.B} req/GPU, prompts = "
+                         f"{a.article}-token shared article + {a.question}+U[0,16]-token question, round 1 "
+                         f"adopting round 0's cached article pages; {2 * L} layers ({L} full + {L} SWA-4096), "
+                         f"Hq=16 Hkv=8 D=256, tpp={a.tpp}, logit softcap {self.geom.softcap:g}")
+        elif a.workload == "gemma2-9b":
             self.geom = gemma2_9b(a.tpp)
             for gg in self.geom.groups:
                 gg.num_layers = a.layers_per_group
@@ -160,7 +182,8 @@ class Workload:
         self.spec = self.geom.spec()
 
     def max_tokens(self, steps):
-        return max(self.ctx + self.image_tokens + steps + 16, 64)
+        extra = self.round0_output if self.prefix_caching else 0
+        return max(self.ctx + self.image_tokens + steps + extra + 16, 64)
 
     def group_max_tokens(self, steps):
         """Per-group ordinal bounds: cross-attention groups store image
@@ -187,8 +210,95 @@ class Workload:
                 smalls = self.B * (math.ceil(min(gg.window, self.ctx + steps + 16) / tpp) + 2)
             else:
                 smalls = self.B * (math.ceil((self.ctx + steps + 16) / tpp) + 1)
+            if self.prefix_caching:  # round 0's cached prompts + round 1's own question / decode pages
+                smalls = self.B * (math.ceil((self.ctx + self.round0_output) / tpp) + 2 +
+                                   math.ceil((self.question + 16 + steps) / tpp) + 2)
             total += math.ceil(smalls / addr.slots_per_large(g)) + self.B  # request-aware units
         return total + 8
+
+    def prefix_prompts(self, ids, q_round):
+        """Article id = request id (one question per article per round)."""
+        out = []
+        for r in ids:
+            art = np.random.default_rng(1_000_003 * r + 17).integers(1, 1 << 40, self.article)
+            qr = np.random.default_rng(7919 * r + 31 * q_round + 5)
+            n = self.question + int(qr.integers(0, 17))
+            out.append([int(x) for x in art] + [int(x) for x in qr.integers(1, 1 << 40, n)])
+        return out
+
+    def prefix_setup(self, eng, ids, dev, chunk_requests=32):
+        """Rounds 0 and 1 of the prefix mix through the product path: admission
+        (lookup_and_pin + adoption), page lists, then per chunk of requests and
+        per layer slot_mapping + reshape_and_cache + tcgen05 paged_prefill of the
+        positions the hit did not cover.  Round 0 then decodes a few tokens and
+        is released with caching.  Returns hit rate and cold / warm TTFT."""
+        import torch
+
+        from paper_2503_18292_b200 import ops
+        g0 = self.geom.groups[0]
+        H, Hkv, D, tpp = g0.num_q_heads, g0.num_kv_heads, g0.head_dim, self.spec.groups[0].tokens_per_page
+        gen = torch.Generator(device=dev).manual_seed(11)
+        rows = {r: i for i, r in enumerate(eng.requests)}
+
+        def admit_round(q_round):
+            prompts = self.prefix_prompts(ids, q_round)
+            t0 = time.perf_counter()
+            hits = [eng.pages.admit(r, p, now=eng.now) for r, p in zip(ids, prompts)]
+            for r, p, h in zip(ids, prompts, hits):
+                n, oom = eng.pages.prefill(r, len(p) - h, now=eng.now)
+                assert not oom and n == len(p) - h, "arena too small for the prefix mix"
+            eng.sync_tables()
+            torch.cuda.synchronize()
+            host_ms = (time.perf_counter() - t0) * 1e3
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dev_ms = 0.0
+            for c0 in range(0, len(ids), chunk_requests):
+                part = list(range(c0, min(len(ids), c0 + chunk_requests)))
+                chunks = [len(prompts[i]) - hits[i] for i in part]
+                T = int(sum(chunks))
+                if T == 0:
+                    continue
+                b0 = rows[ids[part[0]]]
+                cu = torch.tensor(np.concatenate([[0], np.cumsum(chunks)]), dtype=torch.int32, device=dev)
+                req = torch.tensor(np.repeat(np.arange(len(part)), chunks), dtype=torch.int32, device=dev)
+                ords = torch.tensor(np.concatenate([np.arange(hits[i] + 1, len(prompts[i]) + 1) for i in part]),
+                                    dtype=torch.int32, device=dev)
+                q = torch.randn((T, H, D), generator=gen, device=dev).to(torch.bfloat16)
+                k = torch.randn((T, Hkv, D), generator=gen, device=dev).to(torch.bfloat16)
+                v = torch.randn_like(k)
+                out = torch.empty_like(q)
+                slots = torch.empty(T, dtype=torch.int64, device=dev)
+                torch.cuda.synchronize()
+                e0.record()
+                for g, gg in enumerate(self.geom.groups):
+                    t = eng.tables[g]
+                    bt = t.block_table[b0:b0 + len(part)]
+                    ops.slot_mapping(bt, t.max_blocks, req, ords, tpp, slots)
+                    for layer in range(gg.num_layers):
+                        view = eng.view(g, layer)
+                        ops.reshape_and_cache(eng.arena, view, k, v, slots, tpp)
+                        ops.paged_prefill(eng.arena, view, int(gg.kind), q, out, cu, max(chunks), bt,
+                                          t.seq_lens[b0:b0 + len(part)], Hkv, tpp, D ** -0.5, window=gg.window,
+                                          softcap=self.geom.softcap)
+                e1.record()
+                torch.cuda.synchronize()
+                dev_ms += e0.elapsed_time(e1)
+            return prompts, hits, host_ms, dev_ms
+
+        _, _, host0, dev0 = admit_round(0)
+        for _ in range(self.round0_output):  # round 0's answers (page lists only; KV values irrelevant here)
+            assert eng.append(ids) == len(ids)
+        eng.sync_tables()
+        for r in ids:
+            eng.pages.release(r, True, now=eng.now)
+        cached = eng.kv.cache_entries(0)
+        prompts1, hits1, host1, dev1 = admit_round(1)
+        eng.kv.check_invariants()
+        return {"hit_rate": round(sum(hits1) / sum(len(p) for p in prompts1), 4),
+                "cached_blocks_after_round0": int(cached),
+                "cold_ttft_ms": {"host_pages": round(host0, 2), "device_prefill": round(dev0, 2)},
+                "warm_ttft_ms": {"host_pages": round(host1, 2), "device_prefill": round(dev1, 2)},
+                "host_admission_us_per_request": round(host1 * 1e3 / len(ids), 1)}
 
     def prompt(self, eng, ids, rank):
         """Interleaved prompt: images first (cross groups store them), then text;
@@ -226,7 +336,7 @@ def run_ours(a, rank, world, local_rank):
     total_steps = (a.warmup + a.steps + max(3, a.steps // 4) + 8 +
                    (0 if a.no_e2e else a.warmup + a.steps + 4))
     eng = DecodeEngine(wl.geom, wl.arena_large_pages(total_steps), B, wl.max_tokens(total_steps), dev,
-                       group_max_tokens=wl.group_max_tokens(total_steps))
+                       group_max_tokens=wl.group_max_tokens(total_steps), prefix_caching=wl.prefix_caching)
     ids = shard_requests(list(range(B * world)), rank, world)  # this GPU's requests; its pool is private
     eng.add_requests(ids)
     t0 = time.time()
@@ -234,7 +344,11 @@ def run_ours(a, rank, world, local_rank):
     chunk = 1 << 30
     for s in range(0, av.numel(), chunk):
         av[s:s + chunk].normal_()
-    wl.prompt(eng, ids, rank)
+    prefix_stats = None
+    if wl.prefix_caching:
+        prefix_stats = wl.prefix_setup(eng, ids, dev)
+    else:
+        wl.prompt(eng, ids, rank)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
 
@@ -531,7 +645,7 @@ def run_ours(a, rank, world, local_rank):
         "warmup": a.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random N(0,1) bf16 KV/q; page lists from the "
                                                     "native Jenga allocator, seeded interleaved request order)",
-        "config": {"workload": wl.desc, "global_batch": B * world, "seq_len": a.ctx,
+        "config": {"workload": wl.desc, "global_batch": B * world, "seq_len": wl.ctx,
                    "parallelism": f"dp{world} (request shards, independent Jenga pool per GPU)",
                    "l2": "inputs larger than L2 (arena %.1f GB/GPU vs 126 MB L2); no flush needed"
                          % (eng.arena.nbytes / 1e9)},
@@ -555,6 +669,8 @@ def run_ours(a, rank, world, local_rank):
         res["verified"] = verification["verified"] and finite
     if st_bytes:
         res["mamba_state_bytes_per_step"] = int(st_bytes / a.steps)
+    if prefix_stats is not None:
+        res["prefix_mix"] = prefix_stats
     return res
 
 
@@ -759,7 +875,9 @@ def main():
         else:
             dist.init_process_group(backend)
     res = run_ours(a, rank, world, local_rank)
-    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.workload == "gemma2-9b":
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.workload in ("gemma2-9b", "prefix-mix"):
+        if a.workload == "prefix-mix":
+            a.ctx = a.article + a.question
         try:
             res["cpu_baseline"] = cpu_sample(a, steps=1, single_core=True)
         except Exception as e:  # the baseline must not sink the GPU line

@@ -317,8 +317,12 @@ int jenga_pages_pack_csr(const jenga_pages* pl, int g, const uint64_t* requests,
  * smaller than *used_bytes (reported either way).
  * ---------------------------------------------------------------------- */
 typedef struct jenga_table_mirror jenga_table_mirror;
-/* Bytes a delta buffer needs in the worst case (every row rewritten). */
+/* Bytes a delta buffer needs in the worst case (every row rewritten), and
+ * the bytes of a delta describing n_rows rows with n_records records (a
+ * caller copying only a fixed prefix of the buffer to the device each step
+ * sizes it with this and copies the whole used size when a pack needs more). */
 size_t jenga_delta_buffer_bytes(int max_batch, int max_blocks);
+size_t jenga_delta_bytes(int n_rows, int n_records);
 int jenga_table_mirror_create(const jenga_pages* pl, int g, int max_batch, int max_blocks,
                               jenga_table_mirror** out);
 void jenga_table_mirror_destroy(jenga_table_mirror* mirror);
@@ -355,17 +359,18 @@ int jenga_build_block_tables(const int32_t* offsets, const jenga_small_page* pag
 
 /* Apply a delta buffer from jenga_pages_pack_deltas to one group's table:
  * block_table[max_batch][max_blocks] entries, seq_lens[] and slot_mapping[]
- * (the newest stored ordinal's slot; -1 none) of the rows it describes.  The
- * kernel reads `delta` in place — pinned host memory (device-accessible
- * through unified addressing) or device memory — so no host->device copy is
- * issued, the record count may change every step, and the launch can be
- * captured in a CUDA graph that is replayed after each pack.  The launch
- * writes the buffer's sequence number back into its header; the next pack
- * reads it, and if its predecessor never reached the device (a buffer packed
- * and overwritten, or packed before a graph capture and not replayed) it
- * rewrites every row over the full table width.  The caller must not rewrite
- * `delta` before this launch has completed (record an event). */
-int jenga_upload_page_list_deltas(void* delta, int max_batch, int max_blocks,
+ * (the newest stored ordinal's slot; -1 none) of the rows it describes.
+ * `delta` is a device copy of the packed host buffer (the caller copies its
+ * used bytes; a fixed-size prefix copy plus an extra copy only when a pack
+ * outgrows it keeps the step capturable in a CUDA graph).  The launch writes
+ * the buffer's sequence number to `ack` — the host buffer's word 4, pinned
+ * memory the device stores to — so the next pack knows whether its
+ * predecessor reached the device; a pack whose predecessor never did (a
+ * buffer packed and overwritten, or packed before a graph capture and not
+ * replayed) rewrites every row over the full table width.  ack may be NULL
+ * (the next pack then always rewrites everything).  The host buffer must not
+ * be rewritten before the copy has read it (record an event). */
+int jenga_upload_page_list_deltas(const void* delta, int32_t* ack, int max_batch, int max_blocks,
                                   int32_t* block_table, int32_t* seq_lens,
                                   int64_t* slot_mapping, void* stream);
 

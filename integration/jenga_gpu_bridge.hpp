@@ -1,28 +1,3 @@
-# INTEGRATION — binding the reference API to the B200 path
-
-The reference exposes a C++20 API (`proj/include/jenga/*.hpp`) and no device code.
-This repository keeps that API as the host surface and puts the device behind the C ABI
-in `include/jenga_gpu.h`. There are two ways a maintainer plugs it in.
-
-## 1. Reference C++ engine → C ABI (what `SimEngine` would call)
-
-A reference-side worker keeps using `jenga::KvAllocator` / `AddressMap` / `LayerView`
-unchanged. The only new code is the header below, added next to the reference headers
-(`proj/include/jenga/`) and linked with `libjenga_b200.so`. It does four things:
-
-- it sizes one device arena from the allocator's LCM pool;
-- it turns the caller's per-request page lists into device block tables;
-- it launches decode through the reference's own `LayerView`;
-- it maps the ABI's status codes back onto the reference's exceptions (`util.hpp:11-21`).
-
-This file is compiled exactly as shown, against the unmodified reference headers and
-objects, by `oracle/build_oracle.py` (`oracle/_ref/libjenga_bridge_test.so`, harness
-`tests/bridge/bridge_harness.cpp`). `tests/test_gpu_bridge.py` then runs it on a B200.
-That test feeds the reference `KvAllocator`'s own page lists through
-`jenga_build_block_tables` and `jenga_paged_decode_append`, and checks the results against
-the C oracle. A CPU test asserts this document quotes the compiled file verbatim.
-
-```cpp
 // jenga_gpu_bridge.hpp — the reference-side binding of the B200 path.
 //
 // Added next to the reference headers (proj/include/jenga); compiled against
@@ -186,89 +161,3 @@ inline void decode_layer_append(const Arena& arena, const LayerView& v, LayerKin
 }
 
 }  // namespace jenga::gpu
-```
-
-Where each entry plugs into the reference:
-
-| C ABI entry | replaces / feeds | reference site |
-|---|---|---|
-| `jenga_arena_create(dev, pages, LCM)` | `LargePagePool(capacity, LCM)` backing memory | `lcm_allocator.cpp:7-19`, `kv_allocator.cpp:136-152` |
-| `jenga_pages_pack_csr` + `jenga_build_block_tables` | `GroupRuntime::blocks` → `AddressMap::global_page_index` | `simulator.hpp:123-139`, `memory_layout.cpp:22-27` |
-| `jenga_slot_mapping` | slot of `(request, ordinal)` | `store_position` `bidx`, `simulator.cpp:248-253` |
-| `jenga_reshape_and_cache(arena, LayerView, ...)` | writing the new token's K/V into its small page | `PAPER.md:834-838` (kernel interface) |
-| `jenga_paged_decode(arena, LayerView, kind, window, ...)` | attention over `needs_token` ordinals | `layer_policies.cpp:105-120` |
-| `jenga_paged_decode_append(arena, LayerView, kind, window, q, key, value, slot_mapping, ...)` | one decode step of a layer in one launch: the newest token's K/V written to its slot and attended (reshape_and_cache + paged_decode fused) | `simulator.cpp:549-566` (`decode_one` → `store_position`), `layer_policies.cpp:105-120` |
-| `jenga_mamba_state_gather/scatter` | Mamba working page | `simulator.cpp:222-230` |
-| `jenga_page_copy` | Mamba checkpoint snapshot / restore after a prefix hit | `simulator.cpp:231-242, 409-414` |
-| `jenga_pages_admit` (+ `_restore_pending`, `_finish_restore`) | `admit` → `lookup_and_pin` → `adopt_lookup_result` | `simulator.cpp:435-452, 391-433`, `kv_allocator.cpp:241-303` |
-| `jenga_pages_prefill`, `_set_defer_window_free`, `_apply_window_free` | `prefill_some`, `finish_prefill` (`suppress_window_free`) | `simulator.cpp:484-547` |
-| `jenga_paged_prefill(arena, LayerView, kind, window, ...)` | chunked-prefill attention (also the multi-token speculative verify) | `PAPER.md:834-838`, `simulator.cpp:504-547` |
-| `jenga_pages_set_vision_mode` | `EngineConfig::vision_mode` | `simulator.hpp:25-41`, `simulator.cpp:453-476, 525-542` |
-| `jenga_token_rows_scatter/gather` | vision-embedding bytes: the vision group's pages, or the full_reuse overlay into unwritten KV pages | `PAPER.md:1214-1242` |
-| `jenga_spec_combine_with_draft` | `combine_with_draft` | `simulator.cpp:32-41` |
-| `jenga_pages_speculative_decode`, `_rollback_newest` | `speculative_decode_one`, `rollback_newest` | `simulator.cpp:568-640` |
-
-Build: `python paper_2503_18292_b200/build.py` (or `__graft_entry__.build()`) produces
-`paper_2503_18292_b200/libjenga_b200.so` (host runtime + sm_100a kernels, static cudart,
-only `jenga_*` symbols exported). Link it and add `include/` to the include path.
-
-## 2. Python workers (vLLM-style) → ctypes
-
-`paper_2503_18292_b200/_lib.py` is the complete ctypes binding (every symbol of the
-header with its argtypes); `jenga.py` mirrors the reference classes (`ModelSpec`,
-`KvAllocator`, `AddressMap`, `PageLists`, `LayerPolicy` helpers) and `ops.py` takes
-torch tensors. A minimal stub a maintainer would add to a Python worker:
-
-```python
-import ctypes, torch
-from paper_2503_18292_b200 import ops, AddressMap, ModelSpec
-from paper_2503_18292_b200.engine import DecodeEngine
-from paper_2503_18292_b200.geometry import gemma2_9b
-
-eng = DecodeEngine(gemma2_9b(), num_large_pages=24000, max_batch=32, max_tokens=8704)
-eng.add_requests(range(32))
-# per decode step
-eng.append()                  # host allocator: store_position for every request
-eng.sync_tables()             # one pinned H2D of every group's page lists + device block tables
-for layer in range(21):
-    for g in (0, 1):          # full, sliding window: append the new token's K/V and attend, one launch
-        eng.decode_append(g, layer, q[g][layer], k_new[g][layer], v_new[g][layer], out[g][layer])
-        # (equivalently: eng.write_kv(g, layer, k, v); eng.decode(g, layer, q, out))
-```
-
-Chunked prefill with a prefix hit, through the same objects:
-
-```python
-hit = eng.pages.admit(rid, prompt_tokens)          # pins + adopts cached article pages
-eng.pages.set_defer_window_free(rid, True)          # the chunk needs its whole window
-n, oom = eng.pages.prefill(rid, chunk)              # page lists for the chunk
-eng.sync_tables()
-ops.slot_mapping(t.block_table, t.max_blocks, req, ords, tpp, slots)
-for layer in range(L):
-    ops.reshape_and_cache(eng.arena, eng.view(g, layer), k_chunk, v_chunk, slots, tpp)
-    ops.paged_prefill(eng.arena, eng.view(g, layer), kind, q_chunk, out, cu_q, chunk,
-                      t.block_table[:B], t.seq_lens[:B], hkv, tpp, scale, window=W)
-eng.pages.apply_window_free(rid)
-```
-
-Contract notes:
-* `arena_base` passed to `jenga_paged_decode` must be the base of an arena from
-  `jenga_arena_create` for the tensor-core path (the kernel builds one TMA tensor map
-  over the whole arena); other bases get the CUDA-core kernel.
-* The decode workspace (`jenga_paged_decode_workspace_size`) must be zeroed once; the
-  kernels re-arm their split tickets, so it can be reused across launches and CUDA-graph
-  replays.
-* The page-list object is single-owner and not thread-safe, like the reference
-  (`SPEC.md:170, 247`); independent engines may run concurrently (`SPEC.md:535`), one
-  per GPU.
-* `jenga_paged_prefill` runs on tcgen05 (`prefill_tc5.cu`) for bf16/fp16 with head_dim
-  64/128/256: CTA pairs (`cta_group::2`) at 256, ping-ponged CTA pairs (two query tiles
-  per CTA) at 128, one CTA per query block at 64. A/B knobs, read once per process:
-  `JENGA_PREFILL_PP=0` (plain pairs at 128), `JENGA_PREFILL_2SM=0` (single-CTA kernel
-  everywhere), `JENGA_PREFILL_TC5=0` (the mma.sync kernel, `prefill.cu`).
-* Decode knobs (A/B only): `JENGA_DECODE_TILES_PER_SPLIT`, `JENGA_DECODE_HEADS_PER_CTA`,
-  `JENGA_DECODE_KV_BOX=0` (2-D boxes), `JENGA_DECODE_PERSISTENT=1`, `JENGA_PDL=0`;
-  copies: `JENGA_COPY_CFG=chunk_kib,stages,ctas_per_sm`, `JENGA_COPY_L2_KEEP=0`.
-* Multi-token attention (prefill chunks, speculative verify) needs the keys its
-  earliest query sees: hold `jenga_pages_set_defer_window_free` across the chunk and
-  call `jenga_pages_apply_window_free` after the attention ran.

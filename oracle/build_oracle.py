@@ -2,6 +2,12 @@
 product package):
 
   oracle/_ref/liboracle.so    the plain-C restatement (jenga_oracle.c)
+  oracle/_ref/libjenga_bridge_test.so  the reference-side bridge
+                              (integration/jenga_gpu_bridge.hpp) compiled
+                              against the reference headers, with the
+                              reference objects and tests/bridge/
+                              bridge_harness.cpp, linked to the product
+                              library (tests/test_gpu_bridge.py);
   oracle/_ref/libjenga_ref.so the UNMODIFIED reference library compiled from
                               its own sources under /root/reference/proj/src
                               plus our extern "C" shim (ref_shim.cpp), when
@@ -86,9 +92,33 @@ def build_reference() -> Path | None:
     return out
 
 
+def build_bridge() -> Path | None:
+    """The INTEGRATION.md §1 bridge, compiled as a reference maintainer would:
+    against the reference headers, the reference objects (minus our shim) and
+    libjenga_b200.so (+ the CUDA runtime for its device buffers)."""
+    if build_reference() is None:
+        return None
+    root = HERE.parent
+    lib = root / "paper_2503_18292_b200" / "libjenga_b200.so"
+    cuda = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+    if not lib.exists() or not (cuda / "include" / "cuda_runtime_api.h").exists():
+        return None
+    out = OUT / "libjenga_bridge_test.so"
+    src = root / "tests" / "bridge" / "bridge_harness.cpp"
+    hdr = root / "integration" / "jenga_gpu_bridge.hpp"
+    objs = sorted(str(o) for o in (OUT / "obj").glob("*.o") if o.stem != "ref_shim")
+    if _stale(out, [src, hdr, root / "include" / "jenga_gpu.h", lib, *objs]):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-w", "-I", str(REF_INC), "-I", _json_dir(),
+              "-I", str(root / "integration"), "-I", str(root / "include"), "-I", str(cuda / "include"), str(src),
+              *objs, "-o", str(out), "-L", str(lib.parent), "-l:libjenga_b200.so", "-L", str(cuda / "lib64"),
+              "-lcudart", "-Wl,-rpath,$ORIGIN/../../paper_2503_18292_b200", f"-Wl,-rpath,{cuda / 'lib64'}"])
+    return out
+
+
 def build() -> None:
     build_c_oracle()
     build_reference()
+    build_bridge()
 
 
 if __name__ == "__main__":

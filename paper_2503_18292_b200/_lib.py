@@ -150,7 +150,8 @@ _SIGS = {
     "jenga_table_mirror_destroy": (None, [_p]),
     "jenga_table_mirror_reset": (_int, [_p]),
     "jenga_pages_pack_deltas": (_int, [_p, _pu64, _int, _p, C.c_size_t, C.POINTER(C.c_size_t), _pint]),
-    "jenga_upload_page_list_deltas": (_int, [_p, _int, _int, _p, _p, _p, _p]),
+    "jenga_upload_page_list_deltas": (_int, [_p, _p, _int, _int, _p, _p, _p, _p]),
+    "jenga_delta_bytes": (C.c_size_t, [_int, _int]),
     "jenga_arena_create": (_int, [_int, _u64, _u64, C.POINTER(_p)]),
     "jenga_arena_destroy": (None, [_p]),
     "jenga_arena_base": (_p, [_p]),

@@ -707,6 +707,11 @@ size_t records_offset(int n_rows) { return kDeltaHeader + static_cast<size_t>(n_
 size_t delta_bytes(int n_rows, size_t n_records) { return records_offset(n_rows) + n_records * 8; }
 }  // namespace
 
+JENGA_EXPORT size_t jenga_delta_bytes(int n_rows, int n_records) {
+  if (n_rows < 0 || n_records < 0) return 0;
+  return delta_bytes(n_rows, static_cast<size_t>(n_records));
+}
+
 JENGA_EXPORT size_t jenga_delta_buffer_bytes(int max_batch, int max_blocks) {
   if (max_batch < 0 || max_blocks < 0) return 0;
   // worst case: every row rewritten in full, twice its width (old + new length)

@@ -65,61 +65,50 @@ __global__ void __launch_bounds__(256) slot_mapping_kernel(const int32_t* __rest
   out[t] = slot;
 }
 
-// Apply a delta buffer (jenga_pages_pack_deltas) to one group's device table.
-// The buffer is read where it lies — pinned host memory is device-accessible
-// through unified addressing — with ld.global.cv (never a stale cached line),
-// so the number of records can change every step without a host->device copy
-// of its own, and a step that captures this launch in a CUDA graph replays it
-// with whatever the host packed last.
+// Apply a delta buffer (jenga_pages_pack_deltas) to one group's device table:
 //   [0] n_records [1] n_rows [2] max_blocks [3] seq [4] ack [5..7] 0 |
 //   int64 slots[n_rows] | int32 seq_lens[n_rows] (+1 pad if n_rows is odd) |
 //   int32 (flat entry, value)[n_records] (8-byte aligned)
-// The launch acknowledges the buffer by writing seq into word 4, which tells
-// the next pack that its predecessor reached the device.
-__global__ void __launch_bounds__(256) apply_deltas_kernel(int32_t* __restrict__ delta, int max_batch,
+// `delta` is device memory (a copy of the host buffer); the launch writes the
+// buffer's sequence number to `ack` (word 4 of the host buffer, pinned memory
+// the device can store to), which tells the next pack its predecessor landed.
+__global__ void __launch_bounds__(256) apply_deltas_kernel(const int32_t* __restrict__ delta,
+                                                            int32_t* __restrict__ ack, int max_batch,
                                                             int max_blocks, int32_t* __restrict__ table,
                                                             int32_t* __restrict__ seq_lens,
                                                             int64_t* __restrict__ slot_mapping) {
-  const int n_rec = __ldcv(delta);
-  const int n_rows = min(__ldcv(delta + 1), max_batch);
-  if (__ldcv(delta + 2) != max_blocks) return;  // a buffer packed for another table: leave it untouched
-  if (blockIdx.x == 0 && threadIdx.x == 0) __stcg(delta + 4, __ldcv(delta + 3));  // ack
+  const int n_rec = delta[0];
+  const int rows_packed = delta[1];
+  const int n_rows = min(rows_packed, max_batch);
+  if (delta[2] != max_blocks) return;  // a buffer packed for another table: leave it untouched
+  if (ack != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<volatile int32_t*>(ack) = delta[3];
   const int64_t entries = static_cast<int64_t>(max_batch) * max_blocks;
   const int64_t* slots = reinterpret_cast<const int64_t*>(delta + 8);
-  const int rows_packed = __ldcv(delta + 1);
   const int32_t* seqs = delta + 8 + 2 * rows_packed;
   const int2* rec = reinterpret_cast<const int2*>(seqs + rows_packed + (rows_packed & 1));
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += stride) {
-    if (seq_lens) seq_lens[i] = __ldcv(seqs + i);
-    if (slot_mapping) slot_mapping[i] = __ldcv(reinterpret_cast<const long long*>(slots) + i);
+    if (seq_lens) seq_lens[i] = seqs[i];
+    if (slot_mapping) slot_mapping[i] = slots[i];
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rec; i += stride) {
-    const int2 r = __ldcv(rec + i);
+    const int2 r = rec[i];
     if (r.x >= 0 && r.x < entries) table[r.x] = r.y;
   }
 }
 
 }  // namespace
 
-JENGA_EXPORT int jenga_upload_page_list_deltas(void* delta, int max_batch, int max_blocks,
+JENGA_EXPORT int jenga_upload_page_list_deltas(const void* delta, int32_t* ack, int max_batch, int max_blocks,
                                                int32_t* block_table, int32_t* seq_lens, int64_t* slot_mapping,
                                                void* stream) {
   using namespace jenga_dev;
   if (delta == nullptr || block_table == nullptr || max_batch < 0 || max_blocks <= 0 ||
       reinterpret_cast<uintptr_t>(delta) % 8 != 0)
     return set_error(JENGA_ERR_ARG, "jenga_upload_page_list_deltas: invalid arguments");
-  cudaPointerAttributes attr{};
-  if (cudaPointerGetAttributes(&attr, delta) != cudaSuccess || attr.type == cudaMemoryTypeUnregistered) {
-    cudaGetLastError();
-    return set_error(JENGA_ERR_ARG, "jenga_upload_page_list_deltas: delta must be pinned host or device memory");
-  }
-  const int32_t packed_width = attr.type == cudaMemoryTypeHost ? static_cast<const int32_t*>(delta)[2] : 0;
-  if (packed_width != 0 && packed_width != max_blocks)
-    return set_error(JENGA_ERR_ARG, "jenga_upload_page_list_deltas: buffer packed for another table width");
   if (max_batch == 0) return JENGA_OK;
   apply_deltas_kernel<<<4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<int32_t*>(delta), max_batch, max_blocks, block_table, seq_lens, slot_mapping);
+      static_cast<const int32_t*>(delta), ack, max_batch, max_blocks, block_table, seq_lens, slot_mapping);
   note_launch(static_cast<cudaStream_t>(stream), kLaunchSerializing);
   return check_launch("apply_deltas_kernel");
 }

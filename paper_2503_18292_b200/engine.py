@@ -34,9 +34,13 @@ class GroupTables:
     seq_lens: torch.Tensor         # int32 [max_batch]
     slot_mapping: torch.Tensor     # int64 [max_batch] (newest ordinal of each request)
     h_n_stored: torch.Tensor       # int32 [max_batch], host copy of seq_lens as last packed
-    # upload="delta": table mirror + pinned delta buffer read in place by the device
+    # upload="delta": table mirror, pinned delta buffer and its device copy; every
+    # upload copies the fixed prefix `delta_window` (sized for a decode step),
+    # pack_tables copies the rest when a pack outgrows it
     mirror: Optional[TableMirror] = None
     h_delta: Optional[torch.Tensor] = None
+    d_delta: Optional[torch.Tensor] = None
+    delta_window: int = 0
     # upload="full": CSR page lists, pinned + device mirror
     h_offsets: Optional[torch.Tensor] = None
     h_pages: Optional[torch.Tensor] = None
@@ -101,8 +105,11 @@ class DecodeEngine:
                 h_n_stored=torch.zeros(max_batch, dtype=torch.int32))
             if upload == "delta":
                 t.mirror = TableMirror(self.pages, g, max_batch, max_blocks)
-                t.h_delta = torch.zeros(TableMirror.buffer_bytes(max_batch, max_blocks), dtype=torch.uint8,
-                                        pin_memory=True)
+                full = TableMirror.buffer_bytes(max_batch, max_blocks)
+                t.h_delta = torch.zeros(full, dtype=torch.uint8, pin_memory=True)
+                t.d_delta = torch.zeros(full, dtype=torch.uint8, device=self.device)
+                # a decode step changes <= 2 entries per row (appended block, freed window block)
+                t.delta_window = min(full, TableMirror.delta_bytes(max_batch, 4 * max_batch))
             else:
                 def carve(buf, b0=base, mb=max_blocks):
                     o = b0
@@ -160,7 +167,9 @@ class DecodeEngine:
         for g in (range(len(self.tables)) if groups is None else groups):
             t = self.tables[g]
             if self.upload == "delta":
-                _, nrec = t.mirror.pack(self._req_arr[:n], t.h_delta.data_ptr(), t.h_delta.numel())
+                used, nrec = t.mirror.pack(self._req_arr[:n], t.h_delta.data_ptr(), t.h_delta.numel())
+                if used > t.delta_window:  # outgrew the per-step copy: ship the rest now (stream-ordered)
+                    t.d_delta[:used].copy_(t.h_delta[:used], non_blocking=True)
                 rows = int(t.h_delta[4:8].view(torch.int32).item())
                 seq = TableMirror.seq_lens_view(t.h_delta.numpy(), rows)
                 t.h_n_stored[:rows] = torch.from_numpy(seq.copy())
@@ -177,9 +186,9 @@ class DecodeEngine:
         return totals
 
     def upload_tables(self, groups: Optional[Sequence[int]] = None, totals: Optional[Dict[int, int]] = None) -> None:
-        """Device half.  delta: one apply launch per group reading its pinned
-        delta buffer in place (no copy).  full: one pinned -> device copy of the
-        CSR staging buffer, then the block-table build per group.  Fixed launch
+        """Device half.  delta: per group one pinned -> device copy of the
+        delta window and one apply launch.  full: one pinned -> device copy of
+        the CSR staging buffer, then the block-table build per group.  Fixed launch
         shapes either way, so the step can be captured in a CUDA graph and
         replayed after each pack_tables.  `totals` is accepted for API
         symmetry with pack_tables."""
@@ -189,8 +198,9 @@ class DecodeEngine:
         if self.upload == "delta":
             for g in gs:
                 t = self.tables[g]
-                ops.upload_page_list_deltas(t.h_delta, self.max_batch, t.max_blocks, t.block_table, t.seq_lens,
-                                            t.slot_mapping)
+                t.d_delta[: t.delta_window].copy_(t.h_delta[: t.delta_window], non_blocking=True)
+                ops.upload_page_list_deltas(t.d_delta, TableMirror.ack_ptr(t.h_delta.data_ptr()), self.max_batch,
+                                            t.max_blocks, t.block_table, t.seq_lens, t.slot_mapping)
             self._h2d_done.record(cur)
             return
         self._d_stage.copy_(self._h_stage, non_blocking=True)
@@ -203,9 +213,9 @@ class DecodeEngine:
 
     def upload_bytes(self, totals: Dict[int, int]) -> int:
         """Host->device page-list bytes of one upload (the bytes the device reads)."""
-        n = len(self.requests)
         if self.upload == "delta":
-            return sum(32 + 12 * n + 4 * (n & 1) + 8 * nrec for nrec in totals.values())
+            return sum(max(t.delta_window, TableMirror.delta_bytes(self.max_batch, totals.get(g, 0)))
+                       for g, t in enumerate(self.tables) if g in totals)
         return int(self._h_stage.numel() * 4)
 
     # ------------------------------------------------------------ per layer ops

@@ -584,6 +584,15 @@ class TableMirror:
     def buffer_bytes(max_batch: int, max_blocks: int) -> int:
         return int(lib.jenga_delta_buffer_bytes(max_batch, max_blocks))
 
+    @staticmethod
+    def delta_bytes(rows: int, records: int) -> int:
+        return int(lib.jenga_delta_bytes(rows, records))
+
+    @staticmethod
+    def ack_ptr(buf_ptr: int) -> int:
+        """Where the applying launch acknowledges the buffer (header word 4)."""
+        return buf_ptr + 16
+
     def reset(self) -> None:
         check(lib.jenga_table_mirror_reset(self.h))
 

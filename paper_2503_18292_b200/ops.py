@@ -88,17 +88,16 @@ def build_block_tables(offsets: torch.Tensor, pages: torch.Tensor, first_live: t
                                        _ptr(slot_mapping), _ptr(seq_lens), _stream()))
 
 
-def upload_page_list_deltas(delta: torch.Tensor, max_batch: int, max_blocks: int, block_table: torch.Tensor,
-                            seq_lens: Optional[torch.Tensor] = None,
+def upload_page_list_deltas(delta: torch.Tensor, ack_ptr: Optional[int], max_batch: int, max_blocks: int,
+                            block_table: torch.Tensor, seq_lens: Optional[torch.Tensor] = None,
                             slot_mapping: Optional[torch.Tensor] = None) -> None:
-    """Apply a delta buffer (TableMirror.pack; pinned host or device memory,
-    read in place by the kernel) to one group's device table."""
-    if delta.device.type == "cpu" and not delta.is_pinned():
-        raise ValueError("delta buffer must be pinned host memory or on the device")
+    """Apply a delta buffer (TableMirror.pack, copied to the device) to one
+    group's device table; the launch acknowledges it at ack_ptr (the pinned
+    host buffer's header word 4, TableMirror.ack_ptr)."""
     _need(block_table, torch.int32, "block_table")
     if block_table.numel() < max_batch * max_blocks:
         raise ValueError("block_table too small")
-    check(lib.jenga_upload_page_list_deltas(delta.data_ptr(), max_batch, max_blocks, _ptr(block_table),
+    check(lib.jenga_upload_page_list_deltas(_ptr(delta), ack_ptr, max_batch, max_blocks, _ptr(block_table),
                                             _ptr(seq_lens), _ptr(slot_mapping), _stream()))
 
 
