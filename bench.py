@@ -59,6 +59,14 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly instead of one CUDA graph "
                                                           "per step")
     p.add_argument("--layers-per-group", type=int, default=21)
+    p.add_argument("--softcap", type=float, default=None, help="attention-logit soft cap (default: the model's; "
+                                                               "Gemma-2: 50)")
+    p.add_argument("--mamba-mode", default="fused-step", choices=["fused-step", "per-layer", "gather-scatter"],
+                   help="jamba-style: how a step moves the Mamba states through the page table — one in-place "
+                        "update launch for all Mamba layers (fused-step), one per layer in model order "
+                        "(per-layer), or the unfused gather -> dense -> scatter pair per layer (gather-scatter)")
+    p.add_argument("--mamba-decay", type=float, default=0.999,
+                   help="stand-in SSM update of the in-place modes: fp32 state *= decay")
     return p.parse_args()
 
 
@@ -129,6 +137,8 @@ class Workload:
         self.ctx = a.ctx
         self.image_tokens = 0
         self.prefix_caching = False
+        from paper_2503_18292_b200.geometry import gemma2_9b as _g
+        gemma2_9b = (lambda tpp: _g(tpp, softcap=a.softcap)) if a.softcap is not None else _g
         if a.workload == "prefix-mix":
             # BASELINE configs[4]: the reference's multi-article shape (trace.cpp:144-169) on the
             # Gemma-2-9B geometry — every request's prompt = a shared article + a question;
@@ -165,7 +175,11 @@ class Workload:
                 self.layers += [(1, 7 * i + j) for j in range(7)]
             self.desc = (f"jamba-style hybrid decode: {self.B} req/GPU x {a.ctx} ctx, 4 attention layers (Hq=32 Hkv=8 "
                          f"D=128 bf16, tpp={a.tpp}) + 28 Mamba layers with fp32 last-token state pages "
-                         f"(622,592 B/layer) in the same LCM pool; state gathered and scattered per layer")
+                         f"(622,592 B/layer) in the same LCM pool; state traffic: " +
+                         {"fused-step": "one in-place update launch per step for all 28 Mamba layers (state read "
+                                        "+ written back through the page table, fp32 *= decay as the SSM stand-in)",
+                          "per-layer": "one in-place update launch per Mamba layer in model order",
+                          "gather-scatter": "per layer, gather to a dense buffer then scatter back"}[a.mamba_mode])
         elif a.workload == "llama-3.2-11b-vision":
             self.geom = llama32_11b_vision(a.tpp)
             self.B = a.batch_per_gpu or 64
@@ -363,7 +377,7 @@ def run_ours(a, rank, world, local_rank):
     vn = torch.randn((na, B, Hkv, D), generator=gen, device=dev).to(g0.dtype)
     out = torch.empty_like(q)
     state = None
-    if mamba:
+    if mamba and a.mamba_mode == "gather-scatter":
         state = torch.empty((B, eng.view(mamba[0][1], 0).exec_page_size), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     bptl = 2 * Hkv * D * 2
@@ -392,11 +406,18 @@ def run_ours(a, rank, world, local_rank):
             if kind != LayerKind.kMamba and not attention:
                 continue
             if kind == LayerKind.kMamba:
-                if g not in pg:
+                first = g not in pg
+                if first:
                     pg[g] = eng.mamba_page_globals(g)
                 v = eng.view(g, l)
-                ops.mamba_state_gather(eng.arena, v, pg[g], state)   # last-token state -> dense
-                ops.mamba_state_scatter(eng.arena, v, pg[g], state)  # (SSM update out of scope)
+                if a.mamba_mode == "gather-scatter":
+                    ops.mamba_state_gather(eng.arena, v, pg[g], state)   # last-token state -> dense
+                    ops.mamba_state_scatter(eng.arena, v, pg[g], state)  # (SSM update out of scope)
+                elif a.mamba_mode == "per-layer":
+                    ops.mamba_state_update(eng.arena, v, 1, pg[g], a.mamba_decay)
+                elif first:  # fused-step: every Mamba layer of the group in one launch
+                    ops.mamba_state_update(eng.arena, eng.view(g, 0), eng.tables[g].geom.num_layers, pg[g],
+                                           a.mamba_decay)
                 continue
             j = slot[i]
             if hooks is not None:
@@ -876,6 +897,8 @@ def main():
             dist.init_process_group(backend)
     res = run_ours(a, rank, world, local_rank)
     if rank == 0 and world == 1 and not a.no_cpu_baseline and a.workload in ("gemma2-9b", "prefix-mix"):
+        from paper_2503_18292_b200.geometry import gemma2_9b as _g
+        gemma2_9b = (lambda tpp: _g(tpp, softcap=a.softcap)) if a.softcap is not None else _g
         if a.workload == "prefix-mix":
             a.ctx = a.article + a.question
         try:

@@ -445,6 +445,17 @@ int jenga_mamba_state_gather(const void* arena_base, jenga_layer_view view,
 int jenga_mamba_state_scatter(void* arena_base, jenga_layer_view view,
                               const int64_t* page_globals, int batch, const void* dense,
                               void* stream);
+/* The fused form of gather -> SSM update -> scatter (as jenga_paged_decode_append
+ * is of reshape_and_cache + paged_decode): layers [l, l + num_layers) of every
+ * request's working page — view = layer l's LayerView; the slices are one
+ * contiguous run of num_layers * exec_page_size bytes per page — are read
+ * through the page table and written back in place, each fp32 state element
+ * multiplied by `decay` (the stand-in for the selective-scan state update,
+ * whose math is out of scope; decay = 1 moves the bytes unchanged).  No dense
+ * staging buffer: HBM traffic is exactly the state read + write.
+ * page_globals[b] < 0 skips.  The state bytes must be fp32 (decay != 1). */
+int jenga_mamba_state_update(void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                             const int64_t* page_globals, int batch, float decay, void* stream);
 /* Token rows <-> pages (vision-embedding pages, simulator.cpp:453-476,
  * 525-542).  Row t (row_bytes, row_stride_bytes apart)
  * of the token at slot_mapping[t] = page_global*tpp + off (negative = skip;

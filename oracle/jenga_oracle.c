@@ -369,6 +369,21 @@ int orc_mamba_scatter(uint8_t* arena, uint64_t start_offset, uint64_t page_strid
   return ORC_OK;
 }
 
+/* In-place state step over layers [l0, l0 + num_layers) of each request's
+ * working page: the layers' slices are one contiguous run (page-layer layout,
+ * memory_layout.cpp:29-55); every fp32 state element is multiplied by decay
+ * (the stand-in for the selective-scan update, whose math is out of scope). */
+int orc_mamba_update(uint8_t* arena, uint64_t start_offset, uint64_t page_stride, uint64_t exec_bytes,
+                     uint32_t num_layers, const int64_t* page_globals, int batch, float decay) {
+  const uint64_t n = exec_bytes * num_layers / 4;
+  for (int b = 0; b < batch; ++b) {
+    if (page_globals[b] < 0) continue;
+    float* s = (float*)(arena + start_offset + page_globals[b] * page_stride);
+    for (uint64_t i = 0; i < n; ++i) s[i] = s[i] * decay;
+  }
+  return ORC_OK;
+}
+
 /* Checkpoint snapshot (simulator.cpp:231-242): whole small page copy. */
 int orc_page_copy(uint8_t* arena, uint64_t small_page_bytes, const int64_t* src, const int64_t* dst, int n) {
   for (int i = 0; i < n; ++i) {

@@ -47,6 +47,7 @@ class COracle:
         L.orc_mamba_gather.argtypes = [_p, _u64, _u64, _u64, _p, _int, _p]
         L.orc_mamba_scatter.argtypes = [_p, _u64, _u64, _u64, _p, _int, _p]
         L.orc_page_copy.argtypes = [_p, _u64, _p, _p, _int]
+        L.orc_mamba_update.argtypes = [_p, _u64, _u64, _u64, _u32, _p, _int, C.c_float]
         for f in (L.orc_token_rows_scatter, L.orc_token_rows_gather):
             f.argtypes = [_p, _u64, _u64, _u64, _u32, _u32, _u32, _p, _u64, C.c_int64, _p, _int]
 
@@ -144,6 +145,11 @@ class COracle:
         dense = np.ascontiguousarray(dense, dtype=np.uint8)
         self._ok(self.lib.orc_mamba_scatter(arena.ctypes.data_as(_p), view[0], view[1], view[2], pp, len(pg),
                                             dense.ctypes.data_as(_p)))
+
+    def mamba_update(self, arena, view, num_layers, page_globals, decay):
+        pg, pp = _np(page_globals, np.int64)
+        self._ok(self.lib.orc_mamba_update(arena.ctypes.data_as(_p), view[0], view[1], view[2], num_layers, pp,
+                                           len(pg), C.c_float(decay)))
 
     def page_copy(self, arena, small_page_bytes, src, dst):
         s, sp = _np(src, np.int64)

@@ -169,6 +169,7 @@ _SIGS = {
     "jenga_mamba_state_gather": (_int, [_p, LayerViewC, _p, _int, _p, _p]),
     "jenga_mamba_state_scatter": (_int, [_p, LayerViewC, _p, _int, _p, _p]),
     "jenga_page_copy": (_int, [_p, _u64, _p, _p, _int, _p]),
+    "jenga_mamba_state_update": (_int, [_p, LayerViewC, _u32, _p, _int, C.c_float, _p]),
     "jenga_token_rows_scatter": (_int, [_p, LayerViewC, _u32, _u32, _u32, _u32, _p, _u64, C.c_int64, _p, _int, _p]),
     "jenga_token_rows_gather": (_int, [_p, LayerViewC, _u32, _u32, _u32, _u32, _p, _u64, C.c_int64, _p, _int, _p]),
     "jenga_kernel_launch_count": (_u64, []),

@@ -106,6 +106,7 @@ struct CopyArgs {
   uint64_t nvec;  // 16-byte units per item
   int n;
   int src_keep, dst_keep;  // 1: L2 evict_last (a dense staging buffer reused next kernel), 0: evict_first
+  float scale;     // kScale kernels: every fp32 element is multiplied by it on the way through
 };
 
 struct CopyChunk {
@@ -143,19 +144,23 @@ __device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, u
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
 
-template <int kCopyChunk, int kCopyStages>
+template <int kCopyChunk, int kCopyStages, bool kScale>
 __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ uint64_t full[kCopyStages];
   // PDL: the next kernel may get resident; our reads/writes wait for the previous one.
   jenga_dev::pdl_launch_dependents();
-  if (threadIdx.x != 0) return;
+  if (!kScale && threadIdx.x != 0) return;
   const uint64_t total = a.nvec * static_cast<uint64_t>(a.n);
   uint64_t pos = total * blockIdx.x / gridDim.x;
   const uint64_t hi = total * (blockIdx.x + 1) / gridDim.x;
   if (pos >= hi) return;
-  for (int i = 0; i < kCopyStages; ++i) jenga_dev::mbar_init(&full[i], 1);
-  jenga_dev::fence_mbar_init();
+  const bool leader = threadIdx.x == 0;
+  if (leader) {
+    for (int i = 0; i < kCopyStages; ++i) jenga_dev::mbar_init(&full[i], 1);
+    jenga_dev::fence_mbar_init();
+  }
+  if (kScale) __syncwarp();
   jenga_dev::pdl_wait();
   // arena pages stream through L2 once; a dense staging buffer (Mamba state
   // between gather, the SSM update and scatter) is kept resident
@@ -164,13 +169,17 @@ __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
   CopyChunk ring_c[kCopyStages];
   int issued = 0;
   bool more = true;
+  // every lane walks the same chunk sequence (the scale needs all 32 of them);
+  // only the leader issues the bulk copies
   auto issue = [&](int j) {
     CopyChunk c;
     if (!next_copy_chunk<kCopyChunk>(a, pos, hi, c)) return false;
     const int st = j % kCopyStages;
     ring_c[st] = c;
-    jenga_dev::mbar_arrive_expect_tx(&full[st], c.bytes);
-    jenga_dev::bulk_g2s_evict_first(ring + st * kCopyChunk, c.s, c.bytes, &full[st], src_pol);
+    if (leader) {
+      jenga_dev::mbar_arrive_expect_tx(&full[st], c.bytes);
+      jenga_dev::bulk_g2s_evict_first(ring + st * kCopyChunk, c.s, c.bytes, &full[st], src_pol);
+    }
     return true;
   };
   for (; issued < kCopyStages && (more = issue(issued)); ++issued) {
@@ -178,14 +187,30 @@ __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
   for (int k = 0; k < issued; ++k) {
     const int st = k % kCopyStages;
     jenga_dev::mbar_wait(&full[st], (k / kCopyStages) & 1);
-    bulk_s2g(ring_c[st].d, ring + st * kCopyChunk, ring_c[st].bytes, dst_pol);
+    if (kScale) {
+      float4* f = reinterpret_cast<float4*>(ring + st * kCopyChunk);
+      for (uint32_t i = threadIdx.x; i < ring_c[st].bytes / 16; i += 32) {
+        float4 x = f[i];
+        x.x *= a.scale;
+        x.y *= a.scale;
+        x.z *= a.scale;
+        x.w *= a.scale;
+        f[i] = x;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> bulk-copy reads
+      __syncwarp();
+    }
+    if (leader) {
+      bulk_s2g(ring_c[st].d, ring + st * kCopyChunk, ring_c[st].bytes, dst_pol);
+      if (k >= 1 && more) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+    }
     if (k >= 1 && more) {
       // chunk k-1's store has read its stage: refill it with chunk k-1+kCopyStages
-      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      if (kScale) __syncwarp();
       if ((more = issue(issued))) ++issued;
     }
   }
-  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // Token rows <-> pages.  Row t (row_bytes) of the token at slot s = page*tpp +
@@ -253,10 +278,10 @@ int launch_token_rows(bool scatter, void* arena_base, jenga_layer_view view, uin
   return check_launch(scatter ? "token_rows_kernel<scatter>" : "token_rows_kernel<gather>");
 }
 
-template <int CHUNK, int STAGES>
+template <int CHUNK, int STAGES, bool kScale = false>
 int launch_copy(const CopyArgs& args, int ctas_per_sm, void* stream, const char* what) {
   constexpr int smem = CHUNK * STAGES;
-  auto kern = paged_copy_kernel<CHUNK, STAGES>;
+  auto kern = paged_copy_kernel<CHUNK, STAGES, kScale>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = jenga_decode::configure_smem(kern, smem, configured)) return rc;
   // enough CTAs to fill every SM, none without at least one chunk of work
@@ -270,7 +295,8 @@ int launch_copy(const CopyArgs& args, int ctas_per_sm, void* stream, const char*
 
 int launch_paged_copy(const void* src_base, uint64_t src_off, uint64_t src_stride, const int64_t* src_idx,
                       void* dst_base, uint64_t dst_off, uint64_t dst_stride, const int64_t* dst_idx,
-                      uint64_t bytes, int n, void* stream, const char* what, int src_keep, int dst_keep) {
+                      uint64_t bytes, int n, void* stream, const char* what, int src_keep, int dst_keep,
+                      const float* scale = nullptr) {
   using namespace jenga_dev;
   if (n <= 0 || bytes == 0) return JENGA_OK;
   if (bytes % 16 != 0 || src_off % 16 != 0 || dst_off % 16 != 0 || src_stride % 16 != 0 ||
@@ -278,7 +304,9 @@ int launch_paged_copy(const void* src_base, uint64_t src_off, uint64_t src_strid
     return set_error(JENGA_ERR_UNSUPPORTED, std::string(what) + ": sizes/offsets must be 16-byte multiples");
   const CopyArgs args{static_cast<const uint8_t*>(src_base), src_off, src_stride, src_idx,
                       static_cast<uint8_t*>(dst_base), dst_off, dst_stride, dst_idx, bytes / 16, n,
-                      src_keep, dst_keep};
+                      src_keep, dst_keep, scale ? *scale : 1.f};
+  if (scale != nullptr && *scale != 1.f)
+    return launch_copy<kCopyChunkBytes, kCopyStages, true>(args, kCopyCtasPerSm, stream, what);
   return launch_copy<kCopyChunkBytes, kCopyStages>(args, kCopyCtasPerSm, stream, what);
 }
 
@@ -332,6 +360,20 @@ JENGA_EXPORT int jenga_mamba_state_scatter(void* arena_base, jenga_layer_view vi
   return launch_paged_copy(dense, 0, view.exec_page_size, nullptr, arena_base, view.start_offset,
                            view.page_stride, page_globals, view.exec_page_size, batch, stream,
                            "mamba_state_scatter", 1, 0);
+}
+
+JENGA_EXPORT int jenga_mamba_state_update(void* arena_base, jenga_layer_view view, uint32_t num_layers,
+                                          const int64_t* page_globals, int batch, float decay, void* stream) {
+  if (num_layers == 0 || view.exec_page_size % 16 != 0)
+    return jenga_dev::set_error(JENGA_ERR_ARG, "jenga_mamba_state_update: invalid arguments");
+  if (static_cast<uint64_t>(num_layers) * view.exec_page_size > view.page_stride)
+    return jenga_dev::set_error(JENGA_ERR_CONFIG, "jenga_mamba_state_update: layers beyond the small page");
+  // the layers' slices of one page are contiguous: one run per request, read
+  // and written back in place through the same addresses
+  const uint64_t run = static_cast<uint64_t>(num_layers) * view.exec_page_size;
+  return launch_paged_copy(arena_base, view.start_offset, view.page_stride, page_globals, arena_base,
+                           view.start_offset, view.page_stride, page_globals, run, batch, stream,
+                           "mamba_state_update", 0, 0, &decay);
 }
 
 JENGA_EXPORT int jenga_page_copy(void* arena_base, uint64_t small_page_bytes, const int64_t* src_globals,

@@ -245,6 +245,15 @@ def mamba_state_scatter(arena: Arena, view: LayerView, page_globals: torch.Tenso
                                         _ptr(dense), _stream()))
 
 
+def mamba_state_update(arena: Arena, view: LayerView, num_layers: int, page_globals: torch.Tensor,
+                       decay: float = 1.0) -> None:
+    """In-place state step of layers [l, l + num_layers) (view = layer l) of
+    every request's working page (jenga_mamba_state_update)."""
+    _need(page_globals, torch.int64, "page_globals")
+    check(lib.jenga_mamba_state_update(arena.base, view.c(), num_layers, _ptr(page_globals), page_globals.numel(),
+                                       decay, _stream()))
+
+
 def page_copy(arena: Arena, small_page_bytes: int, src_globals: torch.Tensor, dst_globals: torch.Tensor) -> None:
     _need(src_globals, torch.int64, "src_globals")
     _need(dst_globals, torch.int64, "dst_globals")

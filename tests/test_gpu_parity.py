@@ -369,3 +369,32 @@ def test_delta_upload_matches_full_rebuild():
             assert torch.equal(a.block_table, b.block_table), (step, g)
             assert torch.equal(a.seq_lens, b.seq_lens) and torch.equal(a.slot_mapping, b.slot_mapping), (step, g)
             assert torch.equal(a.h_n_stored, b.h_n_stored)
+
+
+@pytest.mark.parametrize("decay,l0,nl", [(1.0, 0, 28), (0.5, 3, 7), (0.9375, 27, 1)])
+def test_mamba_state_update_in_place(orc, decay, l0, nl):
+    """jenga_mamba_state_update — the fused gather -> SSM stand-in -> scatter:
+    layers [l0, l0 + nl) of each working page (one contiguous run per page)
+    read and written back in place through the page table, fp32 state scaled
+    by `decay`; every other byte of the arena untouched (C oracle
+    orc_mamba_update on a host copy); index -1 skipped.  Jamba state size."""
+    geom = ModelGeometry("hyb", [
+        GroupGeometry("attn", LayerKind.kFullAttention, 1, 8, 32, 128, torch.bfloat16, 16),
+        GroupGeometry("ssm", LayerKind.kMamba, 28, state_bytes=(8192 * 3 + 8192 * 16) * 4)])
+    lens = [3, 1, 2, 5, 1, 4, 2]
+    eng, ids = make_engine(geom, lens, poison=False)
+    g = 1
+    pg = eng.mamba_page_globals(g).clone()
+    pg[3] = -1
+    at = eng.arena.tensor()
+    at.view(torch.float32).normal_(generator=torch.Generator(device=eng.device).manual_seed(5))
+    before = arena_host(eng).copy()
+    view = eng.view(g, l0)
+    ops.mamba_state_update(eng.arena, view, nl, pg, decay)
+    torch.cuda.synchronize()
+    want = before.copy()
+    orc.mamba_update(want, tuple(view), nl, pg.cpu().numpy(), decay)
+    got = arena_host(eng)
+    np.testing.assert_array_equal(got, want)
+    if decay != 1.0:
+        assert not np.array_equal(got, before)
