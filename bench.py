@@ -61,7 +61,7 @@ def parse():
     p.add_argument("--layers-per-group", type=int, default=21)
     p.add_argument("--softcap", type=float, default=None, help="attention-logit soft cap (default: the model's; "
                                                                "Gemma-2: 50)")
-    p.add_argument("--mamba-mode", default="fused-step", choices=["fused-step", "per-layer", "gather-scatter"],
+    p.add_argument("--mamba-mode", default="per-layer", choices=["per-layer", "fused-step", "gather-scatter"],
                    help="jamba-style: how a step moves the Mamba states through the page table — one in-place "
                         "update launch for all Mamba layers (fused-step), one per layer in model order "
                         "(per-layer), or the unfused gather -> dense -> scatter pair per layer (gather-scatter)")
