@@ -82,5 +82,30 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines) -> Path:
+    """A profiling-only copy of the library with compile-time defines (e.g. a
+    decode split policy), at paper_2503_18292_b200/variants/libjenga_b200_<name>.so;
+    load it with JENGA_B200_LIB=<path>.  The product build is untouched."""
+    build()
+    host, dev, headers = _sources()
+    vdir = ROOT / "build" / "variants" / name
+    vdir.mkdir(parents=True, exist_ok=True)
+    flags = [f"-D{d}" for d in defines]
+    objs = []
+    for src in dev:
+        obj = vdir / (src.stem + ".cu.o")
+        _compile([NVCC, *NVCC_FLAGS, *flags, "-c", str(src), "-o", str(obj)], None)
+        objs.append(obj)
+    objs += [BUILD / (src.stem + ".o") for src in host]
+    out = PKG / "variants" / f"libjenga_b200_{name}.so"
+    out.parent.mkdir(exist_ok=True)
+    _compile([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(out), *map(str, objs),
+              "-Xlinker", "--exclude-libs,ALL"], None)
+    return out
+
+
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":  # --variant NAME DEFINE...
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        build(verbose=True, force="--force" in sys.argv)

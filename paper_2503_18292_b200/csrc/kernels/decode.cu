@@ -310,6 +310,34 @@ int tiles_per_split(int head_dim) {
   return head_dim >= 256 ? kTilesPerSplit : 96 * 128 / std::max(head_dim, 16);
 }
 
+// Wave-aware split count for the tensor-core kernel (three CTAs per SM).  With
+// requests of similar length the (KV head, request, split) CTAs finish in
+// ceil(CTAs / slots) rounds, so a split count that leaves the last round
+// mostly empty wastes up to a round; the launcher picks the split count s
+// minimising rounds(s) x (tiles per CTA(s) + per-CTA overhead), never below
+// kMinTilesPerSplit tiles per CTA (the workspace granularity).  The overhead
+// (prologue, ring fill, split merge) is JENGA_SPLIT_OVERHEAD_TILES tiles of
+// streaming time; < 0 keeps the byte-sized splits of tiles_per_split().
+#ifndef JENGA_SPLIT_OVERHEAD_TILES
+#define JENGA_SPLIT_OVERHEAD_TILES 4
+#endif
+int wave_tiles_per_split(int64_t pairs, int64_t max_tiles, int64_t slots, int fallback) {
+  if (JENGA_SPLIT_OVERHEAD_TILES < 0 || pairs <= 0 || max_tiles <= 0 || slots <= 0) return fallback;
+  int64_t best_s = 1;
+  double best = 0.0;
+  const int64_t s_max = std::max<int64_t>(1, max_tiles / kMinTilesPerSplit);
+  for (int64_t sp = 1; sp <= s_max; ++sp) {
+    const int64_t per = (max_tiles + sp - 1) / sp;
+    const int64_t rounds = (pairs * sp + slots - 1) / slots;
+    const double cost = static_cast<double>(rounds) * static_cast<double>(per + JENGA_SPLIT_OVERHEAD_TILES);
+    if (sp == 1 || cost < best * 0.999) {
+      best = cost;
+      best_s = sp;
+    }
+  }
+  return static_cast<int>(std::max<int64_t>(kMinTilesPerSplit, (max_tiles + best_s - 1) / best_s));
+}
+
 template <typename T, int D, int G>
 int launch_typed(const DecodeParams& prm, int batch, cudaStream_t stream) {
   constexpr int NS = 4;
@@ -404,6 +432,14 @@ int paged_decode_impl(void* arena_base, jenga_layer_view view, int kind, int dty
   prm.hkv = num_kv_heads;
   prm.tpp = tpp;
   prm.tiles_per_split = tiles_per_split(head_dim);
+  if ((dtype == JENGA_BF16 || dtype == JENGA_F16) && tpp % kTile == 0) {
+    // the tiles a request at full table width can need in this launch
+    int64_t max_tiles = (static_cast<int64_t>(max_blocks) * tpp + kTile - 1) / kTile;
+    if (kind == JENGA_KIND_SLIDING_WINDOW)
+      max_tiles = std::min<int64_t>(max_tiles, (static_cast<int64_t>(window) + kTile - 1) / kTile + 1);
+    prm.tiles_per_split = wave_tiles_per_split(static_cast<int64_t>(batch) * num_kv_heads, max_tiles,
+                                               static_cast<int64_t>(num_sms()) * 3, prm.tiles_per_split);
+  }
   prm.batch = batch;
   prm.max_splits = splits_for(max_blocks, tpp, prm.tiles_per_split);
   if (kind == JENGA_KIND_SLIDING_WINDOW) {
