@@ -20,7 +20,7 @@ from paper_2503_18292_b200.engine import DecodeEngine  # noqa: E402
 from paper_2503_18292_b200.geometry import gemma2_9b  # noqa: E402
 
 
-def run(B, ctx, chunk, iters=10, heads=(16, 8, 256)):
+def run(B, ctx, chunk, iters=10, heads=(16, 8, 256), softcap=0.0):
     H, Hkv, D = heads
     geom = gemma2_9b(16)
     for g in geom.groups:
@@ -43,7 +43,7 @@ def run(B, ctx, chunk, iters=10, heads=(16, 8, 256)):
     out = torch.empty_like(q)
     req = torch.arange(B, dtype=torch.int32, device="cuda").repeat_interleave(chunk)
     ords = (torch.arange(chunk, dtype=torch.int32, device="cuda") + (ctx - chunk + 1)).repeat(B)
-    res = {"B": B, "ctx": ctx, "chunk": chunk, "heads": f"Hq={H} Hkv={Hkv} D={D}"}
+    res = {"B": B, "ctx": ctx, "chunk": chunk, "heads": f"Hq={H} Hkv={Hkv} D={D}", "softcap": softcap}
     for g, name in ((0, "full"), (1, "swa")):
         t = eng.tables[g]
         slots = torch.empty(T, dtype=torch.int64, device="cuda")
@@ -54,7 +54,7 @@ def run(B, ctx, chunk, iters=10, heads=(16, 8, 256)):
         def once():
             ops.reshape_and_cache(eng.arena, view, k, v, slots, 16)
             ops.paged_prefill(eng.arena, view, int(geom.groups[g].kind), q, out, cu, chunk, t.block_table[:B],
-                              t.seq_lens[:B], Hkv, 16, D ** -0.5, window=W)
+                              t.seq_lens[:B], Hkv, 16, D ** -0.5, window=W, softcap=softcap)
         for _ in range(2):
             once()
         torch.cuda.synchronize()
@@ -65,7 +65,7 @@ def run(B, ctx, chunk, iters=10, heads=(16, 8, 256)):
         e1.record()
         for _ in range(iters):
             ops.paged_prefill(eng.arena, view, int(geom.groups[g].kind), q, out, cu, chunk, t.block_table[:B],
-                              t.seq_lens[:B], Hkv, 16, D ** -0.5, window=W)
+                              t.seq_lens[:B], Hkv, 16, D ** -0.5, window=W, softcap=softcap)
         e2.record()
         torch.cuda.synchronize()
         w_us = e0.elapsed_time(e1) * 1e3 / iters
@@ -83,6 +83,8 @@ def run(B, ctx, chunk, iters=10, heads=(16, 8, 256)):
 if __name__ == "__main__":
     for B, ctx, chunk in ((4, 8192, 2048), (16, 4096, 512), (64, 2048, 256)):
         run(B, ctx, chunk)
+    if "--softcap" in sys.argv:  # Gemma-2's attention-logit soft cap (tanh per logit)
+        run(4, 8192, 2048, softcap=50.0)
     if "--d128" in sys.argv:  # Llama-3.2 / Jamba attention heads
         for B, ctx, chunk in ((4, 8192, 2048), (16, 4096, 512)):
             run(B, ctx, chunk, heads=(32, 8, 128))

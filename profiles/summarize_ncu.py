@@ -85,8 +85,20 @@ def full(tag, src):
     if traffic:
         # bench.py sums one full + one SWA layer per pair; report mean per launch
         per = sum(t["bytes"] for t in traffic) / len(traffic)
+        # the bench line the captured command printed: bench.py only uses this
+        # traffic for the exact same workload
+        bench = {}
+        log = src / "ncu_full_bench.log"
+        if log.exists():
+            for line in log.read_text().splitlines():
+                if line.startswith("{") and '"metric"' in line:
+                    bench = json.loads(line)
         (ROOT / "profiles" / "decode_traffic.json").write_text(json.dumps(
             {"source": f"{tag}: ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum",
+             "workload": bench.get("config", {}).get("workload"),
+             "kernel_launches_per_step": (bench.get("roofline", {}).get("algorithmic_bytes_per_step", 0) //
+                                          max(1, bench.get("roofline", {}).get("algorithmic_bytes_per_launch", 1))),
+             "algorithmic_bytes_per_launch": bench.get("roofline", {}).get("algorithmic_bytes_per_launch"),
              "launches": traffic, "traffic_bytes_per_launch": per}, indent=1))
 
 

@@ -5,11 +5,14 @@ interleaved request order.  Checks, through the C ABI:
 
 * block tables / slot mappings / seq_lens of both groups bit-exact against the
   oracle's table build over the same page lists (all 32 requests);
-* reshape_and_cache of the newest token, read back byte-exact (sampled requests / heads);
-* paged decode on the last layer of each group: every request's output is
-  finite, and sampled requests match the C oracle (fp64) within the bf16
-  tolerance — the oracle runs on a compact copy of just those requests' layer
-  slices (the whole arena is too big to copy to the host).
+* the fused decode step the bench times (jenga_paged_decode_append: the newest
+  token's K/V written into its slot by the decode launch itself), on the last
+  layer of each group: the new K/V read back byte-exact (sampled requests /
+  heads), every request's output finite, and 8 sampled requests within the
+  bf16 tolerance of the C oracle (fp64) — the oracle runs on a compact copy
+  of just those requests' layer slices (the whole arena is too big to copy to
+  the host).  Tolerance is normwise per sample set: max|got - want| /
+  max|want| <= 1e-2.
 """
 import gc
 
@@ -82,10 +85,9 @@ def test_gemma_shard_full_size(orc):
             layer = gg.num_layers - 1  # the last layer: largest start_offset in the arena
             k = torch.randn((B, 8, 256), generator=gen, device=eng.device).to(torch.bfloat16)
             v = torch.randn((B, 8, 256), generator=gen, device=eng.device).to(torch.bfloat16)
-            eng.write_kv(g, layer, k, v)
             q = torch.randn((B, 16, 256), generator=gen, device=eng.device).to(torch.bfloat16)
             out = torch.empty_like(q)
-            eng.decode(g, layer, q, out)
+            eng.decode_append(g, layer, q, k, v, out)  # the bench's fused launch
             torch.cuda.synchronize()
             assert torch.isfinite(out.float()).all()
 
@@ -101,7 +103,7 @@ def test_gemma_shard_full_size(orc):
                         got = at[row:row + 512].cpu()
                         assert torch.equal(got, src[b, h].contiguous().view(torch.uint8).cpu())
 
-            sample = [0, 13, 31]
+            sample = [0, 4, 9, 13, 18, 22, 27, 31]
             rows = t.block_table[:B].cpu().numpy()[sample]
             host, ctable, cview = _compact(eng, g, layer, rows)
             want = orc.paged_decode(host, cview, int(gg.kind), BF16, gg.window, q[sample].view(torch.int16).cpu().numpy(),
