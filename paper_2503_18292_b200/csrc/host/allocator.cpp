@@ -120,6 +120,8 @@ TypeAllocator::TypeAllocator(GroupGeometry geo, int owner_id, LargePagePool* poo
   JENGA_CHECK(geo_.slots_per_large >= 1, "slots_per_large must be >= 1");
   units_.resize(pool_->num_pages());
   empty_.resize(uint64_t{pool_->num_pages()} * geo_.slots_per_large);
+  lru_it_.resize(uint64_t{pool_->num_pages()} * geo_.slots_per_large);
+  fe_it_.resize(pool_->num_pages());
 }
 
 TypeAllocator::Unit& TypeAllocator::unit_of(SmallPageId id) {
@@ -231,8 +233,8 @@ uint64_t TypeAllocator::evict_small(SmallPageId id) {
   JENGA_CHECK(r.has_cache_key, "evictable page lost its cache key");
   const uint64_t key = r.cache_key;
   const uint64_t g = global_index(id.large.index, id.slot);
-  lru_.erase(lru_key(r, g));
-  if (u.evictable_count == u.slots.size()) fully_evictable_.erase(id.large.index);
+  lru_.erase(lru_it_[g]);
+  if (u.evictable_count == u.slots.size()) fully_evictable_.erase(fe_it_[id.large.index]);
   u.evictable_count--;
   r.state = SmallPageState::kEmpty;
   r.has_cache_key = false;
@@ -268,8 +270,8 @@ void TypeAllocator::free(SmallPageId id, std::optional<uint64_t> cache_key) {
     r.cache_key = *cache_key;
     r.has_cache_key = true;
     u.evictable_count++;
-    if (u.evictable_count == u.slots.size()) fully_evictable_.insert(id.large.index);
-    lru_.insert(lru_key(r, g));
+    if (u.evictable_count == u.slots.size()) fe_it_[id.large.index] = fully_evictable_.insert(id.large.index).first;
+    lru_it_[g] = lru_.insert(lru_key(r, g)).first;
     return;
   }
   r.state = SmallPageState::kEmpty;
@@ -284,8 +286,8 @@ void TypeAllocator::pin(SmallPageId id, uint64_t request) {
   Unit& u = unit_of(id);
   SmallPageRecord& r = u.slots[id.slot];
   JENGA_CHECK(r.state == SmallPageState::kEvictable, "pin on a non-evictable page");
-  lru_.erase(lru_key(r, global_index(id.large.index, id.slot)));
-  if (u.evictable_count == u.slots.size()) fully_evictable_.erase(id.large.index);
+  lru_.erase(lru_it_[global_index(id.large.index, id.slot)]);
+  if (u.evictable_count == u.slots.size()) fully_evictable_.erase(fe_it_[id.large.index]);
   u.evictable_count--;
   r.state = SmallPageState::kUsed;
   r.has_cache_key = false;
@@ -299,9 +301,9 @@ void TypeAllocator::touch(SmallPageId id, uint64_t step) {
   SmallPageRecord& r = rec(id);
   if (r.state == SmallPageState::kEvictable) {
     const uint64_t g = global_index(id.large.index, id.slot);
-    lru_.erase(lru_key(r, g));
+    lru_.erase(lru_it_[g]);
     r.last_access = step;
-    lru_.insert(lru_key(r, g));
+    lru_it_[g] = lru_.insert(lru_key(r, g)).first;
   } else {
     r.last_access = step;
   }
@@ -312,9 +314,9 @@ void TypeAllocator::set_prefix_length(SmallPageId id, uint64_t len) {
   SmallPageRecord& r = rec(id);
   if (r.state == SmallPageState::kEvictable) {
     const uint64_t g = global_index(id.large.index, id.slot);
-    lru_.erase(lru_key(r, g));
+    lru_.erase(lru_it_[g]);
     r.prefix_length = len;
-    lru_.insert(lru_key(r, g));
+    lru_it_[g] = lru_.insert(lru_key(r, g)).first;
   } else {
     r.prefix_length = len;
   }

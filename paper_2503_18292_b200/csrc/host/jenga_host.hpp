@@ -239,10 +239,15 @@ class TypeAllocator {
   std::vector<Unit> units_;               // indexed by large page index
   uint64_t owned_units_ = 0;
   std::set<LruKey> lru_;                  // begin() = eviction front
+  // node of each evictable page in lru_ / unit in fully_evictable_ (by global
+  // / unit index): a pin or touch erases by iterator instead of searching the
+  // (tens of thousands of entries under prefix caching) ordered set
+  std::vector<std::set<LruKey>::iterator> lru_it_;
   FirstFitBitmap empty_;                  // global indices of empty owned slots
   // request -> its associated empty slots (global indices, kept sorted)
   std::unordered_map<uint64_t, std::vector<uint64_t>> empty_by_request_;
   std::set<uint32_t> fully_evictable_;    // units whose every slot is evictable
+  std::vector<std::set<uint32_t>::iterator> fe_it_;
   uint64_t used_ = 0;
 };
 
