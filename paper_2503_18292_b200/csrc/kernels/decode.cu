@@ -319,7 +319,7 @@ int tiles_per_split(int head_dim) {
 // (prologue, ring fill, split merge) is JENGA_SPLIT_OVERHEAD_TILES tiles of
 // streaming time; < 0 keeps the byte-sized splits of tiles_per_split().
 #ifndef JENGA_SPLIT_OVERHEAD_TILES
-#define JENGA_SPLIT_OVERHEAD_TILES 4
+#define JENGA_SPLIT_OVERHEAD_TILES 32
 #endif
 int wave_tiles_per_split(int64_t pairs, int64_t max_tiles, int64_t slots, int fallback) {
   if (JENGA_SPLIT_OVERHEAD_TILES < 0 || pairs <= 0 || max_tiles <= 0 || slots <= 0) return fallback;
