@@ -163,6 +163,15 @@ __device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16u(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};\n" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 template <typename T>
@@ -911,10 +920,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
   constexpr int V_PIECE = VB * kTile * 128;   // one 16-key piece, this CTA's chunks
   constexpr int V_BYTES = (KT / kTile) * V_PIECE;
   constexpr int STAGE = K_BYTES + V_BYTES;
-  // TMEM per CTA: O_A | O_B | Q_A | Q_B | S_A | S_B
+  // TMEM per CTA: O_A | O_B | Q_A | Q_B | S buffers (NSB per group).  With 64-key
+  // tiles there is room for one S buffer per group, so S_g(j+1) can only start once
+  // PV_g(j) consumed P_g(j) and each group's softmax -> PV -> S chain is serial;
+  // with 32-key tiles two buffers per group fit, S_g(j+1) is computed while the
+  // softmax of tile j runs, and the chain is only softmax -> PV.
+  constexpr int NSB = KT == 32 ? 2 : 1;
   constexpr int O_COL0 = 0, Q_COL0 = 2 * D, S_COL0 = 3 * D;
   constexpr uint32_t TMEM_COLS = 512;
-  static_assert(NBOX % 2 == 0 && KT == 64 && 3 * D + 2 * KT <= 512, "ping-pong kernel shape");
+  static_assert(NBOX % 2 == 0 && (KT == 64 || KT == 32) && 3 * D + 2 * NSB * KT <= 512, "ping-pong kernel shape");
   constexpr int PW = 8, MW = 9;               // producer, MMA warps (0-7 softmax)
 
   extern __shared__ uint8_t smem_raw[];
@@ -923,10 +937,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
   uint64_t* q_full = bars;                    // leader: 16 softmax warps of the pair
   uint64_t* kv_full = bars + 1;               // leader: both CTAs' TMA bytes
   uint64_t* kv_empty = kv_full + NS;          // both: multicast commit
-  uint64_t* s_full = kv_empty + NS;           // both: multicast commit
-  uint64_t* p_full = s_full + 2;              // leader: 8 softmax warps of the pair
-  uint64_t* p_empty = p_full + 2;             // both: multicast commit
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
+  uint64_t* s_full = kv_empty + NS;           // both: multicast commit      [group][buffer]
+  uint64_t* p_full = s_full + 2 * NSB;        // leader: 8 softmax warps    [group][buffer]
+  uint64_t* p_empty = p_full + 2 * NSB;       // both: multicast commit      [group][buffer]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2 * NSB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -950,7 +964,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
       jenga_dev::mbar_init(&kv_full[i], 1);
       jenga_dev::mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2 * NSB; ++i) {
       jenga_dev::mbar_init(&s_full[i], 1);
       jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
       jenga_dev::mbar_init(&p_empty[i], 1);
@@ -1010,23 +1024,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
     if (rank == 0 && lane == 0) {
       const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
       const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
+      // S_g(jj) lands in buffer jj % NSB of group g; its barriers are [g * NSB + jj % NSB],
+      // each used every NSB tiles (phase = (jj / NSB) & 1)
+      auto scol = [&](int jj, int g) { return S_COL0 + (g * NSB + jj % NSB) * KT; };
       auto issue_s = [&](int jj, int g) {  // S_g(jj) = Q_g K_jj^T (K stage already full)
         const uint32_t k_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
-          umma2_ts(tmem + S_COL0 + g * KT, tmem + Q_COL0 + g * (D / 2) + k * 8,
+          umma2_ts(tmem + scol(jj, g), tmem + Q_COL0 + g * (D / 2) + k * 8,
                    umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
-        umma2_commit_both(&s_full[g]);
+        umma2_commit_both(&s_full[g * NSB + jj % NSB]);
       };
       auto issue_pv = [&](int jj, int g) {  // O_g += P_g(jj) V_jj
-        jenga_dev::mbar_wait(&p_full[g], jj & 1);
+        jenga_dev::mbar_wait(&p_full[g * NSB + jj % NSB], (jj / NSB) & 1);
         tc_fence_after();
         const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + K_BYTES);
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k)
-          umma2_ts(tmem + O_COL0 + g * D, tmem + S_COL0 + g * KT + k * 8,
+          umma2_ts(tmem + O_COL0 + g * D, tmem + scol(jj, g) + k * 8,
                    umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o, (jj > 0 || k > 0) ? 1u : 0u);
-        umma2_commit_both(&p_empty[g]);
+        umma2_commit_both(&p_empty[g * NSB + jj % NSB]);
       };
       auto wait_kv = [&](int jj) {
         jenga_dev::mbar_wait(&kv_full[jj % NS], (jj / NS) & 1);
@@ -1039,28 +1056,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
         issue_s(0, 1);
       }
       for (int j = 0; j < ntiles; ++j) {
-        // S_g(j+1) overwrites S_g's buffer (P_g(j)): issued after PV_g(j), in order
-        issue_pv(j, 0);
-        if (j + 1 < ntiles) {
-          wait_kv(j + 1);
-          issue_s(j + 1, 0);
+        if constexpr (NSB == 2) {
+          // S_g(j+1) goes to the other buffer (freed by PV_g(j-1), issued earlier):
+          // issue it before waiting for the softmax of tile j
+          if (j + 1 < ntiles) {
+            wait_kv(j + 1);
+            issue_s(j + 1, 0);
+            issue_s(j + 1, 1);
+          }
+          issue_pv(j, 0);
+          issue_pv(j, 1);
+          umma2_commit_both(&kv_empty[j % NS]);  // both groups' MMAs of tile j issued
+        } else {
+          // S_g(j+1) overwrites S_g's buffer (P_g(j)): issued after PV_g(j), in order
+          issue_pv(j, 0);
+          if (j + 1 < ntiles) {
+            wait_kv(j + 1);
+            issue_s(j + 1, 0);
+          }
+          issue_pv(j, 1);
+          umma2_commit_both(&kv_empty[j % NS]);  // both groups' PVs of tile j issued
+          if (j + 1 < ntiles) issue_s(j + 1, 1);
         }
-        issue_pv(j, 1);
-        umma2_commit_both(&kv_empty[j % NS]);  // both groups' PVs of tile j issued
-        if (j + 1 < ntiles) issue_s(j + 1, 1);
       }
     }
   } else {
     const int grp = warp >> 2;                  // 0: tile A, 1: tile B
     const int r = threadIdx.x & (kRows - 1);    // query row == TMEM lane
     const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const int Q_COL = Q_COL0 + grp * (D / 2), S_COL = S_COL0 + grp * KT, O_COL = O_COL0 + grp * D;
+    const int Q_COL = Q_COL0 + grp * (D / 2), O_COL = O_COL0 + grp * D;
     const int t0 = pt0 + (2 * grp + static_cast<int>(rank)) * QB;
     const int tok = t0 + r / G;
     const bool row_ok = tok < c_len;
     const int ipos = n - c_len + tok;
     const uint32_t q_full0 = map_to_cta0(q_full);
-    const uint32_t p_full0 = map_to_cta0(&p_full[grp]);
+    const uint32_t p_full0 = map_to_cta0(&p_full[grp * NSB]);
     {
       const uint4* qrow = reinterpret_cast<const uint4*>(
           static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
@@ -1092,13 +1122,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
     const float qi = p.qscale * p.inv_cap;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
-      const int sb = 0;  // one S buffer per group
+      const int sbi = grp * NSB + j % NSB;  // this tile's S buffer / barrier index
+      const int S_COL = S_COL0 + sbi * KT, sb = 0;
       const int ktok0 = (tile_lo + j) * KT;
-      jenga_dev::mbar_wait(&s_full[grp], j & 1);
+      jenga_dev::mbar_wait(&s_full[sbi], (j / NSB) & 1);
       tc_fence_after();
-      static_assert(KT == 64, "one 64-column S load");
       float s[KT];
-      tmem_ld64(tmem + lane_addr + S_COL + sb * KT, s);  // both halves behind one wait
+      if constexpr (KT == 64) {
+        tmem_ld64(tmem + lane_addr + S_COL + sb * KT, s);  // both halves behind one wait
+      } else {
+        float v[32];
+        tmem_ld32(tmem + lane_addr + S_COL + sb * KT, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[i] = v[i];
+      }
       if (softcap) {
 #pragma unroll
         for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
@@ -1116,7 +1153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
         const float m_new = fmaxf(m_used, mt);
         if (j >= 1) {
           const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
-          jenga_dev::mbar_wait(&p_empty[grp], (j - 1) & 1);
+          jenga_dev::mbar_wait(&p_empty[grp * NSB + (j - 1) % NSB], ((j - 1) / NSB) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D; c += 32) {
@@ -1145,11 +1182,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
       }
       l += rs0 + rs1;
 #pragma unroll
-      for (int c = 0; c < KT / 2; c += 32) {
-        uint32_t w[32];
+      if constexpr (KT / 2 >= 32) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
-        tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
+        for (int c = 0; c < KT / 2; c += 32) {
+          uint32_t w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
+          tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
+        }
+      } else {
+        tmem_st16u(tmem + lane_addr + S_COL + sb * KT, pk);
       }
       tmem_st_wait();
       // zero this CTA's V columns of keys outside the pair's range
@@ -1171,13 +1213,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
+        const uint32_t pf = p_full0 + 8u * (j % NSB);  // the leader's p_full[grp * NSB + j % NSB]
         if (boundary)
-          arrive_cta0_release(p_full0);
+          arrive_cta0_release(pf);
         else
-          arrive_cta0(p_full0);
+          arrive_cta0(pf);
       }
     }
-    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[grp], (ntiles - 1) & 1);
+    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[grp * NSB + (ntiles - 1) % NSB], ((ntiles - 1) / NSB) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
@@ -1286,7 +1329,7 @@ template <typename T, int D, int G, int KT, int NS>
 int launch_tc5_pp(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   constexpr int NBOX = D / kBoxCols;
   constexpr int STAGE = NBOX * (KT / 2) * 128 + (NBOX / 2) * KT * 128;
-  const int smem = NS * STAGE + (1 + 2 * NS + 6) * 8 + 16 + 1024;
+  const int smem = NS * STAGE + (1 + 2 * NS + 12) * 8 + 16 + 1024;
   CUtensorMap k_map, v_map;
   if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
   auto kern = paged_prefill_tc5_pp_kernel<T, D, G, KT, NS>;
@@ -1297,13 +1340,20 @@ int launch_tc5_pp(const Prefill5Params& prm, int dtype, cudaStream_t s, int batc
   return jenga_dev::check_launch("paged_prefill_tc5_pp_kernel");
 }
 
-template <typename T, int D, int NS>
+// Key-tile width of the ping-pong kernel: 64 keys (one S buffer per group) or 32
+// (two S buffers per group, twice the ring depth).
+#ifndef JENGA_PP_KT
+#define JENGA_PP_KT 64
+#endif
+template <typename T, int D, int NS0>
 int dispatch_pp(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  constexpr int KT = JENGA_PP_KT;
+  constexpr int NS = NS0 * 64 / KT;
   switch (G) {
-    case 1: return launch_tc5_pp<T, D, 1, 64, NS>(prm, dtype, s, batch);
-    case 2: return launch_tc5_pp<T, D, 2, 64, NS>(prm, dtype, s, batch);
-    case 4: return launch_tc5_pp<T, D, 4, 64, NS>(prm, dtype, s, batch);
-    case 8: return launch_tc5_pp<T, D, 8, 64, NS>(prm, dtype, s, batch);
+    case 1: return launch_tc5_pp<T, D, 1, KT, NS>(prm, dtype, s, batch);
+    case 2: return launch_tc5_pp<T, D, 2, KT, NS>(prm, dtype, s, batch);
+    case 4: return launch_tc5_pp<T, D, 4, KT, NS>(prm, dtype, s, batch);
+    case 8: return launch_tc5_pp<T, D, 8, KT, NS>(prm, dtype, s, batch);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
