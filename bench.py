@@ -54,6 +54,10 @@ def parse():
     p.add_argument("--tpp", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-io", default="overlap", choices=["overlap", "serial", "none", "in-only", "out-only"],
+                   help="profiling only: how the e2e leg moves q/k/v and outputs (overlap = the measured "
+                        "contract: side-stream chunks; serial = before / after the step on its stream; "
+                        "none = no copies, isolates the per-step host synchronisation)")
     p.add_argument("--unfused", action="store_true",
                    help="separate reshape_and_cache + paged_decode launches instead of jenga_paged_decode_append")
     p.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly instead of one CUDA graph "
@@ -557,10 +561,12 @@ def run_ours(a, rank, world, local_rank):
         # cross-stream wait / event record inside the step breaks the PDL chain
         # (~15 us each: one chunk per layer costs +0.6 ms a step), so only three
         # chunks each way: inputs [0,1) [1,3) [3,L) and outputs [0,L-3) [L-3,L-1)
-        # [L-1,L).  Measured (Gemma step, 22 MB in / 11 MB out at 55 GB/s): the
-        # e2e step stays ~0.5 ms above the device step however the inputs are
-        # chunked — H2D DMA writes interleaved with the decode's read stream cost
-        # about what they would serialised.
+        # [L-1,L).  Measured (Gemma step, 22 MB in / 11 MB out; --e2e-io):
+        # outputs cost 0.05 ms, the host sync 0.05 ms, the inputs ~0.45 ms whatever
+        # the chunking (1,3 / 1,3,7,15,31 / 1,2,4,...,32 / 2,6,14,30 all within
+        # 0.7%) — H2D DMA writes into HBM under the decode's read stream cost
+        # about what they would serialised; kernels reading q / K / V straight
+        # from pinned host memory (no HBM writes) measured slower still.
         cs = torch.cuda.Stream(device=dev)
         in_bounds = sorted({0, min(1, na), min(3, na), na})
         out_bounds = sorted({0, max(na - 3, 0), max(na - 1, 0), na})
@@ -570,9 +576,21 @@ def run_ours(a, rank, world, local_rank):
         out_end = {out_bounds[c + 1] - 1: c for c in range(len(out_bounds) - 1)}
 
         def e2e_device(totals):
+            if a.e2e_io not in ("overlap", "in-only", "out-only"):
+                if a.e2e_io == "serial":
+                    q.copy_(hq, non_blocking=True)
+                    kn.copy_(hk, non_blocking=True)
+                    vn.copy_(hv, non_blocking=True)
+                device_step(totals)
+                if a.e2e_io == "serial":
+                    ho.copy_(out, non_blocking=True)
+                return
             cs.wait_stream(torch.cuda.current_stream())  # previous step's readers of q/k/v are done
             with torch.cuda.stream(cs):
                 for c in range(len(in_bounds) - 1):
+                    if a.e2e_io == "out-only":
+                        ev_in[c].record(cs)
+                        continue
                     lo, hi = in_bounds[c], in_bounds[c + 1]
                     q[lo:hi].copy_(hq[lo:hi], non_blocking=True)
                     kn[lo:hi].copy_(hk[lo:hi], non_blocking=True)
@@ -584,6 +602,8 @@ def run_ours(a, rank, world, local_rank):
             device_step(totals, hooks=chunk_hooks)
             for c in range(len(out_bounds) - 1):
                 cs.wait_event(ev_out[c])
+                if a.e2e_io == "in-only":
+                    continue
                 with torch.cuda.stream(cs):
                     lo, hi = out_bounds[c], out_bounds[c + 1]
                     ho[lo:hi].copy_(out[lo:hi], non_blocking=True)
