@@ -13,6 +13,17 @@ constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
+// Tensor-core decode residency: CTAs per SM and the stage-ring bytes of each
+// (three 64 KiB rings, ~192 KiB in flight per SM).  Compile-time so profiling
+// variants (build.py --variant) can sweep them; the product uses the defaults.
+#ifndef JENGA_DECODE_CTAS_PER_SM
+#define JENGA_DECODE_CTAS_PER_SM 3
+#endif
+#ifndef JENGA_DECODE_RING_BYTES
+#define JENGA_DECODE_RING_BYTES 65536
+#endif
+constexpr int kDecodeCtasPerSm = JENGA_DECODE_CTAS_PER_SM;
+constexpr int kDecodeRingBytes = JENGA_DECODE_RING_BYTES;
 
 struct DecodeParams {
   const uint8_t* arena;

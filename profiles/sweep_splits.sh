@@ -5,12 +5,15 @@
 #   bytes: byte-sized splits (32 tiles at D=256, 96 at D=128)
 #   cN:    wave-aware splits with N tiles of per-CTA overhead (product: c4)
 out=${1:-gpurun_out/r02_sweep_splits.jsonl}
+variants=${2:-"product bytes c2 c8 c16 c32 c64"}
+workloads=${3:-"gemma2-9b|llama-3.2-11b-vision --ctx 2048|jamba-style|prefix-mix"}
 : > $out
-for spec in "gemma2-9b" "llama-3.2-11b-vision --ctx 2048" "jamba-style" "prefix-mix"; do
+IFS='|' read -ra specs <<< "$workloads"
+for spec in "${specs[@]}"; do
   set -- $spec
   wl=$1; shift
   extra="$*"
-  for v in product bytes c2 c8 c16 c32 c64; do
+  for v in $variants; do
     if [ $v = product ]; then lib=paper_2503_18292_b200/libjenga_b200.so; else lib=paper_2503_18292_b200/variants/libjenga_b200_$v.so; fi
     line=$(JENGA_B200_LIB=$lib timeout 400 python bench.py --workload $wl $extra --steps 10 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1)
     python - "$wl" "$v" "$line" >> $out <<'PY'
