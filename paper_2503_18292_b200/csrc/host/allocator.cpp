@@ -444,36 +444,110 @@ uint64_t chain_block_key(uint64_t parent, const std::vector<uint64_t>& tokens) {
 }
 
 // reference prefix_cache.cpp:59-100
+const PrefixCache::Slot* PrefixCache::probe(const Table& t, uint64_t key) {
+  if (t.slots.empty()) return nullptr;
+  const size_t mask = t.slots.size() - 1;
+  for (size_t i = home(key, mask);; i = (i + 1) & mask) {
+    const Slot& s = t.slots[i];
+    if (s.state == 0) return nullptr;
+    if (s.state == 1 && s.key == key) return &s;
+  }
+}
+
+void PrefixCache::rehash(Table& t, size_t capacity) {
+  std::vector<Slot> old;
+  old.swap(t.slots);
+  t.slots.assign(capacity, Slot{});
+  t.occupied = 0;
+  const size_t mask = capacity - 1;
+  for (const Slot& s : old) {
+    if (s.state != 1) continue;
+    size_t i = home(s.key, mask);
+    while (t.slots[i].state != 0) i = (i + 1) & mask;
+    t.slots[i] = s;
+    ++t.occupied;
+  }
+}
+
+PrefixCache::Slot& PrefixCache::insert_slot(Table& t, uint64_t key) {
+  if (t.slots.empty() || (t.occupied + 1) * 2 > t.slots.size()) {
+    size_t live = 0;
+    for (const Slot& s : t.slots) live += s.state == 1;
+    size_t cap = 64;
+    while (cap < (live + 1) * 4) cap *= 2;  // <= 1/4 live after a rebuild (tombstones dropped)
+    rehash(t, cap);
+  }
+  const size_t mask = t.slots.size() - 1;
+  Slot* tomb = nullptr;
+  for (size_t i = home(key, mask);; i = (i + 1) & mask) {
+    Slot& s = t.slots[i];
+    if (s.state == 1 && s.key == key) return s;
+    if (s.state == 2 && tomb == nullptr) tomb = &s;
+    if (s.state == 0) {
+      Slot& dst = tomb != nullptr ? *tomb : s;
+      if (tomb == nullptr) ++t.occupied;
+      dst = Slot{key, kNil, kNil, 1};
+      return dst;
+    }
+  }
+}
+
 void PrefixCache::register_block(size_t g, const BlockContent& c, SmallPageId page) {
-  JENGA_CHECK(g < by_group_.size(), "group index out of range");
-  by_group_[g][c.key].push_back(Entry{c, page});
+  JENGA_CHECK(g < groups_.size(), "group index out of range");
+  Table& t = groups_[g];
+  uint32_t e;
+  if (!t.free.empty()) {
+    e = t.free.back();
+    t.free.pop_back();
+    t.pool[e] = Entry{c, page, kNil};
+  } else {
+    e = static_cast<uint32_t>(t.pool.size());
+    t.pool.push_back(Entry{c, page, kNil});
+  }
+  Slot& s = insert_slot(t, c.key);
+  if (s.tail == kNil) s.head = e;
+  else t.pool[s.tail].next = e;
+  s.tail = e;
+  ++t.entries;
 }
 
 void PrefixCache::unregister(size_t g, uint64_t key, SmallPageId page) {
-  JENGA_CHECK(g < by_group_.size(), "group index out of range");
-  auto& table = by_group_[g];
-  auto it = table.find(key);
-  if (it == table.end()) return;
-  auto& v = it->second;
-  v.erase(std::remove_if(v.begin(), v.end(), [&](const Entry& e) { return e.page == page; }),
-          v.end());
-  if (v.empty()) table.erase(it);
+  JENGA_CHECK(g < groups_.size(), "group index out of range");
+  Table& t = groups_[g];
+  Slot* s = const_cast<Slot*>(probe(t, key));
+  if (s == nullptr) return;
+  // every entry of the key holding this page (the reference erases them all)
+  uint32_t prev = kNil;
+  for (uint32_t e = s->head; e != kNil;) {
+    const uint32_t next = t.pool[e].next;
+    if (t.pool[e].page == page) {
+      if (prev == kNil) s->head = next;
+      else t.pool[prev].next = next;
+      if (s->tail == e) s->tail = prev;
+      t.pool[e].content.tokens.clear();
+      t.free.push_back(e);
+      --t.entries;
+    } else {
+      prev = e;
+    }
+    e = next;
+  }
+  if (s->head == kNil) s->state = 2;  // tombstone
 }
 
 std::optional<SmallPageId> PrefixCache::find(size_t g, const BlockContent& c) const {
-  JENGA_CHECK(g < by_group_.size(), "group index out of range");
-  auto it = by_group_[g].find(c.key);
-  if (it == by_group_[g].end()) return std::nullopt;
-  for (const Entry& e : it->second)
-    if (e.content.matches(c)) return e.page;
+  JENGA_CHECK(g < groups_.size(), "group index out of range");
+  const Table& t = groups_[g];
+  const Slot* s = probe(t, c.key);
+  if (s == nullptr) return std::nullopt;
+  for (uint32_t e = s->head; e != kNil; e = t.pool[e].next)
+    if (t.pool[e].content.matches(c)) return t.pool[e].page;
   return std::nullopt;
 }
 
 uint64_t PrefixCache::entries(size_t g) const {
-  JENGA_CHECK(g < by_group_.size(), "group index out of range");
-  uint64_t n = 0;
-  for (const auto& kv : by_group_[g]) n += kv.second.size();
-  return n;
+  JENGA_CHECK(g < groups_.size(), "group index out of range");
+  return groups_[g].entries;
 }
 
 // ------------------------------------------------------------ KvAllocator

@@ -263,20 +263,44 @@ struct BlockContent {
 uint64_t block_chain_salt(const std::string& group_name);
 uint64_t chain_block_key(uint64_t parent, const std::vector<uint64_t>& tokens);
 
+// reference prefix_cache.hpp:20-75 semantics: per group, chain key -> the
+// cached pages holding that content, in registration order.  Stored as an
+// open-addressing table (the keys are already mixed 64-bit chain hashes) over a
+// pool of entries chained per key, so a lookup costs a slot probe and an entry
+// read instead of a node-based hash map's chain of dependent cache misses —
+// admission under prefix caching does hundreds of them per request.
 class PrefixCache {
  public:
-  explicit PrefixCache(size_t n) : by_group_(n) {}
+  explicit PrefixCache(size_t n) : groups_(n) {}
   void register_block(size_t g, const BlockContent& c, SmallPageId page);
   void unregister(size_t g, uint64_t key, SmallPageId page);
   std::optional<SmallPageId> find(size_t g, const BlockContent& c) const;
   uint64_t entries(size_t g) const;
 
  private:
+  static constexpr uint32_t kNil = UINT32_MAX;
   struct Entry {
     BlockContent content;
     SmallPageId page;
+    uint32_t next = kNil;
   };
-  std::vector<std::unordered_map<uint64_t, std::vector<Entry>>> by_group_;
+  struct Slot {
+    uint64_t key = 0;
+    uint32_t head = kNil, tail = kNil;  // entries of this key, registration order
+    uint8_t state = 0;                  // 0 empty, 1 live, 2 tombstone
+  };
+  struct Table {
+    std::vector<Slot> slots;  // power-of-two size
+    std::vector<Entry> pool;
+    std::vector<uint32_t> free;
+    uint64_t occupied = 0;    // live + tombstone slots
+    uint64_t entries = 0;
+  };
+  static size_t home(uint64_t key, size_t mask) { return static_cast<size_t>(key ^ (key >> 31)) & mask; }
+  static const Slot* probe(const Table& t, uint64_t key);
+  static Slot& insert_slot(Table& t, uint64_t key);
+  static void rehash(Table& t, size_t capacity);
+  std::vector<Table> groups_;
 };
 
 // ---------------------------------------------------------------- prefix sets
