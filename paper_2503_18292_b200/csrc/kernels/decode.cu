@@ -438,7 +438,7 @@ int paged_decode_impl(void* arena_base, jenga_layer_view view, int kind, int dty
     if (kind == JENGA_KIND_SLIDING_WINDOW)
       max_tiles = std::min<int64_t>(max_tiles, (static_cast<int64_t>(window) + kTile - 1) / kTile + 1);
     prm.tiles_per_split = wave_tiles_per_split(static_cast<int64_t>(batch) * num_kv_heads, max_tiles,
-                                               static_cast<int64_t>(num_sms()) * kDecodeCtasPerSm, prm.tiles_per_split);
+                                               static_cast<int64_t>(num_sms()) * decode_ctas_per_sm(head_dim), prm.tiles_per_split);
   }
   prm.batch = batch;
   prm.max_splits = splits_for(max_blocks, tpp, prm.tiles_per_split);

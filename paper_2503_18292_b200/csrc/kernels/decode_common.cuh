@@ -13,17 +13,28 @@ constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
-// Tensor-core decode residency: CTAs per SM and the stage-ring bytes of each
-// (three 64 KiB rings, ~192 KiB in flight per SM).  Compile-time so profiling
-// variants (build.py --variant) can sweep them; the product uses the defaults.
-#ifndef JENGA_DECODE_CTAS_PER_SM
-#define JENGA_DECODE_CTAS_PER_SM 3
+// Tensor-core decode residency per head_dim: CTAs per SM and the stage-ring
+// bytes of each.  Measured (profiles/r02_sweep_residency.jsonl): two 64 KiB
+// rings per SM at head_dim 256, four 48 KiB rings at 128 and below.
+// Compile-time so profiling variants (build.py --variant) can sweep them.
+#ifndef JENGA_DECODE_CTAS_PER_SM_D256
+#define JENGA_DECODE_CTAS_PER_SM_D256 2
 #endif
-#ifndef JENGA_DECODE_RING_BYTES
-#define JENGA_DECODE_RING_BYTES 65536
+#ifndef JENGA_DECODE_RING_BYTES_D256
+#define JENGA_DECODE_RING_BYTES_D256 65536
 #endif
-constexpr int kDecodeCtasPerSm = JENGA_DECODE_CTAS_PER_SM;
-constexpr int kDecodeRingBytes = JENGA_DECODE_RING_BYTES;
+#ifndef JENGA_DECODE_CTAS_PER_SM_D128
+#define JENGA_DECODE_CTAS_PER_SM_D128 4
+#endif
+#ifndef JENGA_DECODE_RING_BYTES_D128
+#define JENGA_DECODE_RING_BYTES_D128 49152
+#endif
+constexpr int decode_ctas_per_sm(int head_dim) {
+  return head_dim >= 256 ? JENGA_DECODE_CTAS_PER_SM_D256 : JENGA_DECODE_CTAS_PER_SM_D128;
+}
+constexpr int decode_ring_bytes(int head_dim) {
+  return head_dim >= 256 ? JENGA_DECODE_RING_BYTES_D256 : JENGA_DECODE_RING_BYTES_D128;
+}
 
 struct DecodeParams {
   const uint8_t* arena;

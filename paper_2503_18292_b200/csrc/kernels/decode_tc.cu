@@ -89,14 +89,14 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   }
 }
 
-// Stage ring: kDecodeRingBytes per CTA (64 KiB, three CTAs per SM, ~192 KiB in flight per SM),
+// Stage ring: decode_ring_bytes(D) per CTA (decode_common.cuh),
 // a multiple of the four consumer warps so each slot is always consumed by the
 // same warp — a warp that skipped a use of a slot could otherwise wait on a
 // parity two phases ahead and pass early.
 template <int D>
 constexpr int stages() {
   constexpr int stage = 2 * kTile * D * 2;
-  constexpr int ns = (kDecodeRingBytes / stage) / kConsumerWarps * kConsumerWarps;
+  constexpr int ns = (decode_ring_bytes(D) / stage) / kConsumerWarps * kConsumerWarps;
   return ns < kConsumerWarps ? kConsumerWarps : (ns > 12 ? 12 : ns);
 }
 
@@ -304,7 +304,7 @@ __device__ __forceinline__ int32_t tile_row(const DecodeParams& p, const int32_t
 // ------------------------------------------------------------ grid kernel
 // One CTA per (KV head, request, split).
 template <typename T, int D, int G, int NS>
-__global__ void __launch_bounds__(kThreads, kDecodeCtasPerSm)
+__global__ void __launch_bounds__(kThreads, decode_ctas_per_sm(D))
     paged_decode_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
   static_assert(D % kBoxCols == 0, "head_dim must be a multiple of 64");
   static_assert(G <= 8, "at most 8 query heads per KV head (N = 8)");

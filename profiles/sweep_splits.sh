@@ -3,7 +3,8 @@
 # Gemma shard, Llama-3.2-Vision and Jamba-style workloads under compile-time
 # variants of the split policy (paper_2503_18292_b200/build.py --variant).
 #   bytes: byte-sized splits (32 tiles at D=256, 96 at D=128)
-#   cN:    wave-aware splits with N tiles of per-CTA overhead (product: c4)
+#   cN:    wave-aware splits with N tiles of per-CTA overhead (product: c32);
+#   other names: residency variants (CTAs per SM x ring bytes), see DESIGN.md §3
 out=${1:-gpurun_out/r02_sweep_splits.jsonl}
 variants=${2:-"product bytes c2 c8 c16 c32 c64"}
 workloads=${3:-"gemma2-9b|llama-3.2-11b-vision --ctx 2048|jamba-style|prefix-mix"}
