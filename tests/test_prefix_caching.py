@@ -206,3 +206,77 @@ def test_mamba_checkpoint_copies_are_queued_and_dropped_when_evicted():
         pass
     assert pl.take_checkpoint_copies() == []  # its page left the cache: nothing to copy into
     kv.check_invariants()
+
+
+def test_prefix_cache_table_against_a_model():
+    """The prefix cache's open-addressing table (chain key -> cached pages in
+    registration order, reference prefix_cache.cpp:59-100) against a plain
+    dict model under churn: thousands of registrations (through free with
+    content), pins (unregister), evictions, colliding keys with different
+    contents, tombstones and rehashes; every lookup and entry count agrees."""
+    from paper_2503_18292_b200 import BlockContent
+    spec = ModelSpec("c", [LayerGroupSpec("full", LayerKind.kFullAttention, 1, 64, tokens_per_page=2)])
+    kv = KvAllocator(spec, 3000 * 128)
+    rng = np.random.default_rng(11)
+    model = {}      # key -> list of (content tuple, page) in registration order
+    cached = []     # (content, page) currently registered
+    used = []       # pages held by "requests"
+    contents = [BlockContent(int(rng.integers(0, 40)), int(rng.integers(0, 3)), [int(x) for x in rng.integers(0, 4, 2)])
+                for _ in range(300)]  # few keys: many collisions and duplicate contents
+
+    def ckey(c):
+        return (c.key, c.parent_key, tuple(c.tokens))
+
+    def is_cached(pg):
+        try:
+            return kv.record(0, pg)["state"] == 1
+        except Exception:  # its large page went back to the pool
+            return False
+
+    def model_find(c):
+        for cc, page in model.get(c.key, []):
+            if cc == ckey(c):
+                return page
+        return None
+
+    def unreg(page):
+        for k in list(model):
+            model[k] = [(cc, p) for cc, p in model[k] if p != page]
+            if not model[k]:
+                del model[k]
+
+    for step in range(6000):
+        op = rng.random()
+        if op < 0.45:
+            res = kv.allocate(0, int(rng.integers(0, 8)))
+            if res is None:
+                kv.evict_lru_large_page()
+            else:
+                used.append(res.page)
+            # allocation may evict cached pages itself (five-step allocate, kv_allocator.cpp:154-197)
+            for c, pg in [(c, pg) for c, pg in cached if not is_cached(pg)]:
+                unreg(pg)
+            cached = [(c, pg) for c, pg in cached if is_cached(pg)]
+        elif op < 0.8 and used:
+            page = used.pop(int(rng.integers(0, len(used))))
+            c = contents[int(rng.integers(0, len(contents)))]
+            kv.free(0, page, c)
+            model.setdefault(c.key, []).append((ckey(c), page))
+            cached.append((c, page))
+        elif op < 0.9 and cached:
+            c, page = cached.pop(int(rng.integers(0, len(cached))))
+            kv.pin(0, page, 99)
+            unreg(page)
+            used.append(page)
+        elif cached:
+            kv.evict_lru_large_page()
+            for c, pg in [(c, pg) for c, pg in cached if not is_cached(pg)]:
+                unreg(pg)
+            cached = [(c, pg) for c, pg in cached if is_cached(pg)]
+        if step % 50 == 0:
+            for c in contents[:60]:
+                want = model_find(c)
+                got = kv.cache_find(0, c)
+                assert (None if got is None else tuple(got)) == (None if want is None else tuple(want)), step
+            assert kv.cache_entries(0) == sum(len(v) for v in model.values())
+    kv.check_invariants()
