@@ -2,7 +2,7 @@
 # Per-kernel DRAM evidence for every kernel on the path (run under gpurun, 1 GPU):
 # device time + DRAM bytes read/written per launch, for each BASELINE config's
 # decode loop (eager launches so every kernel is its own ncu result) and the
-# chunked-prefill bench.  Summarise with: python profiles/summarize_ncu.py --dram <tag>
+# chunked-prefill bench.  Summarise with: python profiles/summarize_ncu.py --dram <tag> (writes profiles/<tag>_kernels_dram.md; the round-2 table is r02_all_kernels_dram.md)
 set -u
 OUT=${1:-gpurun_out/kernels}
 mkdir -p $OUT
