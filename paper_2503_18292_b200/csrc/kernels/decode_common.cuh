@@ -29,11 +29,21 @@ constexpr int kTilesPerSplit = 32;  // 512 tokens per CTA
 #ifndef JENGA_DECODE_RING_BYTES_D128
 #define JENGA_DECODE_RING_BYTES_D128 49152
 #endif
-constexpr int decode_ctas_per_sm(int head_dim) {
+__host__ __device__ constexpr int decode_ctas_per_sm(int head_dim) {
   return head_dim >= 256 ? JENGA_DECODE_CTAS_PER_SM_D256 : JENGA_DECODE_CTAS_PER_SM_D128;
 }
-constexpr int decode_ring_bytes(int head_dim) {
+__host__ __device__ constexpr int decode_ring_bytes(int head_dim) {
   return head_dim >= 256 ? JENGA_DECODE_RING_BYTES_D256 : JENGA_DECODE_RING_BYTES_D128;
+}
+// Consumer warps per CTA (each owns the stages s with s % CW == its index).
+#ifndef JENGA_DECODE_CONSUMERS_D256
+#define JENGA_DECODE_CONSUMERS_D256 4
+#endif
+#ifndef JENGA_DECODE_CONSUMERS_D128
+#define JENGA_DECODE_CONSUMERS_D128 4
+#endif
+__host__ __device__ constexpr int decode_consumer_warps(int head_dim) {
+  return head_dim >= 256 ? JENGA_DECODE_CONSUMERS_D256 : JENGA_DECODE_CONSUMERS_D128;
 }
 
 struct DecodeParams {
@@ -98,8 +108,9 @@ __device__ __forceinline__ Work assign_work(const DecodeParams& p, int b, int sp
   return w;
 }
 
+template <int CW = kConsumerWarps>
 __device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+  asm volatile("bar.sync 1, %0;\n" ::"n"(CW * 32) : "memory");
 }
 
 // Called by the 128 consumer threads after each warp w wrote its unnormalised
@@ -111,15 +122,15 @@ __device__ __forceinline__ void consumers_sync() {
 // HG KV heads per CTA: warp w holds local head w % HG of round w / HG, so
 // head hl merges warps {hl, hl + HG, ...}.  The CTA covers heads
 // [h0, h0 + HG); one ticket per (request, head group).
-template <typename T, int G, int D, int HG = 1>
+template <typename T, int G, int D, int HG = 1, int CW = kConsumerWarps>
 __device__ __forceinline__ void merge_epilogue(const DecodeParams& p, const float* s_acc, const float* s_ml,
                                                int* s_flag, int nsplit, int split, int b, int h0) {
-  constexpr int R = kConsumerWarps / HG;  // warps per head
-  consumers_sync();
+  constexpr int R = CW / HG;  // warps per head
+  consumers_sync<CW>();
   const int tid = threadIdx.x;
   const int64_t b_h0 = static_cast<int64_t>(b) * p.hkv + h0;
   T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(b) * p.hq + h0 * G) * D;
-  for (int i = tid; i < HG * G * D; i += kConsumerWarps * 32) {
+  for (int i = tid; i < HG * G * D; i += CW * 32) {
     const int hl = i / (G * D);
     const int j = i - hl * G * D;
     const int g = j / D;
@@ -149,15 +160,15 @@ __device__ __forceinline__ void merge_epilogue(const DecodeParams& p, const floa
   if (nsplit == 1) return;
 
   __threadfence();
-  consumers_sync();
+  consumers_sync<CW>();
   if (tid == 0) {
     const int ticket = atomicAdd(&p.counters[b_h0], 1);
     *s_flag = (ticket == nsplit - 1) ? 1 : 0;
   }
-  consumers_sync();
+  consumers_sync<CW>();
   if (*s_flag == 0) return;
   __threadfence();
-  for (int i = tid; i < HG * G * D; i += kConsumerWarps * 32) {
+  for (int i = tid; i < HG * G * D; i += CW * 32) {
     const int hl = i / (G * D);
     const int j = i - hl * G * D;
     const int g = j / D;

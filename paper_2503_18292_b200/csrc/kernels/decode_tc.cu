@@ -95,9 +95,10 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // parity two phases ahead and pass early.
 template <int D>
 constexpr int stages() {
+  constexpr int CW = decode_consumer_warps(D);
   constexpr int stage = 2 * kTile * D * 2;
-  constexpr int ns = (decode_ring_bytes(D) / stage) / kConsumerWarps * kConsumerWarps;
-  return ns < kConsumerWarps ? kConsumerWarps : (ns > 12 ? 12 : ns);
+  constexpr int ns = (decode_ring_bytes(D) / stage) / CW * CW;
+  return ns < CW ? CW : (ns > 12 ? 12 : ns);
 }
 
 // ------------------------------------------------------------ per-warp math
@@ -304,14 +305,15 @@ __device__ __forceinline__ int32_t tile_row(const DecodeParams& p, const int32_t
 // ------------------------------------------------------------ grid kernel
 // One CTA per (KV head, request, split).
 template <typename T, int D, int G, int NS>
-__global__ void __launch_bounds__(kThreads, decode_ctas_per_sm(D))
+__global__ void __launch_bounds__((decode_consumer_warps(D) + 1) * 32, decode_ctas_per_sm(D))
     paged_decode_tc_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int CW = decode_consumer_warps(D);
   static_assert(D % kBoxCols == 0, "head_dim must be a multiple of 64");
   static_assert(G <= 8, "at most 8 query heads per KV head (N = 8)");
-  static_assert(NS % kConsumerWarps == 0, "slots must map to fixed consumer warps");
+  static_assert(NS % CW == 0, "slots must map to fixed consumer warps");
   constexpr int TILE_BYTES = (D / kBoxCols) * kBoxBytes;  // 16 tokens x D x 2 B, one head
   constexpr int STAGE_BYTES = 2 * TILE_BYTES;
-  constexpr int MERGE_BYTES = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
+  constexpr int MERGE_BYTES = (CW * G * D + CW * G * 2) * 4;
   constexpr int RING = NS * STAGE_BYTES;
   constexpr int BAR_OFFSET = RING > MERGE_BYTES ? RING : MERGE_BYTES;
 
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, decode_ctas_per_sm(D))
 
   const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
-  if (warp == kConsumerWarps) {
+  if (warp == CW) {
     if (lane == 0) {  // producer: one elected lane
       jenga_dev::prefetch_tmap(&tmap);
       const uint64_t policy = jenga_dev::l2_policy_evict_first();
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, decode_ctas_per_sm(D))
   HeadState<D> hs;
   jenga_dev::pdl_wait();  // q and the workspace belong to the previous kernels until here
   head_begin<T, D, G>(hs, p, b, h, lane);
-  for (int it = warp; it < wk.t_count; it += kConsumerWarps) {
+  for (int it = warp; it < wk.t_count; it += CW) {
     const int st = it % NS;
     jenga_dev::mbar_wait(&full[st], (it / NS) & 1);
     uint8_t* stage = smem + st * STAGE_BYTES;
@@ -387,11 +389,11 @@ __global__ void __launch_bounds__(kThreads, decode_ctas_per_sm(D))
     __syncwarp();
     if (lane == 0) jenga_dev::mbar_arrive(&empty[st]);
   }
-  consumers_sync();
-  float* s_acc = reinterpret_cast<float*>(smem);  // [4][G][D] (the ring is drained)
-  float* s_ml = s_acc + kConsumerWarps * G * D;   // [4][G][2]
+  consumers_sync<CW>();
+  float* s_acc = reinterpret_cast<float*>(smem);  // [CW][G][D] (the ring is drained)
+  float* s_ml = s_acc + CW * G * D;               // [CW][G][2]
   head_store<D, G>(hs, s_acc, s_ml, warp, lane);
-  merge_epilogue<T, G, D>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h);
+  merge_epilogue<T, G, D, 1, CW>(p, s_acc, s_ml, s_flag, wk.nsplit, split, b, h);
 }
 
 // ------------------------------------------------------------ host side
@@ -451,13 +453,14 @@ int tensor_map(const void* base, int D, int dtype, int tpp, CUtensorMap* out) {
 template <typename T, int D, int G>
 int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaStream_t stream) {
   constexpr int STAGE = 2 * kTile * D * 2;
-  constexpr int MERGE = (kConsumerWarps * G * D + kConsumerWarps * G * 2) * 4;
+  constexpr int CW = decode_consumer_warps(D);
+  constexpr int MERGE = (CW * G * D + CW * G * 2) * 4;
   constexpr int NS = stages<D>();
   const int smem = std::max(NS * STAGE, MERGE) + 2 * NS * 8 + 16 + 1024;
   auto kern = paged_decode_tc_kernel<T, D, G, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  jenga_dev::launch_maybe_pdl(kern, decode_grid(prm, batch), dim3(kThreads), smem, stream, prm, tmap);
+  jenga_dev::launch_maybe_pdl(kern, decode_grid(prm, batch), dim3((CW + 1) * 32), smem, stream, prm, tmap);
   return jenga_dev::check_launch("paged_decode_tc_kernel");
 }
 
