@@ -391,7 +391,16 @@ int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view, int dtype,
                             const void* key, const void* value, int64_t kv_token_stride,
                             const int64_t* slot_mapping, int n_tokens, void* stream);
 
-/* Paged decode attention through the two-level table.
+/* PDL ordering: decode launches (jenga_paged_decode / _append) use programmatic
+ * dependent launch and may stream K/V tiles before their predecessor in the
+ * stream has finished.  The library tracks, per stream, whether a kernel that
+ * lets its dependents start early and writes arena bytes (jenga_reshape_and_cache,
+ * the page / state copies) is still in the PDL chain, and then makes the decode
+ * wait before its first load; every library launch on one stream is therefore
+ * ordered as issued.  Kernels of your own that write the arena between library
+ * launches must not use the programmatic-serialization attribute.
+ *
+ * Paged decode attention through the two-level table.
  *   kind: JENGA_KIND_FULL / SLIDING_WINDOW / CROSS_ATTENTION
  *   q[B][Hq][D], out[B][Hq][D] (dtype), block_table[B][max_blocks],
  *   seq_lens[B] = live length n (ordinals 1..n stored; SWA attends (n-W, n]).
