@@ -591,6 +591,12 @@ __device__ __forceinline__ void umma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint6
       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void umma2_ss(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
@@ -1252,6 +1258,432 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
 }
 
 
+// Number of the 8 exponentials per group of 8 S columns computed on the FMA pipe
+// (degree-3 polynomial) instead of the MUFU, in the 128-key kernel.
+#ifndef JENGA_PF_EMU
+#define JENGA_PF_EMU 0
+#endif
+
+// 2^x on the FMA pipe for x <= 0: round-to-nearest split x = j + f (f in
+// [-0.5, 0.5]) by the 1.5 * 2^23 shift, 2^f by a degree-3 minimax polynomial
+// (relative error < 1e-4, below the bf16 rounding of P), 2^j added into the
+// exponent field.  x below -126 flushes towards 0 like ex2.approx.ftz.
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float q = fmaf(0.0555041086f, f, 0.2402264923f);
+  q = fmaf(q, f, 0.6931471806f);
+  q = fmaf(q, f, 1.0f);
+  return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
+}
+
+template <typename T, int D, int G, int NQ, int NSK, int NSV>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2) * 32, 1)
+    paged_prefill_tc5_wide_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
+                                  const __grid_constant__ CUtensorMap v_map) {
+  // 128-key tiles on a CTA pair (cta_group::2, M = 256).  S = Q K^T is issued
+  // with N = 128 keys (the 64-key form runs the tensor core at ~72%: its
+  // instructions cannot be issued faster than ~45 cycles each), so Q moves
+  // to shared memory (SS MMA) and TMEM holds only accumulators:
+  //   NQ = 1 (head_dim 256): O (256 columns) + two S buffers (2 x 128);
+  //   NQ = 2 (head_dim 128): two 128-row query tiles A / B per CTA, each with
+  //          O (128) + one S buffer (128); the MMA issuer ping-pongs
+  //          PV_A(j), S_A(j+1), PV_B(j), S_B(j+1).
+  // K and V stream through separate rings (K of tile j+1 is needed before V of
+  // tile j): K slot released when the tile's S MMAs complete, V slot when its PV
+  // MMAs complete.  Shared-memory layouts (128-byte swizzle):
+  //   Q: [query tile][chunk c][128 rows][128 B]   (written by the softmax threads)
+  //   K: [8-key group][chunk c][8 rows][128 B]    (one 4-D TMA box per 16-key piece; this CTA's 64 keys)
+  //   V: [16-key piece][chunk c][16 rows][128 B]  (one 3-D box per piece; this CTA's half of head_dim)
+  constexpr int KT = 128;
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int VB = NBOX / 2;
+  constexpr int QB = kRows / G;
+  constexpr int KH = KT / 2;
+  constexpr int K_GROUP = NBOX * 8 * 128;
+  constexpr int K_BYTES = (KH / 8) * K_GROUP;
+  constexpr int V_PIECE = VB * kTile * 128;
+  constexpr int V_BYTES = (KT / kTile) * V_PIECE;
+  constexpr int Q_BYTES = NBOX * kRows * 128;
+  constexpr int NSB = 2 / NQ;                 // S buffers per query tile
+  constexpr int S_COL0 = NQ * D;
+  constexpr uint32_t TMEM_COLS = 512;
+  static_assert(NBOX % 2 == 0 && NQ * D + NQ * NSB * KT == 512, "128-key kernel shape");
+  constexpr int SW = NQ * kSoftWarps, PW = SW, MW = SW + 1;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* qs = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* kring = qs + NQ * Q_BYTES;
+  uint8_t* vring = kring + NSK * K_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vring + NSV * V_BYTES);
+  uint64_t* q_full = bars;                    // leader: all softmax warps of the pair
+  uint64_t* k_full = bars + 1;                // leader: both CTAs' TMA bytes
+  uint64_t* k_empty = k_full + NSK;           // both: multicast commit
+  uint64_t* v_full = k_empty + NSK;
+  uint64_t* v_empty = v_full + NSV;
+  uint64_t* s_full = v_empty + NSV;           // both: multicast commit      [tile][buffer]
+  uint64_t* p_full = s_full + NQ * NSB;       // leader: the tile's 8 softmax warps
+  uint64_t* p_empty = p_full + NQ * NSB;      // both: multicast commit
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NQ * NSB);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int unit = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
+  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
+  const int pt0 = 2 * NQ * unit * QB;
+  if (pt0 >= c_len) return;  // uniform over the pair
+  const int n = p.seq_lens[b];
+  const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
+  const int pos0 = n - c_len + pt0;
+  const int pos1 = n - c_len + min(pt0 + 2 * NQ * QB, c_len) - 1;  // union of the pair's query rows
+  int key_lo = 0;
+  const int key_hi = cross ? n - 1 : pos1;
+  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
+  const int tile_lo = key_lo / KT;
+  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    jenga_dev::mbar_init(q_full, 2 * SW);
+    for (int i = 0; i < NSK; ++i) {
+      jenga_dev::mbar_init(&k_full[i], 1);
+      jenga_dev::mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < NSV; ++i) {
+      jenga_dev::mbar_init(&v_full[i], 1);
+      jenga_dev::mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < NQ * NSB; ++i) {
+      jenga_dev::mbar_init(&s_full[i], 1);
+      jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
+      jenga_dev::mbar_init(&p_empty[i], 1);
+    }
+    jenga_dev::fence_mbar_init();
+  }
+  if (warp == MW) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     jenga_dev::smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
+
+  if (warp == PW) {
+    // Lane l < 8 owns the 16-key page piece l of every tile: its block index by
+    // multiply-shift division, its page from the warp's table look-ahead (lane i
+    // holds table[base + i] / table[base + 32 + i]) by one shuffle, its arena row
+    // by one multiply-add; the lanes then issue their own TMA boxes.
+    if (lane == 0) { jenga_dev::prefetch_tmap(&k_map); jenga_dev::prefetch_tmap(&v_map); }
+    const uint64_t policy = jenga_dev::l2_policy_evict_first();
+    const int64_t row_bytes = D * 2;
+    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
+    const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
+    const uint32_t tpp = static_cast<uint32_t>(p.tpp);
+    uint32_t lg = 0;
+    while ((1u << lg) < tpp) ++lg;
+    const uint32_t dm = static_cast<uint32_t>(((1ull << (31 + lg)) + tpp - 1) / tpp), ds = lg - 1;  // tpp >= 16
+    const int mb = p.max_blocks;
+    int base = static_cast<int>(static_cast<uint32_t>(tile_lo * KT) / tpp);
+    int cur = __ldg(table + min(base + lane, mb - 1)), nxt = __ldg(table + min(base + 32 + lane, mb - 1));
+    const int piece = lane & 7;
+    auto row_for = [&](int jj) {  // warp-uniform call; this lane's piece of tile jj
+      const uint32_t tok = static_cast<uint32_t>((tile_lo + jj) * KT + piece * kTile);
+      const int blk = static_cast<int>(__umulhi(tok, dm) >> ds);
+      const int off = static_cast<int>(tok - static_cast<uint32_t>(blk) * tpp);
+      const int blk0 = __shfl_sync(0xffffffffu, blk, 0);
+      while (blk0 >= base + 32) {
+        base += 32;
+        cur = nxt;
+        nxt = __ldg(table + min(base + 32 + lane, mb - 1));
+      }
+      const int rel = blk - base;  // < 64: a tile spans at most 8 blocks
+      const int a = __shfl_sync(0xffffffffu, cur, rel & 31), c = __shfl_sync(0xffffffffu, nxt, rel & 31);
+      const int32_t page = rel < 32 ? a : c;
+      return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + off);
+    };
+    const int k_lane0 = static_cast<int>(rank) * (KH / kTile);  // this CTA's half of the keys
+    auto issue_k = [&](int jj, int32_t row) {
+      const int st = jj % NSK;
+      if (jj >= NSK) jenga_dev::mbar_wait(&k_empty[st], ((jj / NSK) & 1) ^ 1);
+      const uint32_t full0 = map_to_cta0(&k_full[st]);
+      if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * K_BYTES);
+      if (lane >= k_lane0 && lane < k_lane0 + KH / kTile)
+        tma_load_4d_pair(kring + st * K_BYTES + (lane - k_lane0) * 2 * K_GROUP, &k_map, row, full0, policy);
+    };
+    auto issue_v = [&](int jj, int32_t row) {
+      const int st = jj % NSV;
+      if (jj >= NSV) jenga_dev::mbar_wait(&v_empty[st], ((jj / NSV) & 1) ^ 1);
+      const uint32_t full0 = map_to_cta0(&v_full[st]);
+      if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * V_BYTES);
+      if (lane < KT / kTile)
+        tma_load_3d_pair(vring + st * V_BYTES + lane * V_PIECE, &v_map, row + p.tpp, static_cast<int>(rank) * VB,
+                         full0, policy);
+    };
+    int32_t row_cur = 0, row_nxt = 0;
+    if (ntiles > 0) {
+      row_cur = row_for(0);
+      issue_k(0, row_cur);
+    }
+    for (int j = 0; j < ntiles; ++j) {
+      if (j + 1 < ntiles) {  // K runs one tile ahead of V
+        row_nxt = row_for(j + 1);
+        issue_k(j + 1, row_nxt);
+      }
+      issue_v(j, row_cur);
+      row_cur = row_nxt;
+    }
+  } else if (warp == MW) {
+    if (rank == 0 && lane == 0) {
+      const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
+      const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
+      // descriptors as base + constant (one add per MMA on the uniform datapath)
+      const uint64_t q_desc0 = umma_desc(jenga_dev::smem_u32(qs), 16, 1024);
+      const uint64_t k_desc0 = umma_desc(jenga_dev::smem_u32(kring), 16, K_GROUP);
+      const uint64_t v_desc0 = umma_desc(jenga_dev::smem_u32(vring), kTile * 128, 1024);
+      auto sidx = [&](int jj, int g) { return g * NSB + jj % NSB; };
+      auto issue_s = [&](int jj, int g) {  // S_g(jj) = Q_g K_jj^T (K slot already full)
+        const uint64_t kd = k_desc0 + ((jj % NSK) * K_BYTES >> 4);
+        const uint64_t qd = q_desc0 + (g * Q_BYTES >> 4);
+        const uint32_t d = tmem + S_COL0 + sidx(jj, g) * KT;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
+          umma2_ss(d, qd + (((k >> 2) * kRows * 128 + (k & 3) * 32) >> 4), kd + off, id_s, k > 0 ? 1u : 0u);
+        }
+        umma2_commit_both(&s_full[sidx(jj, g)]);
+      };
+      auto issue_pv = [&](int jj, int g) {  // O_g += P_g(jj) V_jj (V slot already full)
+        jenga_dev::mbar_wait(&p_full[sidx(jj, g)], (jj / NSB) & 1);
+        tc_fence_after();
+        const uint64_t vd = v_desc0 + ((jj % NSV) * V_BYTES >> 4);
+        const uint32_t a = tmem + S_COL0 + sidx(jj, g) * KT;
+#pragma unroll
+        for (int k = 0; k < KT / 16; ++k)
+          umma2_ts(tmem + g * D, a + k * 8, vd + (k * V_PIECE >> 4), id_o, (jj > 0 || k > 0) ? 1u : 0u);
+        umma2_commit_both(&p_empty[sidx(jj, g)]);
+      };
+      auto wait_v = [&](int jj) {
+        jenga_dev::mbar_wait(&v_full[jj % NSV], (jj / NSV) & 1);
+        tc_fence_after();
+      };
+      // boundary tiles (first / last) get V rows zeroed by the softmax threads after
+      // s_full: their S is issued only once V has landed too
+      auto wait_k = [&](int jj) {
+        jenga_dev::mbar_wait(&k_full[jj % NSK], (jj / NSK) & 1);
+        tc_fence_after();
+        const int kt0 = (tile_lo + jj) * KT;
+        if (kt0 < key_lo || kt0 + KT - 1 > key_hi) wait_v(jj);
+      };
+      jenga_dev::mbar_wait(q_full, 0);
+      tc_fence_after();
+      if constexpr (NQ == 1) {
+        // S(j+1) into the other buffer before O += P(j) V(j)
+        for (int j = 0; j < ntiles; ++j) {
+          wait_k(j);
+          issue_s(j, 0);
+          umma2_commit_both(&k_empty[j % NSK]);
+          if (j >= 1) {
+            wait_v(j - 1);
+            issue_pv(j - 1, 0);
+            umma2_commit_both(&v_empty[(j - 1) % NSV]);
+          }
+        }
+        if (ntiles > 0) {
+          wait_v(ntiles - 1);
+          issue_pv(ntiles - 1, 0);
+          umma2_commit_both(&v_empty[(ntiles - 1) % NSV]);
+        }
+      } else {
+        if (ntiles > 0) {
+          wait_k(0);
+          issue_s(0, 0);
+          issue_s(0, 1);
+          umma2_commit_both(&k_empty[0]);
+        }
+        for (int j = 0; j < ntiles; ++j) {
+          // S_g(j+1) overwrites S_g's buffer (P_g(j)): issued after PV_g(j), in order
+          wait_v(j);
+          issue_pv(j, 0);
+          if (j + 1 < ntiles) {
+            wait_k(j + 1);
+            issue_s(j + 1, 0);
+          }
+          issue_pv(j, 1);
+          umma2_commit_both(&v_empty[j % NSV]);
+          if (j + 1 < ntiles) {
+            issue_s(j + 1, 1);
+            umma2_commit_both(&k_empty[(j + 1) % NSK]);
+          }
+        }
+      }
+    }
+  } else {
+    const int grp = NQ == 2 ? warp >> 2 : 0;   // query tile of this softmax warpgroup
+    const int r = threadIdx.x & (kRows - 1);    // query row == TMEM lane
+    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int O_COL = grp * D;
+    const int t0 = pt0 + (NQ * grp + static_cast<int>(rank)) * QB;
+    const int tok = t0 + r / G;
+    const bool row_ok = tok < c_len;
+    const int ipos = n - c_len + tok;
+    const uint32_t p_full0 = map_to_cta0(&p_full[grp * NSB]);
+    {  // Q row -> shared memory, 128-byte swizzled K-major
+      const uint4* qrow = reinterpret_cast<const uint4*>(
+          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
+      uint8_t* qt = qs + grp * Q_BYTES + r * 128;
+#pragma unroll
+      for (int c = 0; c < NBOX; ++c) {
+        uint4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + u) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(qt + c * kRows * 128 + ((u ^ (r & 7)) << 4)) = x[u];
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) arrive_cta0_release(map_to_cta0(q_full));
+    }
+    int lo_r = 0, hi_r = cross ? n - 1 : ipos;
+    if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
+      lo_r = static_cast<int>(ipos + 1 - p.window);
+    if (!row_ok || hi_r < lo_r) lo_r = hi_r = 1 << 30;
+    const uint32_t span = static_cast<uint32_t>(hi_r - lo_r);
+    const bool softcap = p.cap_log2 > 0.f;
+    const float sc = softcap ? 1.f : p.qscale;
+    const float qi = p.qscale * p.inv_cap;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      const int sbi = grp * NSB + j % NSB;
+      const uint32_t s_addr = tmem + lane_addr + S_COL0 + sbi * KT;
+      const int ktok0 = (tile_lo + j) * KT;
+      jenga_dev::mbar_wait(&s_full[sbi], (j / NSB) & 1);
+      tc_fence_after();
+      float s[KT];
+      {
+        float* s0 = s;
+        tmem_ld64(s_addr, *reinterpret_cast<float(*)[64]>(s0));
+        tmem_ld64(s_addr + 64, *reinterpret_cast<float(*)[64]>(s0 + 64));
+      }
+      if (softcap) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
+      }
+      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i)
+          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
+      }
+      float m8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m8[i] = s[i];
+#pragma unroll
+      for (int i = 8; i < KT; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], s[i + u]);
+      }
+      float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      mt *= sc;
+      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+        const float m_new = fmaxf(m_used, mt);
+        if (j >= 1) {
+          const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
+          jenga_dev::mbar_wait(&p_empty[grp * NSB + (j - 1) % NSB], ((j - 1) / NSB) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + O_COL + c, v);
+            uint32_t u[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
+            tmem_st32u(tmem + lane_addr + O_COL + c, u);
+          }
+          tmem_st_wait();
+          l *= alpha;
+        }
+        m_used = m_new;
+      }
+      const float neg = m_used == -INFINITY ? 0.f : -m_used;
+      float rs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < KT; c += 64) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const float x0 = fmaf(s[c + i], sc, neg), x1 = fmaf(s[c + i + 1], sc, neg);
+          const float a = ((i & 7) >= 8 - JENGA_PF_EMU) ? exp2_fma(x0) : jenga_dev::fast_exp2(x0);
+          const float bb = (((i + 1) & 7) >= 8 - JENGA_PF_EMU) ? exp2_fma(x1) : jenga_dev::fast_exp2(x1);
+          rs[i & 7] += a;
+          rs[(i + 1) & 7] += bb;
+          pk[i / 2] = pack2<T>(a, bb);
+        }
+        tmem_st32u(s_addr + c / 2, pk);
+      }
+      l += ((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7]));
+      tmem_st_wait();
+      // zero this CTA's V columns of keys outside the pair's range (group A only:
+      // PV_B(j) is issued after PV_A(j)); the issuer waited for this tile's V
+      // before S(j), so s_full(j) implies it has landed
+      const bool boundary = grp == 0 && (ktok0 < key_lo || ktok0 + KT - 1 > key_hi);
+      if (boundary) {
+        uint8_t* vs = vring + (j % NSV) * V_BYTES;
+        for (int idx = r; idx < KT * VB; idx += kRows) {
+          const int vrow = idx % KT, chunk = idx / KT;
+          const int key = ktok0 + vrow;
+          if (key >= key_lo && key <= key_hi) continue;
+          uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
+                                                 (vrow % kTile) * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t pf = p_full0 + 8u * (j % NSB);
+        if (boundary)
+          arrive_cta0_release(pf);
+        else
+          arrive_cta0(pf);
+      }
+    }
+    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[grp * NSB + (ntiles - 1) % NSB], ((ntiles - 1) / NSB) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      float v[32];
+      if (ntiles > 0) {
+        tmem_ld32(tmem + lane_addr + O_COL + c, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
+                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
+                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
+                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's last remote arrivals and MMAs are done
+  if (warp == MW) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -1340,6 +1772,43 @@ int launch_tc5_pp(const Prefill5Params& prm, int dtype, cudaStream_t s, int batc
   return jenga_dev::check_launch("paged_prefill_tc5_pp_kernel");
 }
 
+template <typename T, int D, int G, int NQ, int NSK, int NSV>
+int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  constexpr int NBOX = D / kBoxCols;
+  constexpr int K_BYTES = (64 / 8) * NBOX * 8 * 128, V_BYTES = 8 * (NBOX / 2) * kTile * 128;
+  constexpr int Q_BYTES = NBOX * kRows * 128, NSB = 2 / NQ;
+  const int smem = NQ * Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + (1 + 2 * NSK + 2 * NSV + 3 * NQ * NSB) * 8 + 16 + 1024;
+  CUtensorMap k_map, v_map;
+  if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
+  auto kern = paged_prefill_tc5_wide_kernel<T, D, G, NQ, NSK, NSV>;
+  static std::atomic<uint64_t> configured{0};
+  if (int rc = configure_smem(kern, smem, configured)) return rc;
+  dim3 grid((prm.q_blocks + 2 * NQ - 1) / (2 * NQ) * 2, prm.hkv, batch);  // a CTA pair per 2 * NQ query blocks
+  kern<<<grid, (NQ * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map);
+  return jenga_dev::check_launch("paged_prefill_tc5_wide_kernel");
+}
+
+template <typename T, int D, int NQ, int NSK, int NSV>
+int dispatch_wide(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+  switch (G) {
+    case 1: return launch_tc5_wide<T, D, 1, NQ, NSK, NSV>(prm, dtype, s, batch);
+    case 2: return launch_tc5_wide<T, D, 2, NQ, NSK, NSV>(prm, dtype, s, batch);
+    case 4: return launch_tc5_wide<T, D, 4, NQ, NSK, NSV>(prm, dtype, s, batch);
+    case 8: return launch_tc5_wide<T, D, 8, NQ, NSK, NSV>(prm, dtype, s, batch);
+  }
+  return JENGA_ERR_UNSUPPORTED;
+}
+
+#ifndef JENGA_PF_WIDE
+#define JENGA_PF_WIDE 1
+#endif
+#ifndef JENGA_PF_NSK256
+#define JENGA_PF_NSK256 2
+#endif
+#ifndef JENGA_PF_NSV256
+#define JENGA_PF_NSV256 3
+#endif
+
 // Key-tile width of the ping-pong kernel: 64 keys (one S buffer per group) or 32
 // (two S buffers per group, twice the ring depth).
 #ifndef JENGA_PP_KT
@@ -1387,8 +1856,12 @@ int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int 
 template <typename T>
 int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (D) {
-    case 256: return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
-    case 128: return dispatch_pp<T, 128, 8>(G, prm, dtype, s, batch);
+    case 256:
+      if (JENGA_PF_WIDE) return dispatch_wide<T, 256, 1, JENGA_PF_NSK256, JENGA_PF_NSV256>(G, prm, dtype, s, batch);
+      return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
+    case 128:
+      if (JENGA_PF_WIDE) return dispatch_wide<T, 128, 2, 5, 5>(G, prm, dtype, s, batch);
+      return dispatch_pp<T, 128, 8>(G, prm, dtype, s, batch);
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
   }
   return jenga_dev::set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: head_dim must be 64, 128 or 256");

@@ -1,0 +1,320 @@
+// Microbenchmark: issue rate of tcgen05.mma.cta_group::{1,2}.kind::f16 (bf16
+// in, f32 accumulate) per instruction shape, A from TMEM (TS) or shared memory
+// (SS), B K-major or MN-major from shared memory.  One elected thread of the
+// leader CTA issues `iters` back-to-back MMAs into one accumulator and commits;
+// cycles are clock64 deltas from the first issue to the commit's mbarrier flip.
+// Also measures tcgen05.ld throughput (32x32b.x32, 4 / 8 / 16 warps).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o umma_shapes umma_shapes.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t idesc(int m, int n, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W;\n\t}\n" ::"r"(
+          su32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void csync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// MODE: 0 = TS (A in TMEM), 1 = SS (A in smem).  Fully unrolled groups of 16
+// MMAs with descriptors precomputed (base + constant), as a tuned issuer would.
+template <int CG, int M, int N, int MODE, int BMN>
+__global__ void mma_rate(int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* base = smem + ((1024 - (su32(smem) & 1023)) & 1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  uint32_t rank = CG == 2 ? ctarank() : 0;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(base)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  if (CG == 2) csync(); else __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = slot;
+  if (rank == 0 && threadIdx.x == 0) {
+    const uint32_t id = idesc(M, N, BMN);
+    const uint64_t da0 = desc(su32(base), 16, 1024);
+    const uint64_t db0 = BMN ? desc(su32(base + 32 * 1024), 16 * 128, 1024) : desc(su32(base + 32 * 1024), 16, 1024);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i += 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint64_t db = db0 + (BMN ? (k & 3) * 128 : (k & 3) * 2);
+        const uint64_t da = da0 + (k & 3) * 2;
+        const uint32_t acc = (i + k) > 0;
+        if constexpr (MODE == 0) {
+          if constexpr (CG == 2)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem),
+                         "r"(tmem + 256 + (k & 3) * 8), "l"(db), "r"(id), "r"(acc));
+          else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem),
+                         "r"(tmem + 256 + (k & 3) * 8), "l"(db), "r"(id), "r"(acc));
+        } else {
+          if constexpr (CG == 2)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                         "l"(da), "l"(db), "r"(id), "r"(acc));
+          else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                         "l"(da), "l"(db), "r"(id), "r"(acc));
+        }
+      }
+    }
+    if (CG == 2)
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+              su32(&bar)),
+          "h"((uint16_t)3)
+          : "memory");
+    else
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(&bar))
+                   : "memory");
+    long long t1 = clock64();
+    mbar_wait(&bar, 0);
+    long long t2 = clock64();
+    out[blockIdx.x * 2] = t2 - t0;
+    out[blockIdx.x * 2 + 1] = t1 - t0;
+  } else if (threadIdx.x == 0 && CG == 2) {
+    mbar_wait(&bar, 0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  if (CG == 2) csync(); else __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+// tcgen05.ld throughput: each warp reads its 32 lanes; NLD loads of 32x32b.xX
+// (X columns each) in flight behind one wait; 8 independent accumulators.
+template <int X, int NLD>
+__global__ void ld_rate(int passes, long long* out, float* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = slot + ((uint32_t)((warp & 3) * 32) << 16);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  __syncthreads();
+  long long t0 = clock64();
+  for (int p = 0; p < passes; ++p) {
+    uint32_t r[X * NLD];
+#pragma unroll
+    for (int l = 0; l < NLD; ++l) {
+      const uint32_t a = tmem + ((p + l + (warp >> 2)) * X) % 512;
+      if constexpr (X == 32)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+            : "=r"(r[l * X + 0]), "=r"(r[l * X + 1]), "=r"(r[l * X + 2]), "=r"(r[l * X + 3]), "=r"(r[l * X + 4]),
+              "=r"(r[l * X + 5]), "=r"(r[l * X + 6]), "=r"(r[l * X + 7]), "=r"(r[l * X + 8]), "=r"(r[l * X + 9]),
+              "=r"(r[l * X + 10]), "=r"(r[l * X + 11]), "=r"(r[l * X + 12]), "=r"(r[l * X + 13]), "=r"(r[l * X + 14]),
+              "=r"(r[l * X + 15]), "=r"(r[l * X + 16]), "=r"(r[l * X + 17]), "=r"(r[l * X + 18]), "=r"(r[l * X + 19]),
+              "=r"(r[l * X + 20]), "=r"(r[l * X + 21]), "=r"(r[l * X + 22]), "=r"(r[l * X + 23]), "=r"(r[l * X + 24]),
+              "=r"(r[l * X + 25]), "=r"(r[l * X + 26]), "=r"(r[l * X + 27]), "=r"(r[l * X + 28]), "=r"(r[l * X + 29]),
+              "=r"(r[l * X + 30]), "=r"(r[l * X + 31])
+            : "r"(a)
+            : "memory");
+      else
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];\n"
+            : "=r"(r[l * X + 0]), "=r"(r[l * X + 1]), "=r"(r[l * X + 2]), "=r"(r[l * X + 3]), "=r"(r[l * X + 4]),
+              "=r"(r[l * X + 5]), "=r"(r[l * X + 6]), "=r"(r[l * X + 7]), "=r"(r[l * X + 8]), "=r"(r[l * X + 9]),
+              "=r"(r[l * X + 10]), "=r"(r[l * X + 11]), "=r"(r[l * X + 12]), "=r"(r[l * X + 13]), "=r"(r[l * X + 14]),
+              "=r"(r[l * X + 15])
+            : "r"(a)
+            : "memory");
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < X * NLD; ++i) acc[i & 7] += __uint_as_float(r[i]);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 12345.f) sink[threadIdx.x] = s;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(slot));
+  }
+}
+
+// MUFU.EX2 vs an FMA-pipe exp2 (degree-3 polynomial, Cody-Waite): 8 independent chains.
+template <int POLY>
+__global__ void exp_rate(int iters, long long* out, float* sink) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float y;
+      if constexpr (POLY) {
+        const float t = x[i] + 12582912.f;          // round to nearest integer in the low mantissa bits
+        const float j = t - 12582912.f;
+        const float f = x[i] - j;                   // [-0.5, 0.5]
+        float p = fmaf(0.0555041086f, f, 0.2402264923f);
+        p = fmaf(p, f, 0.6931471806f);
+        p = fmaf(p, f, 1.0f);
+        y = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+      } else {
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[i]));
+      }
+      x[i] = y * -0.5f;
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.f) sink[threadIdx.x] = s;
+}
+
+int main() {
+  long long* d_out;
+  float* sink;
+  cudaMalloc(&d_out, 4096 * sizeof(long long));
+  cudaMalloc(&sink, 4096 * sizeof(float));
+  long long h[2 * 296];
+  const int smem = 100 * 1024;
+  const int iters = 4096;
+  auto run = [&](auto kern, int cg, int m, int n, int mode, int bmn) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int grid : {2, 296}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cg;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, iters, d_out);
+        if (e != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+          printf("launch failed %s\n", cudaGetErrorString(cudaGetLastError()));
+          exit(1);
+        }
+      }
+      cudaMemcpy(h, d_out, sizeof(long long) * 2 * grid, cudaMemcpyDeviceToHost);
+      double tot = 0, iss = 0;
+      int cnt = 0;
+      for (int i = 0; i < grid; i += cg) { tot += h[2 * i]; iss += h[2 * i + 1]; ++cnt; }
+      tot /= cnt; iss /= cnt;
+      const double flop_per_sm_clk = 2.0 * m * n * 16 * iters / tot / cg;
+      printf("{\"cg\": %d, \"m\": %d, \"n\": %d, \"a\": \"%s\", \"b\": \"%s\", \"grid\": %d, \"cyc_per_mma\": %.1f, "
+             "\"issue_cyc_per_mma\": %.1f, \"flop_per_sm_clk\": %.0f, \"frac_of_8192\": %.3f}\n",
+             cg, m, n, mode ? "smem" : "tmem", bmn ? "mn" : "k", grid, tot / iters, iss / iters,
+             flop_per_sm_clk, flop_per_sm_clk / 8192);
+    }
+  };
+  run(mma_rate<2, 256, 64, 0, 0>, 2, 256, 64, 0, 0);
+  run(mma_rate<2, 256, 128, 0, 0>, 2, 256, 128, 0, 0);
+  run(mma_rate<2, 256, 256, 0, 0>, 2, 256, 256, 0, 0);
+  run(mma_rate<2, 256, 64, 1, 0>, 2, 256, 64, 1, 0);
+  run(mma_rate<2, 256, 128, 1, 0>, 2, 256, 128, 1, 0);
+  run(mma_rate<2, 256, 256, 1, 0>, 2, 256, 256, 1, 0);
+  run(mma_rate<2, 256, 128, 0, 1>, 2, 256, 128, 0, 1);
+  run(mma_rate<2, 256, 256, 0, 1>, 2, 256, 256, 0, 1);
+  run(mma_rate<1, 128, 64, 0, 0>, 1, 128, 64, 0, 0);
+  run(mma_rate<1, 128, 128, 0, 0>, 1, 128, 128, 0, 0);
+  run(mma_rate<1, 128, 256, 0, 0>, 1, 128, 256, 0, 0);
+  run(mma_rate<1, 128, 128, 1, 0>, 1, 128, 128, 1, 0);
+  run(mma_rate<1, 128, 256, 1, 0>, 1, 128, 256, 1, 0);
+  auto ld = [&](auto kern, int x, int nld) {
+    for (int warps : {4, 8, 16}) {
+      const int passes = 2048;
+      kern<<<148, warps * 32>>>(passes, d_out, sink);
+      kern<<<148, warps * 32>>>(passes, d_out, sink);
+      if (cudaDeviceSynchronize() != cudaSuccess) { printf("ld failed\n"); exit(1); }
+      cudaMemcpy(h, d_out, sizeof(long long) * 148, cudaMemcpyDeviceToHost);
+      double tot = 0;
+      for (int i = 0; i < 148; ++i) tot += h[i];
+      tot /= 148;
+      const double bytes = (double)warps * 32 * x * nld * 4 * passes;
+      printf("{\"tmem_ld\": \"32x32b.x%d x%d per wait\", \"warps\": %d, \"bytes_per_clk_per_sm\": %.1f, "
+             "\"cyc_per_pass\": %.1f}\n", x, nld, warps, bytes / tot, tot / passes);
+    }
+  };
+  ld(ld_rate<32, 1>, 32, 1);
+  ld(ld_rate<32, 2>, 32, 2);
+  ld(ld_rate<32, 4>, 32, 4);
+  ld(ld_rate<16, 4>, 16, 4);
+  auto ex = [&](auto kern, const char* name) {
+    for (int warps : {4, 8, 16}) {
+      const int iters = 1024;
+      kern<<<148, warps * 32>>>(iters, d_out, sink);
+      kern<<<148, warps * 32>>>(iters, d_out, sink);
+      if (cudaDeviceSynchronize() != cudaSuccess) { printf("exp failed\n"); exit(1); }
+      cudaMemcpy(h, d_out, sizeof(long long) * 148, cudaMemcpyDeviceToHost);
+      double tot = 0;
+      for (int i = 0; i < 148; ++i) tot += h[i];
+      tot /= 148;
+      printf("{\"exp2\": \"%s\", \"warps\": %d, \"per_clk_per_sm\": %.2f}\n", name, warps,
+             (double)warps * 32 * 8 * iters / tot);
+    }
+  };
+  ex(exp_rate<0>, "mufu");
+  ex(exp_rate<1>, "poly3");
+  return 0;
+}
