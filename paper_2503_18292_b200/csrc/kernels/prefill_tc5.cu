@@ -1,34 +1,21 @@
 // Chunked-prefill paged attention on the 5th-generation tensor cores
-// (tcgen05.mma + TMEM), bf16/fp16.  Same contract as prefill.cu (which keeps
-// the mma.sync path for comparison, JENGA_PREFILL_TC5=0).
-//
-// Three kernels share the algorithm; rows are (token, query head) pairs
-// r = t*G + g as in prefill.cu, 128 rows per query block:
-//  * paged_prefill_tc5_pair_kernel (head_dim 256, default): a cluster of 2 CTAs,
-//    tcgen05.mma.cta_group::2 with M = 256 over two adjacent query blocks; each
-//    SM holds half of every K/V tile (its half of the keys for K, its half of
-//    head_dim for V).
-//  * paged_prefill_tc5_pp_kernel (head_dim 128, default): the same pair, each
-//    CTA holding TWO query blocks (A, B) with their own O / Q / S in TMEM and
-//    their own softmax warpgroup; the MMA issuer ping-pongs between them.
-//  * paged_prefill_tc5_kernel (head_dim 64, or JENGA_PREFILL_2SM=0): one CTA
-//    per query block, cta_group::1.
-// Warp roles (pair / single: 6 warps; ping-pong: 10):
-//   softmax    thread r owns query row r = TMEM lane r of S and O (32x32b
-//              tcgen05.ld); scores masked with the reference liveness rule
-//              (layer_policies.cpp:105-120), exponentiated against a lazily
-//              updated row max (O rescaled in TMEM only when the max grows by
-//              more than 2^8); P written back over its S columns (tcgen05.st) —
-//              the TMEM A operand of O += P V.
-//   producer   one warp walks the block table (warp-shuffled look-ahead); lane 0
-//              issues one 4-D TMA box per 16-key page piece of K and one 3-D box
-//              per piece of V (128-byte swizzle) into a ring of K/V stages.
-//   MMA        one elected thread, TMEM owner:
-//                S = Q . K_j^T   (A = Q from TMEM, B = K K-major)
-//                O += P_j . V_j  (A = P from TMEM, B = V MN-major)
-//              S_{j+1} issued before O += P_j V_j; tcgen05.commit releases K/V
-//              stages and S/P buffers.
-// TMEM: O in columns [0, D), Q after it (D/2 packed columns), then S buffers.
+// (tcgen05.mma + TMEM), bf16/fp16.  Rows are (token, query head) pairs
+// r = t*G + g, 128 rows per query block.  Two kernels:
+//  * paged_prefill_tc5_wide_kernel (head_dim 128 and 256): a cluster of 2 CTAs,
+//    tcgen05.mma.cta_group::2 with M = 256 over two adjacent query blocks, 128-key
+//    tiles (S = Q K^T issued with N = 128), Q in shared memory, TMEM = O plus
+//    (512 - D) / 128 S buffers so S runs ahead of the softmax; each SM holds half
+//    of every K/V tile (its 64 keys of K, its half of head_dim of V); 8 softmax
+//    warps (two per TMEM lane quarter, each owning half of the key columns), a
+//    TMA producer warp and a whole-warp MMA issuer.
+//  * paged_prefill_tc5_kernel (head_dim 64): one CTA per query block,
+//    cta_group::1, 64-key tiles, Q in TMEM (its single 64-column chunk is too
+//    narrow to split V across a pair).
+// Softmax (both): thread r owns query row r = TMEM lane r of S and O
+// (32x32b tcgen05.ld); scores masked with the reference liveness rule
+// (layer_policies.cpp:105-120), exponentiated against a lazily updated row max
+// (O rescaled in TMEM only when the max grows by more than 2^8); P written back
+// over its S columns (tcgen05.st) -- the TMEM A operand of O += P V.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -50,7 +37,6 @@ constexpr int kSoftWarps = 4;
 constexpr int kProducerWarp = 4;
 constexpr int kMmaWarp = 5;
 constexpr int kT5Threads = 6 * 32;
-constexpr int kPPThreads = 10 * 32;  // ping-pong pair kernel: 8 softmax warps + producer + MMA
 constexpr int kBoxCols = 64;
 constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescales
 
@@ -163,14 +149,6 @@ __device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_st16u(uint32_t addr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16};\n" ::"r"(addr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -551,17 +529,15 @@ __device__ __forceinline__ void arrive_cta0(uint32_t cluster_bar) {
 __device__ __forceinline__ void arrive_cta0_release(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
 }
+// Cluster-scope release arrive out of line: inlined under a branch, ptxas
+// predicates its MEMBAR.GPU / ERRBAR sequence, whose fixed stall cycles are paid
+// even when predicated off (~5% of the 128-key kernel).
+__device__ __noinline__ void arrive_cta0_release_ool(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
 __device__ __forceinline__ void expect_tx_cta0(uint32_t cluster_bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;\n" ::"r"(cluster_bar), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, int32_t c0, int32_t c1,
-                                                 uint32_t cluster_bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(jenga_dev::smem_u32(dst)),
-      "l"(tmap), "r"(cluster_bar), "r"(c0), "r"(c1), "l"(policy)
-      : "memory");
 }
 // 3-D box over the arena viewed as [chunk][row][64 cols] (dim0 = 64 columns,
 // dim1 = rows at row_bytes, dim2 = 64-column chunks at 128 B): one TMA covers
@@ -584,718 +560,99 @@ __device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* tmap, in
       "l"(tmap), "r"(cluster_bar), "r"(0), "r"(row), "r"(0), "r"(0), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void umma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
-                                         uint32_t acc) {
+
+#ifdef JENGA_PF_TRACE
+// Profiling-only (variant builds): clock64 stamps of the pipeline events of the
+// first CTA pair's leader, [event][tile] for tiles < 64.
+__device__ long long g_pf_trace[16][64];
+#define PF_TRACE(ev, j) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64) g_pf_trace[ev][j] = clock64(); } while (0)
+#else
+#define PF_TRACE(ev, j) do { } while (0)
+#endif
+
+// Whole-warp forms: the warp runs the issue loop convergently (operands are
+// warp-uniform, so they stay in uniform registers) and elect.sync picks the one
+// issuing lane inside the asm -- no per-instruction ELECT / BRA.U.ANY loop or
+// R2UR round trips, which capped the single-thread issuer at ~90 cycles per MMA.
+__device__ __forceinline__ void umma2_ss_w(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void umma2_ss(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+__device__ __forceinline__ void umma2_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                           uint32_t acc) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_commit_both_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
           jenga_dev::smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
       : "memory");
 }
 
-template <typename T, int D, int G, int KT, int NS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT5Threads, 1)
-    paged_prefill_tc5_pair_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
-                                  const __grid_constant__ CUtensorMap v_map) {
-  // Shared-memory layouts (all 128-byte swizzled, one TMA box per group / piece):
-  //   K: [8-key group g][chunk c][8 rows][128 B]  (k_map 4-D box {64, 8, NBOX, 2}: one 16-key piece);
-  //      the K-major descriptor walks chunks at 1 KiB, 8-key groups at SBO = NBOX KiB
-  //   V: [16-key piece][chunk c][16 rows][128 B]  (v_map box {64, 16, VB});
-  //      the MN-major descriptor walks chunks at LBO = 2 KiB, 8-key groups at 1 KiB
-  constexpr int NBOX = D / kBoxCols;
-  constexpr int VB = NBOX / 2;                // V column chunks held by each CTA
-  constexpr int QB = kRows / G;
-  constexpr int KH = KT / 2;                  // keys of the K tile held by each CTA
-  constexpr int K_GROUP = NBOX * 8 * 128;     // one 8-key group, all chunks
-  constexpr int K_BYTES = (KH / 8) * K_GROUP;
-  constexpr int V_PIECE = VB * kTile * 128;   // one 16-key piece, this CTA's chunks
-  constexpr int V_BYTES = (KT / kTile) * V_PIECE;
-  constexpr int STAGE = K_BYTES + V_BYTES;
-  constexpr int Q_COL = D, S_COL = D + D / 2;
-  constexpr uint32_t TMEM_COLS = 512;
-  static_assert(NBOX % 2 == 0 && KT == 64 && S_COL + 2 * KT <= 512, "pair kernel shape");
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
-  uint64_t* q_full = bars;                    // leader: 8 softmax warps of the pair
-  uint64_t* kv_full = bars + 1;               // leader: both CTAs' TMA bytes
-  uint64_t* kv_empty = kv_full + NS;          // both: multicast commit
-  uint64_t* s_full = kv_empty + NS;           // both: multicast commit
-  uint64_t* p_full = s_full + 2;              // leader: 8 softmax warps of the pair
-  uint64_t* p_empty = p_full + 2;             // both: multicast commit
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int pair = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
-  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
-  const int pt0 = 2 * pair * QB;
-  if (pt0 >= c_len) return;  // uniform over the pair
-  const int n = p.seq_lens[b];
-  const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
-  const int pos0 = n - c_len + pt0;
-  const int pos1 = n - c_len + min(pt0 + 2 * QB, c_len) - 1;
-  int key_lo = 0;
-  const int key_hi = cross ? n - 1 : pos1;
-  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
-  const int tile_lo = key_lo / KT;
-  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
-  const int t0 = pt0 + static_cast<int>(rank) * QB;
-
-  if (threadIdx.x == 0) {
-    jenga_dev::mbar_init(q_full, 2 * kSoftWarps);
-    for (int i = 0; i < NS; ++i) {
-      jenga_dev::mbar_init(&kv_full[i], 1);
-      jenga_dev::mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      jenga_dev::mbar_init(&s_full[i], 1);
-      jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
-      jenga_dev::mbar_init(&p_empty[i], 1);
-    }
-    jenga_dev::fence_mbar_init();
-  }
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     jenga_dev::smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
-  }
-  tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
-
-  if (warp == kProducerWarp) {  // the whole warp walks the table; lane 0 issues
-    if (lane == 0) { jenga_dev::prefetch_tmap(&k_map); jenga_dev::prefetch_tmap(&v_map); }
-    const uint64_t policy = jenga_dev::l2_policy_evict_first();
-    const int64_t row_bytes = D * 2;
-    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
-    const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
-    PageLookahead pl;
-    pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
-    // pages of one tile (KT / tpp <= 4 for tpp >= 16), looked up once in key order
-    auto row_of = [&](int32_t page, int tok) {
-      return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
-    };
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j % NS;
-      if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
-      const uint32_t full0 = map_to_cta0(&kv_full[st]);
-      if (rank == 0 && lane == 0) expect_tx_cta0(full0, 2 * STAGE);
-      uint8_t* ks = ring + st * STAGE;
-      uint8_t* vs = ks + K_BYTES;
-      const int ktok0 = (tile_lo + j) * KT;
-      int32_t pages[KT / kTile];
-#pragma unroll
-      for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
-      if (lane == 0) {
-#pragma unroll
-        for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys, a page piece each
-          const int kk = static_cast<int>(rank) * KH + pc * kTile;   // key offset within the tile
-          const int32_t pg = rank ? pages[KH / kTile + pc] : pages[pc];
-          tma_load_4d_pair(ks + pc * 2 * K_GROUP, &k_map, row_of(pg, ktok0 + kk), full0, policy);
-        }
-#pragma unroll
-        for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim
-          const int32_t row = row_of(pages[pc], ktok0 + pc * kTile) + p.tpp;
-          tma_load_3d_pair(vs + pc * V_PIECE, &v_map, row, static_cast<int>(rank) * VB, full0, policy);
-        }
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    if (rank == 0 && lane == 0) {
-      const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
-      const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
-      auto issue_pv = [&](int jj) {
-        const int sb = jj & 1;
-        jenga_dev::mbar_wait(&p_full[sb], (jj >> 1) & 1);
-        tc_fence_after();
-        const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + K_BYTES);
-#pragma unroll
-        for (int k = 0; k < KT / 16; ++k)
-          umma2_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o,
-                   (jj > 0 || k > 0) ? 1u : 0u);
-        umma2_commit_both(&p_empty[sb]);
-        umma2_commit_both(&kv_empty[jj % NS]);
-      };
-      jenga_dev::mbar_wait(q_full, 0);
-      for (int j = 0; j < ntiles; ++j) {
-        const int st = j % NS, sb = j & 1;
-        jenga_dev::mbar_wait(&kv_full[st], (j / NS) & 1);
-        tc_fence_after();
-        const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          umma2_ts(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
-                   umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
-        umma2_commit_both(&s_full[sb]);
-        if (j >= 1) issue_pv(j - 1);
-      }
-      if (ntiles > 0) issue_pv(ntiles - 1);
-    }
-  } else {
-    const int r = threadIdx.x;
-    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
-    const int tok = t0 + r / G;
-    const bool row_ok = tok < c_len;
-    const int ipos = n - c_len + tok;
-    const uint32_t q_full0 = map_to_cta0(q_full);
-    const uint32_t p_full0_base = map_to_cta0(&p_full[0]);  // the leader's p_full[i] = base + 8 i
-    {
-      const uint4* qrow = reinterpret_cast<const uint4*>(
-          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t w[32];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 x = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + i) : make_uint4(0, 0, 0, 0);
-          w[4 * i] = x.x;
-          w[4 * i + 1] = x.y;
-          w[4 * i + 2] = x.z;
-          w[4 * i + 3] = x.w;
-        }
-        tmem_st32u(tmem + lane_addr + Q_COL + c * 32, w);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) arrive_cta0(q_full0);
-    }
-    int lo_r = 0, hi_r = cross ? n - 1 : ipos;
-    if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
-      lo_r = static_cast<int>(ipos + 1 - p.window);
-    if (!row_ok || hi_r < lo_r) lo_r = hi_r = 1 << 30;
-    const uint32_t span = static_cast<uint32_t>(hi_r - lo_r);
-    const bool softcap = p.cap_log2 > 0.f;
-    const float sc = softcap ? 1.f : p.qscale;
-    const float qi = p.qscale * p.inv_cap;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
-      const int sb = j & 1;
-      const int ktok0 = (tile_lo + j) * KT;
-      jenga_dev::mbar_wait(&s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      static_assert(KT == 64, "one 64-column S load");
-      float s[KT];
-      tmem_ld64(tmem + lane_addr + S_COL + sb * KT, s);  // both halves behind one wait
-      if (softcap) {
-#pragma unroll
-        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
-      }
-      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {
-#pragma unroll
-        for (int i = 0; i < KT; ++i)
-          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
-      }
-      float mt = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < KT; ++i) mt = fmaxf(mt, s[i]);
-      mt *= sc;
-      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
-        const float m_new = fmaxf(m_used, mt);
-        if (j >= 1) {
-          const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
-          jenga_dev::mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
-            float v[32];
-            tmem_ld32(tmem + lane_addr + c, v);
-            uint32_t u[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
-            tmem_st32u(tmem + lane_addr + c, u);
-          }
-          tmem_st_wait();
-          l *= alpha;
-        }
-        m_used = m_new;
-      }
-      uint32_t pk[KT / 2];
-      float rs0 = 0.f, rs1 = 0.f;
-      const float neg = m_used == -INFINITY ? 0.f : -m_used;
-#pragma unroll
-      for (int i = 0; i < KT; i += 2) {
-        const float a = jenga_dev::fast_exp2(fmaf(s[i], sc, neg));
-        const float bb = jenga_dev::fast_exp2(fmaf(s[i + 1], sc, neg));
-        rs0 += a;
-        rs1 += bb;
-        pk[i / 2] = pack2<T>(a, bb);
-      }
-      l += rs0 + rs1;
-#pragma unroll
-      for (int c = 0; c < KT / 2; c += 32) {
-        uint32_t w[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
-        tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
-      }
-      tmem_st_wait();
-      // zero this CTA's V columns of keys outside the pair's range
-      const bool boundary = ktok0 < key_lo || ktok0 + KT - 1 > key_hi;
-      if (boundary) {
-        uint8_t* vs = ring + (j % NS) * STAGE + K_BYTES;
-        for (int idx = r; idx < KT * VB; idx += kRows) {
-          const int vrow = idx % KT, chunk = idx / KT;
-          const int key = ktok0 + vrow;
-          if (key >= key_lo && key <= key_hi) continue;
-          uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
-                                                 (vrow % kTile) * 128);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
-        }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (boundary)
-          arrive_cta0_release((p_full0_base + 8u * sb));
-        else
-          arrive_cta0((p_full0_base + 8u * sb));
-      }
-    }
-    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
-#pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
-      float v[32];
-      if (ntiles > 0) {
-        tmem_ld32(tmem + lane_addr + c, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      if (row_ok) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
-                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
-                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
-                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
-      }
-    }
-  }
-  tc_fence_before();
-  cluster_sync();  // the peer's last remote arrivals and MMAs are done
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
-  }
+// Packed f32x2 FMA / add (FFMA2 / FADD2 on sm_100a: two lanes per issue slot).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.ftz.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.ftz.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// exp2_fma for two lanes, the polynomial on FFMA2.
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 f = fadd2(x, fadd2(make_float2(12582912.f, 12582912.f), make_float2(-t.x, -t.y)));
+  float2 q = ffma2(make_float2(0.0555041086f, 0.0555041086f), f, make_float2(0.2402264923f, 0.2402264923f));
+  q = ffma2(q, f, make_float2(0.6931471806f, 0.6931471806f));
+  q = ffma2(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <typename T, int D, int G, int KT, int NS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPPThreads, 1)
-    paged_prefill_tc5_pp_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
-                                const __grid_constant__ CUtensorMap v_map) {
-  // Ping-pong variant of the CTA-pair kernel for head_dim <= 128: each CTA holds
-  // TWO 128-row query tiles (A: query blocks 4q + rank, B: 4q + 2 + rank) with
-  // their own O, Q and S in TMEM and their own softmax warpgroup (warps 0-3: A,
-  // 4-7: B).  Every K/V tile feeds both, and the MMA issuer interleaves
-  //   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
-  // so one group's softmax runs while the tensor core works on the other's tile.
-  // Shared-memory layouts (all 128-byte swizzled, one TMA box per group / piece):
-  //   K: [8-key group g][chunk c][8 rows][128 B]  (k_map 4-D box {64, 8, NBOX, 2}: one 16-key piece);
-  //      the K-major descriptor walks chunks at 1 KiB, 8-key groups at SBO = NBOX KiB
-  //   V: [16-key piece][chunk c][16 rows][128 B]  (v_map box {64, 16, VB});
-  //      the MN-major descriptor walks chunks at LBO = 2 KiB, 8-key groups at 1 KiB
-  constexpr int NBOX = D / kBoxCols;
-  constexpr int VB = NBOX / 2;                // V column chunks held by each CTA
-  constexpr int QB = kRows / G;
-  constexpr int KH = KT / 2;                  // keys of the K tile held by each CTA
-  constexpr int K_GROUP = NBOX * 8 * 128;     // one 8-key group, all chunks
-  constexpr int K_BYTES = (KH / 8) * K_GROUP;
-  constexpr int V_PIECE = VB * kTile * 128;   // one 16-key piece, this CTA's chunks
-  constexpr int V_BYTES = (KT / kTile) * V_PIECE;
-  constexpr int STAGE = K_BYTES + V_BYTES;
-  // TMEM per CTA: O_A | O_B | Q_A | Q_B | S buffers (NSB per group).  With 64-key
-  // tiles there is room for one S buffer per group, so S_g(j+1) can only start once
-  // PV_g(j) consumed P_g(j) and each group's softmax -> PV -> S chain is serial;
-  // with 32-key tiles two buffers per group fit, S_g(j+1) is computed while the
-  // softmax of tile j runs, and the chain is only softmax -> PV.
-  constexpr int NSB = KT == 32 ? 2 : 1;
-  constexpr int O_COL0 = 0, Q_COL0 = 2 * D, S_COL0 = 3 * D;
-  constexpr uint32_t TMEM_COLS = 512;
-  static_assert(NBOX % 2 == 0 && (KT == 64 || KT == 32) && 3 * D + 2 * NSB * KT <= 512, "ping-pong kernel shape");
-  constexpr int PW = 8, MW = 9;               // producer, MMA warps (0-7 softmax)
-
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* ring = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + NS * STAGE);
-  uint64_t* q_full = bars;                    // leader: 16 softmax warps of the pair
-  uint64_t* kv_full = bars + 1;               // leader: both CTAs' TMA bytes
-  uint64_t* kv_empty = kv_full + NS;          // both: multicast commit
-  uint64_t* s_full = kv_empty + NS;           // both: multicast commit      [group][buffer]
-  uint64_t* p_full = s_full + 2 * NSB;        // leader: 8 softmax warps    [group][buffer]
-  uint64_t* p_empty = p_full + 2 * NSB;       // both: multicast commit      [group][buffer]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + 2 * NSB);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const int quad = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
-  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
-  const int pt0 = 4 * quad * QB;
-  if (pt0 >= c_len) return;  // uniform over the pair
-  const int n = p.seq_lens[b];
-  const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
-  const int pos0 = n - c_len + pt0;
-  const int pos1 = n - c_len + min(pt0 + 4 * QB, c_len) - 1;  // union of both tiles' keys
-  int key_lo = 0;
-  const int key_hi = cross ? n - 1 : pos1;
-  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
-  const int tile_lo = key_lo / KT;
-  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
-
-  if (threadIdx.x == 0) {
-    jenga_dev::mbar_init(q_full, 2 * 2 * kSoftWarps);
-    for (int i = 0; i < NS; ++i) {
-      jenga_dev::mbar_init(&kv_full[i], 1);
-      jenga_dev::mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2 * NSB; ++i) {
-      jenga_dev::mbar_init(&s_full[i], 1);
-      jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
-      jenga_dev::mbar_init(&p_empty[i], 1);
-    }
-    jenga_dev::fence_mbar_init();
-  }
-  if (warp == MW) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     jenga_dev::smem_u32(tmem_slot)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
-  }
-  tc_fence_before();
-  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
-
-  if (warp == PW) {  // the whole warp walks the table; lane 0 issues
-    if (lane == 0) { jenga_dev::prefetch_tmap(&k_map); jenga_dev::prefetch_tmap(&v_map); }
-    const uint64_t policy = jenga_dev::l2_policy_evict_first();
-    const int64_t row_bytes = D * 2;
-    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
-    const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
-    PageLookahead pl;
-    pl.init(table, p.max_blocks, tile_lo * KT / p.tpp, lane);
-    // pages of one tile (KT / tpp <= 4 for tpp >= 16), looked up once in key order
-    auto row_of = [&](int32_t page, int tok) {
-      return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + tok % p.tpp);
-    };
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j % NS;
-      if (j >= NS) jenga_dev::mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
-      const uint32_t full0 = map_to_cta0(&kv_full[st]);
-      if (rank == 0 && lane == 0) expect_tx_cta0(full0, 2 * STAGE);
-      uint8_t* ks = ring + st * STAGE;
-      uint8_t* vs = ks + K_BYTES;
-      const int ktok0 = (tile_lo + j) * KT;
-      int32_t pages[KT / kTile];
-#pragma unroll
-      for (int pc = 0; pc < KT / kTile; ++pc) pages[pc] = pl.get((ktok0 + pc * kTile) / p.tpp, lane);
-      if (lane == 0) {
-#pragma unroll
-        for (int pc = 0; pc < KH / kTile; ++pc) {  // this CTA's half of the keys, a page piece each
-          const int kk = static_cast<int>(rank) * KH + pc * kTile;   // key offset within the tile
-          const int32_t pg = rank ? pages[KH / kTile + pc] : pages[pc];
-          tma_load_4d_pair(ks + pc * 2 * K_GROUP, &k_map, row_of(pg, ktok0 + kk), full0, policy);
-        }
-#pragma unroll
-        for (int pc = 0; pc < KT / kTile; ++pc) {  // all keys, this CTA's half of head_dim
-          const int32_t row = row_of(pages[pc], ktok0 + pc * kTile) + p.tpp;
-          tma_load_3d_pair(vs + pc * V_PIECE, &v_map, row, static_cast<int>(rank) * VB, full0, policy);
-        }
-      }
-    }
-  } else if (warp == MW) {
-    if (rank == 0 && lane == 0) {
-      const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
-      const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
-      // S_g(jj) lands in buffer jj % NSB of group g; its barriers are [g * NSB + jj % NSB],
-      // each used every NSB tiles (phase = (jj / NSB) & 1)
-      auto scol = [&](int jj, int g) { return S_COL0 + (g * NSB + jj % NSB) * KT; };
-      auto issue_s = [&](int jj, int g) {  // S_g(jj) = Q_g K_jj^T (K stage already full)
-        const uint32_t k_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          umma2_ts(tmem + scol(jj, g), tmem + Q_COL0 + g * (D / 2) + k * 8,
-                   umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
-        umma2_commit_both(&s_full[g * NSB + jj % NSB]);
-      };
-      auto issue_pv = [&](int jj, int g) {  // O_g += P_g(jj) V_jj
-        jenga_dev::mbar_wait(&p_full[g * NSB + jj % NSB], (jj / NSB) & 1);
-        tc_fence_after();
-        const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + K_BYTES);
-#pragma unroll
-        for (int k = 0; k < KT / 16; ++k)
-          umma2_ts(tmem + O_COL0 + g * D, tmem + scol(jj, g) + k * 8,
-                   umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o, (jj > 0 || k > 0) ? 1u : 0u);
-        umma2_commit_both(&p_empty[g * NSB + jj % NSB]);
-      };
-      auto wait_kv = [&](int jj) {
-        jenga_dev::mbar_wait(&kv_full[jj % NS], (jj / NS) & 1);
-        tc_fence_after();
-      };
-      jenga_dev::mbar_wait(q_full, 0);
-      if (ntiles > 0) {
-        wait_kv(0);
-        issue_s(0, 0);
-        issue_s(0, 1);
-      }
-      for (int j = 0; j < ntiles; ++j) {
-        if constexpr (NSB == 2) {
-          // S_g(j+1) goes to the other buffer (freed by PV_g(j-1), issued earlier):
-          // issue it before waiting for the softmax of tile j
-          if (j + 1 < ntiles) {
-            wait_kv(j + 1);
-            issue_s(j + 1, 0);
-            issue_s(j + 1, 1);
-          }
-          issue_pv(j, 0);
-          issue_pv(j, 1);
-          umma2_commit_both(&kv_empty[j % NS]);  // both groups' MMAs of tile j issued
-        } else {
-          // S_g(j+1) overwrites S_g's buffer (P_g(j)): issued after PV_g(j), in order
-          issue_pv(j, 0);
-          if (j + 1 < ntiles) {
-            wait_kv(j + 1);
-            issue_s(j + 1, 0);
-          }
-          issue_pv(j, 1);
-          umma2_commit_both(&kv_empty[j % NS]);  // both groups' PVs of tile j issued
-          if (j + 1 < ntiles) issue_s(j + 1, 1);
-        }
-      }
-    }
-  } else {
-    const int grp = warp >> 2;                  // 0: tile A, 1: tile B
-    const int r = threadIdx.x & (kRows - 1);    // query row == TMEM lane
-    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const int Q_COL = Q_COL0 + grp * (D / 2), O_COL = O_COL0 + grp * D;
-    const int t0 = pt0 + (2 * grp + static_cast<int>(rank)) * QB;
-    const int tok = t0 + r / G;
-    const bool row_ok = tok < c_len;
-    const int ipos = n - c_len + tok;
-    const uint32_t q_full0 = map_to_cta0(q_full);
-    const uint32_t p_full0 = map_to_cta0(&p_full[grp * NSB]);
-    {
-      const uint4* qrow = reinterpret_cast<const uint4*>(
-          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t w[32];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 x = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + i) : make_uint4(0, 0, 0, 0);
-          w[4 * i] = x.x;
-          w[4 * i + 1] = x.y;
-          w[4 * i + 2] = x.z;
-          w[4 * i + 3] = x.w;
-        }
-        tmem_st32u(tmem + lane_addr + Q_COL + c * 32, w);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) arrive_cta0(q_full0);
-    }
-    int lo_r = 0, hi_r = cross ? n - 1 : ipos;
-    if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
-      lo_r = static_cast<int>(ipos + 1 - p.window);
-    if (!row_ok || hi_r < lo_r) lo_r = hi_r = 1 << 30;
-    const uint32_t span = static_cast<uint32_t>(hi_r - lo_r);
-    const bool softcap = p.cap_log2 > 0.f;
-    const float sc = softcap ? 1.f : p.qscale;
-    const float qi = p.qscale * p.inv_cap;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
-      const int sbi = grp * NSB + j % NSB;  // this tile's S buffer / barrier index
-      const int S_COL = S_COL0 + sbi * KT, sb = 0;
-      const int ktok0 = (tile_lo + j) * KT;
-      jenga_dev::mbar_wait(&s_full[sbi], (j / NSB) & 1);
-      tc_fence_after();
-      float s[KT];
-      if constexpr (KT == 64) {
-        tmem_ld64(tmem + lane_addr + S_COL + sb * KT, s);  // both halves behind one wait
-      } else {
-        float v[32];
-        tmem_ld32(tmem + lane_addr + S_COL + sb * KT, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[i] = v[i];
-      }
-      if (softcap) {
-#pragma unroll
-        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
-      }
-      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {
-#pragma unroll
-        for (int i = 0; i < KT; ++i)
-          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
-      }
-      float mt = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < KT; ++i) mt = fmaxf(mt, s[i]);
-      mt *= sc;
-      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
-        const float m_new = fmaxf(m_used, mt);
-        if (j >= 1) {
-          const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
-          jenga_dev::mbar_wait(&p_empty[grp * NSB + (j - 1) % NSB], ((j - 1) / NSB) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
-            float v[32];
-            tmem_ld32(tmem + lane_addr + O_COL + c, v);
-            uint32_t u[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
-            tmem_st32u(tmem + lane_addr + O_COL + c, u);
-          }
-          tmem_st_wait();
-          l *= alpha;
-        }
-        m_used = m_new;
-      }
-      uint32_t pk[KT / 2];
-      float rs0 = 0.f, rs1 = 0.f;
-      const float neg = m_used == -INFINITY ? 0.f : -m_used;
-#pragma unroll
-      for (int i = 0; i < KT; i += 2) {
-        const float a = jenga_dev::fast_exp2(fmaf(s[i], sc, neg));
-        const float bb = jenga_dev::fast_exp2(fmaf(s[i + 1], sc, neg));
-        rs0 += a;
-        rs1 += bb;
-        pk[i / 2] = pack2<T>(a, bb);
-      }
-      l += rs0 + rs1;
-#pragma unroll
-      if constexpr (KT / 2 >= 32) {
-#pragma unroll
-        for (int c = 0; c < KT / 2; c += 32) {
-          uint32_t w[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) w[i] = pk[c + i];
-          tmem_st32u(tmem + lane_addr + S_COL + sb * KT + c, w);
-        }
-      } else {
-        tmem_st16u(tmem + lane_addr + S_COL + sb * KT, pk);
-      }
-      tmem_st_wait();
-      // zero this CTA's V columns of keys outside the pair's range
-      // boundary V rows: zeroed by group A only (PV_B(j) is issued after PV_A(j))
-      const bool boundary = grp == 0 && (ktok0 < key_lo || ktok0 + KT - 1 > key_hi);
-      if (boundary) {
-        uint8_t* vs = ring + (j % NS) * STAGE + K_BYTES;
-        for (int idx = r; idx < KT * VB; idx += kRows) {
-          const int vrow = idx % KT, chunk = idx / KT;
-          const int key = ktok0 + vrow;
-          if (key >= key_lo && key <= key_hi) continue;
-          uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
-                                                 (vrow % kTile) * 128);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) line[c] = make_uint4(0, 0, 0, 0);
-        }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t pf = p_full0 + 8u * (j % NSB);  // the leader's p_full[grp * NSB + j % NSB]
-        if (boundary)
-          arrive_cta0_release(pf);
-        else
-          arrive_cta0(pf);
-      }
-    }
-    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[grp * NSB + (ntiles - 1) % NSB], ((ntiles - 1) / NSB) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
-#pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
-      float v[32];
-      if (ntiles > 0) {
-        tmem_ld32(tmem + lane_addr + O_COL + c, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
-      }
-      if (row_ok) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
-                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
-                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
-                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
-      }
-    }
-  }
-  tc_fence_before();
-  cluster_sync();  // the peer's last remote arrivals and MMAs are done
-  if (warp == MW) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
-  }
-}
-
-
-// Number of the 8 exponentials per group of 8 S columns computed on the FMA pipe
-// (degree-3 polynomial) instead of the MUFU, in the 128-key kernel.
-#ifndef JENGA_PF_EMU
-#define JENGA_PF_EMU 0
+// Pairs (of every 4 pairs of S columns) whose exponentials the 128-key kernel
+// computes on the FMA pipe instead of the MUFU.
+#ifndef JENGA_PF_EMU2
+#define JENGA_PF_EMU2 1
 #endif
 
-// 2^x on the FMA pipe for x <= 0: round-to-nearest split x = j + f (f in
-// [-0.5, 0.5]) by the 1.5 * 2^23 shift, 2^f by a degree-3 minimax polynomial
-// (relative error < 1e-4, below the bf16 rounding of P), 2^j added into the
-// exponent field.  x below -126 flushes towards 0 like ex2.approx.ftz.
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -127.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  float q = fmaf(0.0555041086f, f, 0.2402264923f);
-  q = fmaf(q, f, 0.6931471806f);
-  q = fmaf(q, f, 1.0f);
-  return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
-}
-
-template <typename T, int D, int G, int NQ, int NSK, int NSV>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2) * 32, 1)
+template <typename T, int D, int G, int NSK, int NSV>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2) * 32, 1)
     paged_prefill_tc5_wide_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
                                   const __grid_constant__ CUtensorMap v_map) {
-  // 128-key tiles on a CTA pair (cta_group::2, M = 256).  S = Q K^T is issued
-  // with N = 128 keys (the 64-key form runs the tensor core at ~72%: its
-  // instructions cannot be issued faster than ~45 cycles each), so Q moves
-  // to shared memory (SS MMA) and TMEM holds only accumulators:
-  //   NQ = 1 (head_dim 256): O (256 columns) + two S buffers (2 x 128);
-  //   NQ = 2 (head_dim 128): two 128-row query tiles A / B per CTA, each with
-  //          O (128) + one S buffer (128); the MMA issuer ping-pongs
-  //          PV_A(j), S_A(j+1), PV_B(j), S_B(j+1).
-  // K and V stream through separate rings (K of tile j+1 is needed before V of
+  // 128-key tiles on a CTA pair (cta_group::2, M = 256 query rows, 128 per CTA).
+  // S = Q K^T is issued with N = 128 keys (64-key instructions run the tensor
+  // core at ~72%: they cannot be issued faster than ~45 cycles each), so Q lives
+  // in shared memory (SS MMA) and TMEM holds O (D columns) plus NSB = (512 - D) / 128
+  // S buffers: 2 at head_dim 256, 3 at 128.  The MMA issuer keeps S NSB - 1 tiles
+  // ahead of the softmax (S(j + NSB) is issued right after O += P(j) V(j), which
+  // frees its buffer), so the softmax never waits for a tile's scores.
+  // Softmax: 8 warps, two per TMEM lane quarter; warp w owns query rows
+  // 32 (w & 3) .. + 31 and key columns 64 (w >> 2) .. + 63 of every S tile (the row
+  // max is exchanged between the two warps of a row through shared memory), so two
+  // warps per SM sub-partition keep the MUFU busy through each other's loads,
+  // reductions and TMEM stores.
+  // K and V stream through separate rings (K of tile j + 1 is needed before V of
   // tile j): K slot released when the tile's S MMAs complete, V slot when its PV
   // MMAs complete.  Shared-memory layouts (128-byte swizzle):
-  //   Q: [query tile][chunk c][128 rows][128 B]   (written by the softmax threads)
-  //   K: [8-key group][chunk c][8 rows][128 B]    (one 4-D TMA box per 16-key piece; this CTA's 64 keys)
-  //   V: [16-key piece][chunk c][16 rows][128 B]  (one 3-D box per piece; this CTA's half of head_dim)
+  //   Q: [chunk c][128 rows][128 B]              (written by the softmax threads)
+  //   K: [8-key group][chunk c][8 rows][128 B]   (one 4-D TMA box per 16-key piece; this CTA's 64 keys)
+  //   V: [16-key piece][chunk c][16 rows][128 B] (one 3-D box per piece; this CTA's half of head_dim)
   constexpr int KT = 128;
   constexpr int NBOX = D / kBoxCols;
   constexpr int VB = NBOX / 2;
@@ -1306,37 +663,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
   constexpr int V_PIECE = VB * kTile * 128;
   constexpr int V_BYTES = (KT / kTile) * V_PIECE;
   constexpr int Q_BYTES = NBOX * kRows * 128;
-  constexpr int NSB = 2 / NQ;                 // S buffers per query tile
-  constexpr int S_COL0 = NQ * D;
+  constexpr int NSB = (512 - D) / KT;         // S buffers
+  constexpr int S_COL0 = D;
+  constexpr int HC = KT / 2;                  // S columns per softmax warp
   constexpr uint32_t TMEM_COLS = 512;
-  static_assert(NBOX % 2 == 0 && NQ * D + NQ * NSB * KT == 512, "128-key kernel shape");
-  constexpr int SW = NQ * kSoftWarps, PW = SW, MW = SW + 1;
+  static_assert(NBOX % 2 == 0 && D + NSB * KT == 512, "128-key kernel shape");
+  constexpr int SW = 2 * kSoftWarps, PW = SW, MW = SW + 1;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* qs = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* kring = qs + NQ * Q_BYTES;
+  uint8_t* kring = qs + Q_BYTES;
   uint8_t* vring = kring + NSK * K_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vring + NSV * V_BYTES);
+  float* red = reinterpret_cast<float*>(vring + NSV * V_BYTES);  // [tile parity][half][row]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 2 * kRows);
   uint64_t* q_full = bars;                    // leader: all softmax warps of the pair
   uint64_t* k_full = bars + 1;                // leader: both CTAs' TMA bytes
   uint64_t* k_empty = k_full + NSK;           // both: multicast commit
   uint64_t* v_full = k_empty + NSK;
   uint64_t* v_empty = v_full + NSV;
-  uint64_t* s_full = v_empty + NSV;           // both: multicast commit      [tile][buffer]
-  uint64_t* p_full = s_full + NQ * NSB;       // leader: the tile's 8 softmax warps
-  uint64_t* p_empty = p_full + NQ * NSB;      // both: multicast commit
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NQ * NSB);
+  uint64_t* s_full = v_empty + NSV;           // both: multicast commit      [buffer]
+  uint64_t* p_full = s_full + NSB;            // leader: 16 softmax warps     [buffer]
+  uint64_t* p_empty = p_full + NSB;           // both: multicast commit      [buffer]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NSB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int unit = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
   const int c_len = p.cu_q[b + 1] - p.cu_q[b];
-  const int pt0 = 2 * NQ * unit * QB;
+  const int pt0 = 2 * unit * QB;
   if (pt0 >= c_len) return;  // uniform over the pair
   const int n = p.seq_lens[b];
   const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
   const int pos0 = n - c_len + pt0;
-  const int pos1 = n - c_len + min(pt0 + 2 * NQ * QB, c_len) - 1;  // union of the pair's query rows
+  const int pos1 = n - c_len + min(pt0 + 2 * QB, c_len) - 1;  // union of the pair's query rows
   int key_lo = 0;
   const int key_hi = cross ? n - 1 : pos1;
   if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
@@ -1353,9 +712,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
       jenga_dev::mbar_init(&v_full[i], 1);
       jenga_dev::mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < NQ * NSB; ++i) {
+    for (int i = 0; i < NSB; ++i) {
       jenga_dev::mbar_init(&s_full[i], 1);
-      jenga_dev::mbar_init(&p_full[i], 2 * kSoftWarps);
+      jenga_dev::mbar_init(&p_full[i], 2 * SW);
       jenga_dev::mbar_init(&p_empty[i], 1);
     }
     jenga_dev::fence_mbar_init();
@@ -1410,6 +769,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
       const int st = jj % NSK;
       if (jj >= NSK) jenga_dev::mbar_wait(&k_empty[st], ((jj / NSK) & 1) ^ 1);
       const uint32_t full0 = map_to_cta0(&k_full[st]);
+#ifdef JENGA_PF_NOLOAD
+      if (lane == 0 && rank == 0) arrive_cta0(full0);  // timing-only variant: no K/V traffic
+      return;
+#endif
       if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * K_BYTES);
       if (lane >= k_lane0 && lane < k_lane0 + KH / kTile)
         tma_load_4d_pair(kring + st * K_BYTES + (lane - k_lane0) * 2 * K_GROUP, &k_map, row, full0, policy);
@@ -1418,6 +781,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
       const int st = jj % NSV;
       if (jj >= NSV) jenga_dev::mbar_wait(&v_empty[st], ((jj / NSV) & 1) ^ 1);
       const uint32_t full0 = map_to_cta0(&v_full[st]);
+#ifdef JENGA_PF_NOLOAD
+      if (lane == 0 && rank == 0) arrive_cta0(full0);
+      return;
+#endif
       if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * V_BYTES);
       if (lane < KT / kTile)
         tma_load_3d_pair(vring + st * V_BYTES + lane * V_PIECE, &v_map, row + p.tpp, static_cast<int>(rank) * VB,
@@ -1437,35 +804,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
       row_cur = row_nxt;
     }
   } else if (warp == MW) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {  // the whole warp runs the loop; elect.sync issues
       const uint32_t id_s = idesc_f16<T>(2 * kRows, KT, 0);
       const uint32_t id_o = idesc_f16<T>(2 * kRows, D, 1);
       // descriptors as base + constant (one add per MMA on the uniform datapath)
       const uint64_t q_desc0 = umma_desc(jenga_dev::smem_u32(qs), 16, 1024);
       const uint64_t k_desc0 = umma_desc(jenga_dev::smem_u32(kring), 16, K_GROUP);
       const uint64_t v_desc0 = umma_desc(jenga_dev::smem_u32(vring), kTile * 128, 1024);
-      auto sidx = [&](int jj, int g) { return g * NSB + jj % NSB; };
-      auto issue_s = [&](int jj, int g) {  // S_g(jj) = Q_g K_jj^T (K slot already full)
-        const uint64_t kd = k_desc0 + ((jj % NSK) * K_BYTES >> 4);
-        const uint64_t qd = q_desc0 + (g * Q_BYTES >> 4);
-        const uint32_t d = tmem + S_COL0 + sidx(jj, g) * KT;
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
-          umma2_ss(d, qd + (((k >> 2) * kRows * 128 + (k & 3) * 32) >> 4), kd + off, id_s, k > 0 ? 1u : 0u);
-        }
-        umma2_commit_both(&s_full[sidx(jj, g)]);
-      };
-      auto issue_pv = [&](int jj, int g) {  // O_g += P_g(jj) V_jj (V slot already full)
-        jenga_dev::mbar_wait(&p_full[sidx(jj, g)], (jj / NSB) & 1);
-        tc_fence_after();
-        const uint64_t vd = v_desc0 + ((jj % NSV) * V_BYTES >> 4);
-        const uint32_t a = tmem + S_COL0 + sidx(jj, g) * KT;
-#pragma unroll
-        for (int k = 0; k < KT / 16; ++k)
-          umma2_ts(tmem + g * D, a + k * 8, vd + (k * V_PIECE >> 4), id_o, (jj > 0 || k > 0) ? 1u : 0u);
-        umma2_commit_both(&p_empty[sidx(jj, g)]);
-      };
       auto wait_v = [&](int jj) {
         jenga_dev::mbar_wait(&v_full[jj % NSV], (jj / NSV) & 1);
         tc_fence_after();
@@ -1478,65 +823,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
         const int kt0 = (tile_lo + jj) * KT;
         if (kt0 < key_lo || kt0 + KT - 1 > key_hi) wait_v(jj);
       };
+      auto issue_s = [&](int jj) {  // S(jj) = Q K_jj^T into buffer jj % NSB
+        wait_k(jj);
+        const uint64_t kd = k_desc0 + ((jj % NSK) * K_BYTES >> 4);
+        const uint32_t d = tmem + S_COL0 + (jj % NSB) * KT;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
+          umma2_ss_w(d, q_desc0 + (((k >> 2) * kRows * 128 + (k & 3) * 32) >> 4), kd + off, id_s, k > 0 ? 1u : 0u);
+        }
+        umma2_commit_both_w(&s_full[jj % NSB]);
+        umma2_commit_both_w(&k_empty[jj % NSK]);
+        if (lane == 0) PF_TRACE(2, jj);
+      };
+      auto issue_pv = [&](int jj) {  // O += P(jj) V_jj
+        jenga_dev::mbar_wait(&p_full[jj % NSB], (jj / NSB) & 1);
+        if (lane == 0) PF_TRACE(0, jj);
+        tc_fence_after();
+        wait_v(jj);
+        const uint64_t vd = v_desc0 + ((jj % NSV) * V_BYTES >> 4);
+        const uint32_t a = tmem + S_COL0 + (jj % NSB) * KT;
+#pragma unroll
+        for (int k = 0; k < KT / 16; ++k)
+          umma2_ts_w(tmem, a + k * 8, vd + (k * V_PIECE >> 4), id_o, (jj > 0 || k > 0) ? 1u : 0u);
+        umma2_commit_both_w(&p_empty[jj % NSB]);
+        umma2_commit_both_w(&v_empty[jj % NSV]);
+      };
       jenga_dev::mbar_wait(q_full, 0);
       tc_fence_after();
-      if constexpr (NQ == 1) {
-        // S(j+1) into the other buffer before O += P(j) V(j)
-        for (int j = 0; j < ntiles; ++j) {
-          wait_k(j);
-          issue_s(j, 0);
-          umma2_commit_both(&k_empty[j % NSK]);
-          if (j >= 1) {
-            wait_v(j - 1);
-            issue_pv(j - 1, 0);
-            umma2_commit_both(&v_empty[(j - 1) % NSV]);
-          }
-        }
-        if (ntiles > 0) {
-          wait_v(ntiles - 1);
-          issue_pv(ntiles - 1, 0);
-          umma2_commit_both(&v_empty[(ntiles - 1) % NSV]);
-        }
-      } else {
-        if (ntiles > 0) {
-          wait_k(0);
-          issue_s(0, 0);
-          issue_s(0, 1);
-          umma2_commit_both(&k_empty[0]);
-        }
-        for (int j = 0; j < ntiles; ++j) {
-          // S_g(j+1) overwrites S_g's buffer (P_g(j)): issued after PV_g(j), in order
-          wait_v(j);
-          issue_pv(j, 0);
-          if (j + 1 < ntiles) {
-            wait_k(j + 1);
-            issue_s(j + 1, 0);
-          }
-          issue_pv(j, 1);
-          umma2_commit_both(&v_empty[j % NSV]);
-          if (j + 1 < ntiles) {
-            issue_s(j + 1, 1);
-            umma2_commit_both(&k_empty[(j + 1) % NSK]);
-          }
-        }
+      for (int j = 0; j < NSB - 1 && j < ntiles; ++j) issue_s(j);
+      for (int j = 0; j < ntiles; ++j) {
+        // S(j + NSB - 1) goes to the buffer PV(j - 1) released (in order), ahead of PV(j)
+        if (j + NSB - 1 < ntiles) issue_s(j + NSB - 1);
+        issue_pv(j);
       }
     }
   } else {
-    const int grp = NQ == 2 ? warp >> 2 : 0;   // query tile of this softmax warpgroup
+    const int hf = warp >> 2;                   // column half of every S tile / O
     const int r = threadIdx.x & (kRows - 1);    // query row == TMEM lane
     const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const int O_COL = grp * D;
-    const int t0 = pt0 + (NQ * grp + static_cast<int>(rank)) * QB;
+    const int t0 = pt0 + static_cast<int>(rank) * QB;
     const int tok = t0 + r / G;
     const bool row_ok = tok < c_len;
     const int ipos = n - c_len + tok;
-    const uint32_t p_full0 = map_to_cta0(&p_full[grp * NSB]);
-    {  // Q row -> shared memory, 128-byte swizzled K-major
+    const uint32_t p_full0 = map_to_cta0(&p_full[0]);
+    const uint32_t pair_bar = 1 + (warp & 3);   // named barrier of the two warps sharing these rows
+    {  // this thread's half of its Q row -> shared memory, 128-byte swizzled K-major
       const uint4* qrow = reinterpret_cast<const uint4*>(
           static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
-      uint8_t* qt = qs + grp * Q_BYTES + r * 128;
+      uint8_t* qt = qs + r * 128;
 #pragma unroll
-      for (int c = 0; c < NBOX; ++c) {
+      for (int cc = 0; cc < NBOX / 2; ++cc) {
+        const int c = hf * (NBOX / 2) + cc;
         uint4 x[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) x[u] = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + u) : make_uint4(0, 0, 0, 0);
@@ -1558,50 +896,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
     const float qi = p.qscale * p.inv_cap;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
-      const int sbi = grp * NSB + j % NSB;
-      const uint32_t s_addr = tmem + lane_addr + S_COL0 + sbi * KT;
-      const int ktok0 = (tile_lo + j) * KT;
-      jenga_dev::mbar_wait(&s_full[sbi], (j / NSB) & 1);
+      const int sb = j % NSB;
+      const uint32_t s_addr = tmem + lane_addr + S_COL0 + sb * KT;
+      const int kc0 = (tile_lo + j) * KT + hf * HC;   // key of this warp's first column
+      jenga_dev::mbar_wait(&s_full[sb], (j / NSB) & 1);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(4 + 6 * hf, j);
       tc_fence_after();
-      float s[KT];
-      {
-        float* s0 = s;
-        tmem_ld64(s_addr, *reinterpret_cast<float(*)[64]>(s0));
-        tmem_ld64(s_addr + 64, *reinterpret_cast<float(*)[64]>(s0 + 64));
+#ifdef JENGA_PF_NOSOFTMAX
+      if (true) {  // timing-only variant: hand the tile straight back to the MMA issuer
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_cta0(p_full0 + 8u * sb);
+        continue;
       }
+#endif
+      float s[HC];
+      tmem_ld64(s_addr + hf * HC, s);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(5 + 6 * hf, j);
       if (softcap) {
 #pragma unroll
-        for (int i = 0; i < KT; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
+        for (int i = 0; i < HC; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
       }
-      if (ktok0 < lo_r || ktok0 + KT - 1 > hi_r) {
+      if (kc0 < lo_r || kc0 + HC - 1 > hi_r) {
 #pragma unroll
-        for (int i = 0; i < KT; ++i)
-          s[i] = static_cast<uint32_t>(ktok0 + i - lo_r) <= span ? s[i] : -INFINITY;
+        for (int i = 0; i < HC; ++i)
+          s[i] = static_cast<uint32_t>(kc0 + i - lo_r) <= span ? s[i] : -INFINITY;
       }
       float m8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) m8[i] = s[i];
 #pragma unroll
-      for (int i = 8; i < KT; i += 8) {
+      for (int i = 8; i < HC; i += 8) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], s[i + u]);
       }
       float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      // Rescale test for the row: its max over both halves.  The two warps of these
+      // rows first OR their "some row grew by more than 2^8" votes with one
+      // barrier reduction; only then (rarely, after the first tiles) do they
+      // exchange the half-row maxima through shared memory.
       mt *= sc;
-      if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+      uint32_t grow;
+      asm volatile("{\n\t.reg .pred p, q;\n\tsetp.gt.f32 p, %1, %2;\n\tbar.red.or.pred q, %3, %4, p;\n\tselp.u32 %0, 1, 0, q;\n\t}\n"
+                   : "=r"(grow) : "f"(mt), "f"(m_used + kRescaleThreshold), "r"(pair_bar), "n"(64) : "memory");
+      if (grow) {
+        float* rd = red + (j & 1) * 2 * kRows;
+        rd[hf * kRows + r] = mt;
+        asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64) : "memory");
+        mt = fmaxf(mt, rd[(hf ^ 1) * kRows + r]);
         const float m_new = fmaxf(m_used, mt);
         if (j >= 1) {
           const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
-          jenga_dev::mbar_wait(&p_empty[grp * NSB + (j - 1) % NSB], ((j - 1) / NSB) & 1);
+          jenga_dev::mbar_wait(&p_empty[(j - 1) % NSB], ((j - 1) / NSB) & 1);
           tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < D; c += 32) {
+          for (int c = hf * (D / 2); c < (hf + 1) * (D / 2); c += 32) {
             float v[32];
-            tmem_ld32(tmem + lane_addr + O_COL + c, v);
+            tmem_ld32(tmem + lane_addr + c, v);
             uint32_t u[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
-            tmem_st32u(tmem + lane_addr + O_COL + c, u);
+            tmem_st32u(tmem + lane_addr + c, u);
           }
           tmem_st_wait();
           l *= alpha;
@@ -1609,30 +964,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
         m_used = m_new;
       }
       const float neg = m_used == -INFINITY ? 0.f : -m_used;
-      float rs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float2 rs[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      uint32_t pk[HC / 2];
+      const float2 sc2 = make_float2(sc, sc), neg2 = make_float2(neg, neg);
 #pragma unroll
-      for (int c = 0; c < KT; c += 64) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          const float x0 = fmaf(s[c + i], sc, neg), x1 = fmaf(s[c + i + 1], sc, neg);
-          const float a = ((i & 7) >= 8 - JENGA_PF_EMU) ? exp2_fma(x0) : jenga_dev::fast_exp2(x0);
-          const float bb = (((i + 1) & 7) >= 8 - JENGA_PF_EMU) ? exp2_fma(x1) : jenga_dev::fast_exp2(x1);
-          rs[i & 7] += a;
-          rs[(i + 1) & 7] += bb;
-          pk[i / 2] = pack2<T>(a, bb);
-        }
-        tmem_st32u(s_addr + c / 2, pk);
+      for (int i = 0; i < HC; i += 2) {
+        const float2 x = ffma2(make_float2(s[i], s[i + 1]), sc2, neg2);
+        float2 e;
+        if (((i >> 1) & 3) >= 4 - JENGA_PF_EMU2)
+          e = exp2_fma2(x);
+        else
+          e = make_float2(jenga_dev::fast_exp2(x.x), jenga_dev::fast_exp2(x.y));
+        rs[(i >> 1) & 3] = fadd2(rs[(i >> 1) & 3], e);
+        pk[i / 2] = pack2<T>(e.x, e.y);
       }
-      l += ((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7]));
+      tmem_st32u(s_addr + hf * (HC / 2), pk);  // P (bf16 pairs) over this half's first S columns
+      {
+        const float2 t = fadd2(fadd2(rs[0], rs[1]), fadd2(rs[2], rs[3]));
+        l += t.x + t.y;
+      }
       tmem_st_wait();
-      // zero this CTA's V columns of keys outside the pair's range (group A only:
-      // PV_B(j) is issued after PV_A(j)); the issuer waited for this tile's V
-      // before S(j), so s_full(j) implies it has landed
-      const bool boundary = grp == 0 && (ktok0 < key_lo || ktok0 + KT - 1 > key_hi);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(6 + 6 * hf, j);
+      // zero this CTA's V columns of keys outside the pair's range; the issuer waited
+      // for this tile's V before S(j), so s_full(j) implies it has landed
+      const int ktok0 = (tile_lo + j) * KT;
+      const bool boundary = ktok0 < key_lo || ktok0 + KT - 1 > key_hi;
       if (boundary) {
         uint8_t* vs = vring + (j % NSV) * V_BYTES;
-        for (int idx = r; idx < KT * VB; idx += kRows) {
+        for (int idx = threadIdx.x; idx < KT * VB; idx += SW * 32) {
           const int vrow = idx % KT, chunk = idx / KT;
           const int key = ktok0 + vrow;
           if (key >= key_lo && key <= key_hi) continue;
@@ -1645,23 +1004,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NQ * kSoftWarps + 2
       }
       tc_fence_before();
       __syncwarp();
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(7 + 6 * hf, j);
       if (lane == 0) {
-        const uint32_t pf = p_full0 + 8u * (j % NSB);
         if (boundary)
-          arrive_cta0_release(pf);
+          arrive_cta0_release_ool(p_full0 + 8u * sb);
         else
-          arrive_cta0(pf);
+          arrive_cta0(p_full0 + 8u * sb);
       }
     }
-    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[grp * NSB + (ntiles - 1) % NSB], ((ntiles - 1) / NSB) & 1);
+    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[(ntiles - 1) % NSB], ((ntiles - 1) / NSB) & 1);
     tc_fence_after();
+    {  // row sum over both halves
+      float* rd = red + (ntiles & 1) * 2 * kRows;  // the parity the last tile's exchange did not use
+      rd[hf * kRows + r] = l;
+      asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64) : "memory");
+      l += rd[(hf ^ 1) * kRows + r];
+    }
     const float inv = l > 0.f ? 1.f / l : 0.f;
     T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
 #pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
+    for (int c = hf * (D / 2); c < (hf + 1) * (D / 2); c += 32) {
       float v[32];
       if (ntiles > 0) {
-        tmem_ld32(tmem + lane_addr + O_COL + c, v);
+        tmem_ld32(tmem + lane_addr + c, v);
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -1742,101 +1107,40 @@ int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) 
   return jenga_dev::check_launch("paged_prefill_tc5_kernel");
 }
 
-template <typename T, int D, int G, int KT, int NS>
-int launch_tc5_pair(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
-  constexpr int NBOX = D / kBoxCols;
-  constexpr int STAGE = NBOX * (KT / 2) * 128 + (NBOX / 2) * KT * 128;
-  const int smem = NS * STAGE + (1 + 2 * NS + 6) * 8 + 16 + 1024;
-  CUtensorMap k_map, v_map;  // V: this CTA's half of head_dim per box
-  if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
-  auto kern = paged_prefill_tc5_pair_kernel<T, D, G, KT, NS>;
-  static std::atomic<uint64_t> configured{0};
-  if (int rc = configure_smem(kern, smem, configured)) return rc;
-  dim3 grid((prm.q_blocks + 1) / 2 * 2, prm.hkv, batch);
-  kern<<<grid, kT5Threads, smem, s>>>(prm, k_map, v_map);
-  return jenga_dev::check_launch("paged_prefill_tc5_pair_kernel");
-}
-
-template <typename T, int D, int G, int KT, int NS>
-int launch_tc5_pp(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
-  constexpr int NBOX = D / kBoxCols;
-  constexpr int STAGE = NBOX * (KT / 2) * 128 + (NBOX / 2) * KT * 128;
-  const int smem = NS * STAGE + (1 + 2 * NS + 12) * 8 + 16 + 1024;
-  CUtensorMap k_map, v_map;
-  if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
-  auto kern = paged_prefill_tc5_pp_kernel<T, D, G, KT, NS>;
-  static std::atomic<uint64_t> configured{0};
-  if (int rc = configure_smem(kern, smem, configured)) return rc;
-  dim3 grid((prm.q_blocks + 3) / 4 * 2, prm.hkv, batch);  // a CTA pair per 4 query blocks
-  kern<<<grid, kPPThreads, smem, s>>>(prm, k_map, v_map);
-  return jenga_dev::check_launch("paged_prefill_tc5_pp_kernel");
-}
-
-template <typename T, int D, int G, int NQ, int NSK, int NSV>
+template <typename T, int D, int G, int NSK, int NSV>
 int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   constexpr int NBOX = D / kBoxCols;
   constexpr int K_BYTES = (64 / 8) * NBOX * 8 * 128, V_BYTES = 8 * (NBOX / 2) * kTile * 128;
-  constexpr int Q_BYTES = NBOX * kRows * 128, NSB = 2 / NQ;
-  const int smem = NQ * Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + (1 + 2 * NSK + 2 * NSV + 3 * NQ * NSB) * 8 + 16 + 1024;
+  constexpr int Q_BYTES = NBOX * kRows * 128, NSB = (512 - D) / 128;
+  const int smem = Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + 2 * 2 * kRows * 4 +
+                   (1 + 2 * NSK + 2 * NSV + 3 * NSB) * 8 + 16 + 1024;
   CUtensorMap k_map, v_map;
   if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
-  auto kern = paged_prefill_tc5_wide_kernel<T, D, G, NQ, NSK, NSV>;
+  auto kern = paged_prefill_tc5_wide_kernel<T, D, G, NSK, NSV>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  dim3 grid((prm.q_blocks + 2 * NQ - 1) / (2 * NQ) * 2, prm.hkv, batch);  // a CTA pair per 2 * NQ query blocks
-  kern<<<grid, (NQ * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map);
+  dim3 grid((prm.q_blocks + 1) / 2 * 2, prm.hkv, batch);  // a CTA pair per 2 query blocks
+  kern<<<grid, (2 * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map);
   return jenga_dev::check_launch("paged_prefill_tc5_wide_kernel");
 }
 
-template <typename T, int D, int NQ, int NSK, int NSV>
+template <typename T, int D, int NSK, int NSV>
 int dispatch_wide(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (G) {
-    case 1: return launch_tc5_wide<T, D, 1, NQ, NSK, NSV>(prm, dtype, s, batch);
-    case 2: return launch_tc5_wide<T, D, 2, NQ, NSK, NSV>(prm, dtype, s, batch);
-    case 4: return launch_tc5_wide<T, D, 4, NQ, NSK, NSV>(prm, dtype, s, batch);
-    case 8: return launch_tc5_wide<T, D, 8, NQ, NSK, NSV>(prm, dtype, s, batch);
+    case 1: return launch_tc5_wide<T, D, 1, NSK, NSV>(prm, dtype, s, batch);
+    case 2: return launch_tc5_wide<T, D, 2, NSK, NSV>(prm, dtype, s, batch);
+    case 4: return launch_tc5_wide<T, D, 4, NSK, NSV>(prm, dtype, s, batch);
+    case 8: return launch_tc5_wide<T, D, 8, NSK, NSV>(prm, dtype, s, batch);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
 
-#ifndef JENGA_PF_WIDE
-#define JENGA_PF_WIDE 1
-#endif
 #ifndef JENGA_PF_NSK256
 #define JENGA_PF_NSK256 2
 #endif
 #ifndef JENGA_PF_NSV256
-#define JENGA_PF_NSV256 3
+#define JENGA_PF_NSV256 2
 #endif
-
-// Key-tile width of the ping-pong kernel: 64 keys (one S buffer per group) or 32
-// (two S buffers per group, twice the ring depth).
-#ifndef JENGA_PP_KT
-#define JENGA_PP_KT 64
-#endif
-template <typename T, int D, int NS0>
-int dispatch_pp(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
-  constexpr int KT = JENGA_PP_KT;
-  constexpr int NS = NS0 * 64 / KT;
-  switch (G) {
-    case 1: return launch_tc5_pp<T, D, 1, KT, NS>(prm, dtype, s, batch);
-    case 2: return launch_tc5_pp<T, D, 2, KT, NS>(prm, dtype, s, batch);
-    case 4: return launch_tc5_pp<T, D, 4, KT, NS>(prm, dtype, s, batch);
-    case 8: return launch_tc5_pp<T, D, 8, KT, NS>(prm, dtype, s, batch);
-  }
-  return JENGA_ERR_UNSUPPORTED;
-}
-
-template <typename T, int D, int NS>
-int dispatch_pair(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
-  switch (G) {
-    case 1: return launch_tc5_pair<T, D, 1, 64, NS>(prm, dtype, s, batch);
-    case 2: return launch_tc5_pair<T, D, 2, 64, NS>(prm, dtype, s, batch);
-    case 4: return launch_tc5_pair<T, D, 4, 64, NS>(prm, dtype, s, batch);
-    case 8: return launch_tc5_pair<T, D, 8, 64, NS>(prm, dtype, s, batch);
-  }
-  return JENGA_ERR_UNSUPPORTED;
-}
 
 template <typename T, int D, int NS>
 int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
@@ -1856,18 +1160,20 @@ int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int 
 template <typename T>
 int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   switch (D) {
-    case 256:
-      if (JENGA_PF_WIDE) return dispatch_wide<T, 256, 1, JENGA_PF_NSK256, JENGA_PF_NSV256>(G, prm, dtype, s, batch);
-      return dispatch_pair<T, 256, 6>(G, prm, dtype, s, batch);
-    case 128:
-      if (JENGA_PF_WIDE) return dispatch_wide<T, 128, 2, 5, 5>(G, prm, dtype, s, batch);
-      return dispatch_pp<T, 128, 8>(G, prm, dtype, s, batch);
+    case 256: return dispatch_wide<T, 256, JENGA_PF_NSK256, JENGA_PF_NSV256>(G, prm, dtype, s, batch);
+    case 128: return dispatch_wide<T, 128, 6, 5>(G, prm, dtype, s, batch);
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
   }
   return jenga_dev::set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: head_dim must be 64, 128 or 256");
 }
 
 }  // namespace
+
+#ifdef JENGA_PF_TRACE
+JENGA_EXPORT int jenga_debug_prefill_trace(long long* dst) {
+  return cudaMemcpyFromSymbol(dst, g_pf_trace, sizeof(g_pf_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // Chunked-prefill paged attention (the reference's
 // prefill_some stores a chunk of positions per step, simulator.cpp:504-547).

@@ -1,0 +1,165 @@
+// Microbenchmark of the prefill softmax inner step on one 128-key S tile per
+// thread (one query row per thread, S in TMEM as in prefill_tc5.cu): TMEM load,
+// row max, scale + exp2, row sum, bf16 pack, TMEM store of P.  Variants:
+//   0: scalar FFMA / FADD (the kernel's form)
+//   1: packed FFMA2 / FADD2 (f32x2)
+//   2: 1 + a quarter of the exponentials from an FFMA2 polynomial
+// Prints cycles per tile per warp for 4 and 8 warps per SM.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o softmax_rate.bin softmax_rate.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_bf16.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd; mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5}; mov.b64 rc, {%6, %7};\n"
+      "fma.rn.ftz.f32x2 rd, ra, rb, rc;\n mov.b64 {%0, %1}, rd; }"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd; mov.b64 ra, {%2, %3}; mov.b64 rb, {%4, %5};\n"
+      "add.rn.ftz.f32x2 rd, ra, rb;\n mov.b64 {%0, %1}, rd; }"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// 2^x for two lanes on the FMA pipe (degree-3), x <= 0
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f); x.y = fmaxf(x.y, -127.f);
+  const float2 big = make_float2(12582912.f, 12582912.f), nbig = make_float2(-12582912.f, -12582912.f);
+  const float2 t = fadd2(x, big);
+  const float2 j = fadd2(t, nbig);
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 q = ffma2(make_float2(0.0555041086f, 0.0555041086f), f, make_float2(0.2402264923f, 0.2402264923f));
+  q = ffma2(q, f, make_float2(0.6931471806f, 0.6931471806f));
+  q = ffma2(q, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
+__device__ __forceinline__ void ld32(uint32_t addr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+}
+__device__ __forceinline__ void st32(uint32_t addr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+template <int V>
+__global__ void __launch_bounds__(256, 1) softmax_rate(int iters, long long* out, float* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tm = slot + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
+  {
+    uint32_t z[32];
+    for (int i = 0; i < 32; ++i) z[i] = __float_as_uint(-0.01f * (i + (threadIdx.x & 7)));
+    for (int c = 0; c < 128; c += 32) st32(tm + c, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  float m_used = 0.f, l = 0.f;
+  const float sc = 0.0883883f;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float s[128];
+    ld32(tm, s); ld32(tm + 32, s + 32); ld32(tm + 64, s + 64); ld32(tm + 96, s + 96);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    float m8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m8[i] = s[i];
+#pragma unroll
+    for (int i = 8; i < 128; i += 8)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], s[i + u]);
+    float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+    m_used = fmaxf(m_used, mt * sc) + 1e-7f * it;
+    const float neg = -m_used;
+    uint32_t pk[64];
+    if constexpr (V == 0) {
+      float rs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) {
+        const float a = ex2(fmaf(s[i], sc, neg)), b = ex2(fmaf(s[i + 1], sc, neg));
+        rs[i & 7] += a; rs[(i + 1) & 7] += b;
+        pk[i / 2] = pack_bf16(a, b);
+      }
+      l += ((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7]));
+    } else {
+      float2 rs[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+      const float2 sc2 = make_float2(sc, sc), ng2 = make_float2(neg, neg);
+#pragma unroll
+      for (int i = 0; i < 128; i += 2) {
+        const float2 x = ffma2(make_float2(s[i], s[i + 1]), sc2, ng2);
+        float2 e;
+        if (V == 2 && (i & 7) == 6) e = exp2_poly2(x);
+        else e = make_float2(ex2(x.x), ex2(x.y));
+        rs[(i >> 1) & 3] = fadd2(rs[(i >> 1) & 3], e);
+        pk[i / 2] = pack_bf16(e.x, e.y);
+      }
+      const float2 r = fadd2(fadd2(rs[0], rs[1]), fadd2(rs[2], rs[3]));
+      l += r.x + r.y;
+    }
+    st32(tm + 256 + (warp >> 2) * 64, pk);
+    st32(tm + 256 + (warp >> 2) * 64 + 32, pk + 32);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  if (l == 12345.f) sink[threadIdx.x] = l;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(slot));
+  }
+}
+
+int main() {
+  long long* d_out; float* sink; long long h[148];
+  cudaMalloc(&d_out, 148 * sizeof(long long)); cudaMalloc(&sink, 4096 * sizeof(float));
+  auto run = [&](auto kern, int v) {
+    for (int warps : {4, 8}) {
+      const int iters = 256;
+      kern<<<148, warps * 32>>>(iters, d_out, sink);
+      kern<<<148, warps * 32>>>(iters, d_out, sink);
+      if (cudaDeviceSynchronize() != cudaSuccess) { printf("failed\n"); return; }
+      cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+      double tot = 0; for (int i = 0; i < 148; ++i) tot += h[i]; tot /= 148;
+      printf("{\"variant\": %d, \"warps\": %d, \"cyc_per_tile\": %.0f, \"exp_per_clk_per_sm\": %.2f}\n", v, warps,
+             tot / iters, warps * 32.0 * 128 * iters / tot);
+    }
+  };
+  run(softmax_rate<0>, 0);
+  run(softmax_rate<1>, 1);
+  run(softmax_rate<2>, 2);
+  return 0;
+}

@@ -44,7 +44,7 @@ __device__ __forceinline__ void csync() {
 // MODE: 0 = TS (A in TMEM), 1 = SS (A in smem).  Fully unrolled groups of 16
 // MMAs with descriptors precomputed (base + constant), as a tuned issuer would.
 template <int CG, int M, int N, int MODE, int BMN>
-__global__ void mma_rate(int iters, long long* out) {
+__global__ void mma_rate(int iters, long long* out, int noise) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* base = smem + ((1024 - (su32(smem) & 1023)) & 1023);
   __shared__ uint64_t bar;
@@ -118,6 +118,31 @@ __global__ void mma_rate(int iters, long long* out) {
     out[blockIdx.x * 2 + 1] = t1 - t0;
   } else if (threadIdx.x == 0 && CG == 2) {
     mbar_wait(&bar, 0);
+  } else if (noise && warp >= 4) {
+    // TMEM traffic like the softmax warps: load 64 columns, store 32, until the MMAs finish
+    const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + ((warp >> 2) & 1) * 128;
+    uint32_t phase_done = 0;
+    while (!phase_done) {
+      uint32_t r[32];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(ta) : "memory");
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(ta + 64),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      uint32_t ok;
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                   : "=r"(ok) : "r"(su32(&bar)) : "memory");
+      phase_done = __shfl_sync(0xffffffffu, ok, 0);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   if (CG == 2) csync(); else __syncthreads();
@@ -235,12 +260,13 @@ int main() {
   long long h[2 * 296];
   const int smem = 100 * 1024;
   const int iters = 4096;
+  int noise = 0;
   auto run = [&](auto kern, int cg, int m, int n, int mode, int bmn) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int grid : {2, 296}) {
+    for (int grid : {296}) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(128);
+      cfg.blockDim = dim3(noise ? 384 : 128);
       cfg.dynamicSmemBytes = smem;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
@@ -250,7 +276,7 @@ int main() {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       for (int rep = 0; rep < 2; ++rep) {
-        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, iters, d_out);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, iters, d_out, noise);
         if (e != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
           printf("launch failed %s\n", cudaGetErrorString(cudaGetLastError()));
           exit(1);
@@ -262,12 +288,18 @@ int main() {
       for (int i = 0; i < grid; i += cg) { tot += h[2 * i]; iss += h[2 * i + 1]; ++cnt; }
       tot /= cnt; iss /= cnt;
       const double flop_per_sm_clk = 2.0 * m * n * 16 * iters / tot / cg;
-      printf("{\"cg\": %d, \"m\": %d, \"n\": %d, \"a\": \"%s\", \"b\": \"%s\", \"grid\": %d, \"cyc_per_mma\": %.1f, "
+      printf("{\"noise\": %d, \"cg\": %d, \"m\": %d, \"n\": %d, \"a\": \"%s\", \"b\": \"%s\", \"grid\": %d, \"cyc_per_mma\": %.1f, "
              "\"issue_cyc_per_mma\": %.1f, \"flop_per_sm_clk\": %.0f, \"frac_of_8192\": %.3f}\n",
-             cg, m, n, mode ? "smem" : "tmem", bmn ? "mn" : "k", grid, tot / iters, iss / iters,
+             noise, cg, m, n, mode ? "smem" : "tmem", bmn ? "mn" : "k", grid, tot / iters, iss / iters,
              flop_per_sm_clk, flop_per_sm_clk / 8192);
     }
   };
+  for (noise = 0; noise < 2; ++noise) {
+  run(mma_rate<2, 256, 128, 0, 1>, 2, 256, 128, 0, 1);
+  run(mma_rate<2, 256, 256, 0, 1>, 2, 256, 256, 0, 1);
+  run(mma_rate<2, 256, 128, 1, 0>, 2, 256, 128, 1, 0);
+  }
+  noise = 0;
   run(mma_rate<2, 256, 64, 0, 0>, 2, 256, 64, 0, 0);
   run(mma_rate<2, 256, 128, 0, 0>, 2, 256, 128, 0, 0);
   run(mma_rate<2, 256, 256, 0, 0>, 2, 256, 256, 0, 0);
