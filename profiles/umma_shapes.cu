@@ -230,7 +230,16 @@ __global__ void exp_rate(int iters, long long* out, float* sink) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       float y;
-      if constexpr (POLY) {
+      if constexpr (POLY == 2) {  // two exponentials per MUFU instruction if bf16x2 is native
+        uint32_t in = __float_as_uint(x[i]) & 0xffff0000u, o;
+        in |= in >> 16;
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(o) : "r"(in));
+        y = __uint_as_float(o & 0xffff0000u);
+      } else if constexpr (POLY == 3) {
+        uint32_t in = __float_as_uint(x[i]) & 0xffff0000u, o;
+        asm volatile("ex2.approx.ftz.bf16 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&o)) : "h"((unsigned short)(in >> 16)));
+        y = __uint_as_float((o & 0xffffu) << 16);
+      } else if constexpr (POLY) {
         const float t = x[i] + 12582912.f;          // round to nearest integer in the low mantissa bits
         const float j = t - 12582912.f;
         const float f = x[i] - j;                   // [-0.5, 0.5]
@@ -348,5 +357,7 @@ int main() {
   };
   ex(exp_rate<0>, "mufu");
   ex(exp_rate<1>, "poly3");
+  ex(exp_rate<2>, "mufu bf16x2 (per instruction; x2 exps)");
+  ex(exp_rate<3>, "mufu bf16 scalar");
   return 0;
 }
