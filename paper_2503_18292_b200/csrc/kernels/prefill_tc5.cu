@@ -625,6 +625,10 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
 
+#ifndef JENGA_PF_SPLITO
+#define JENGA_PF_SPLITO 1
+#endif
+
 // Pairs (of every 4 pairs of S columns) whose exponentials the 128-key kernel
 // computes on the FMA pipe instead of the MUFU.
 #ifndef JENGA_PF_EMU2
@@ -663,11 +667,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   constexpr int V_PIECE = VB * kTile * 128;
   constexpr int V_BYTES = (KT / kTile) * V_PIECE;
   constexpr int Q_BYTES = NBOX * kRows * 128;
-  constexpr int NSB = (512 - D) / KT;         // S buffers
-  constexpr int S_COL0 = D;
+  // SPLITO (head_dim 128): one O accumulator per key half, so each softmax warp keeps
+  // its own running max / sum and the two warps of a lane quarter never synchronise
+  // per tile (their load / max / store phases drift apart and overlap each other's
+  // exponentials); the halves are merged once at the end.  TMEM: O_0 | O_1 | 2 S.
+  constexpr bool SPLITO = JENGA_PF_SPLITO && D == 128;
+  constexpr int NO = SPLITO ? 2 : 1;          // O accumulators
+  constexpr int NPH = SPLITO ? 2 : 1;         // P handoffs (p_full / p_empty) per S buffer
+  constexpr int NSB = (512 - NO * D) / KT;    // S buffers
+  constexpr int S_COL0 = NO * D;
   constexpr int HC = KT / 2;                  // S columns per softmax warp
   constexpr uint32_t TMEM_COLS = 512;
-  static_assert(NBOX % 2 == 0 && D + NSB * KT == 512, "128-key kernel shape");
+  static_assert(NBOX % 2 == 0 && NO * D + NSB * KT == 512, "128-key kernel shape");
   constexpr int SW = 2 * kSoftWarps, PW = SW, MW = SW + 1;
 
   extern __shared__ uint8_t smem_raw[];
@@ -682,9 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   uint64_t* v_full = k_empty + NSK;
   uint64_t* v_empty = v_full + NSV;
   uint64_t* s_full = v_empty + NSV;           // both: multicast commit      [buffer]
-  uint64_t* p_full = s_full + NSB;            // leader: 16 softmax warps     [buffer]
-  uint64_t* p_empty = p_full + NSB;           // both: multicast commit      [buffer]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NSB);
+  uint64_t* p_full = s_full + NSB;            // leader: the softmax warps   [buffer][half]
+  uint64_t* p_empty = p_full + NSB * NPH;     // both: multicast commit      [buffer][half]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NSB * NPH);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -712,9 +723,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       jenga_dev::mbar_init(&v_full[i], 1);
       jenga_dev::mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < NSB; ++i) {
-      jenga_dev::mbar_init(&s_full[i], 1);
-      jenga_dev::mbar_init(&p_full[i], 2 * SW);
+    for (int i = 0; i < NSB; ++i) jenga_dev::mbar_init(&s_full[i], 1);
+    for (int i = 0; i < NSB * NPH; ++i) {
+      jenga_dev::mbar_init(&p_full[i], 2 * SW / NPH);
       jenga_dev::mbar_init(&p_empty[i], 1);
     }
     jenga_dev::fence_mbar_init();
@@ -836,17 +847,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         umma2_commit_both_w(&k_empty[jj % NSK]);
         if (lane == 0) PF_TRACE(2, jj);
       };
-      auto issue_pv = [&](int jj) {  // O += P(jj) V_jj
-        jenga_dev::mbar_wait(&p_full[jj % NSB], (jj / NSB) & 1);
-        if (lane == 0) PF_TRACE(0, jj);
-        tc_fence_after();
-        wait_v(jj);
+      auto issue_pv = [&](int jj) {  // O_h += P_h(jj) V_h,jj for each key half h (one half without SPLITO)
         const uint64_t vd = v_desc0 + ((jj % NSV) * V_BYTES >> 4);
         const uint32_t a = tmem + S_COL0 + (jj % NSB) * KT;
+        constexpr int KPH = KT / 16 / NPH;  // 16-key MMAs per handoff
 #pragma unroll
-        for (int k = 0; k < KT / 16; ++k)
-          umma2_ts_w(tmem, a + k * 8, vd + (k * V_PIECE >> 4), id_o, (jj > 0 || k > 0) ? 1u : 0u);
-        umma2_commit_both_w(&p_empty[jj % NSB]);
+        for (int hh = 0; hh < NPH; ++hh) {
+          jenga_dev::mbar_wait(&p_full[(jj % NSB) * NPH + hh], (jj / NSB) & 1);
+          if (lane == 0 && hh == 0) PF_TRACE(0, jj);
+          tc_fence_after();
+          if (hh == 0) wait_v(jj);
+#pragma unroll
+          for (int k = 0; k < KPH; ++k) {
+            const int kk = hh * KPH + k;
+            // P of key half kk / 4 sits in that half's own first 32 S columns
+            umma2_ts_w(tmem + hh * D, a + (kk >> 2) * HC + (kk & 3) * 8, vd + (kk * V_PIECE >> 4), id_o,
+                       (jj > 0 || k > 0) ? 1u : 0u);
+          }
+          umma2_commit_both_w(&p_empty[(jj % NSB) * NPH + hh]);
+        }
         umma2_commit_both_w(&v_empty[jj % NSV]);
       };
       jenga_dev::mbar_wait(q_full, 0);
@@ -906,7 +925,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       if (true) {  // timing-only variant: hand the tile straight back to the MMA issuer
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) arrive_cta0(p_full0 + 8u * sb);
+        if (lane == 0) arrive_cta0(p_full0 + 8u * (sb * NPH + (SPLITO ? hf : 0)));
         continue;
       }
 #endif
@@ -931,11 +950,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], s[i + u]);
       }
       float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      mt *= sc;
+      if constexpr (SPLITO) {
+        // this warp's own running max over its key half; O_hf rescaled alone
+        if (__any_sync(0xffffffffu, mt > m_used + kRescaleThreshold)) {
+          const float m_new = fmaxf(m_used, mt);
+          if (j >= 1) {
+            const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
+            jenga_dev::mbar_wait(&p_empty[((j - 1) % NSB) * NPH + hf], ((j - 1) / NSB) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = hf * D; c < (hf + 1) * D; c += 32) {
+              float v[32];
+              tmem_ld32(tmem + lane_addr + c, v);
+              uint32_t u[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(v[i] * alpha);
+              tmem_st32u(tmem + lane_addr + c, u);
+            }
+            tmem_st_wait();
+            l *= alpha;
+          }
+          m_used = m_new;
+        }
+      } else {
       // Rescale test for the row: its max over both halves.  The two warps of these
       // rows first OR their "some row grew by more than 2^8" votes with one
       // barrier reduction; only then (rarely, after the first tiles) do they
       // exchange the half-row maxima through shared memory.
-      mt *= sc;
       uint32_t grow;
       asm volatile("{\n\t.reg .pred p, q;\n\tsetp.gt.f32 p, %1, %2;\n\tbar.red.or.pred q, %3, %4, p;\n\tselp.u32 %0, 1, 0, q;\n\t}\n"
                    : "=r"(grow) : "f"(mt), "f"(m_used + kRescaleThreshold), "r"(pair_bar), "n"(64) : "memory");
@@ -963,6 +1005,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         }
         m_used = m_new;
       }
+      }
       const float neg = m_used == -INFINITY ? 0.f : -m_used;
       float2 rs[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
       uint32_t pk[HC / 2];
@@ -978,7 +1021,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         rs[(i >> 1) & 3] = fadd2(rs[(i >> 1) & 3], e);
         pk[i / 2] = pack2<T>(e.x, e.y);
       }
-      tmem_st32u(s_addr + hf * (HC / 2), pk);  // P (bf16 pairs) over this half's first S columns
+      // P (bf16 pairs) over the first 32 of this warp's own 64 S columns: the other
+      // warp of the lane quarter may still be reading its half of S (SPLITO: no per-tile sync)
+      tmem_st32u(s_addr + hf * HC, pk);
       {
         const float2 t = fadd2(fadd2(rs[0], rs[1]), fadd2(rs[2], rs[3]));
         l += t.x + t.y;
@@ -990,9 +1035,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       const int ktok0 = (tile_lo + j) * KT;
       const bool boundary = ktok0 < key_lo || ktok0 + KT - 1 > key_hi;
       if (boundary) {
+        // SPLITO: each half zeroes the V rows its own PV reads (it hands off alone)
         uint8_t* vs = vring + (j % NSV) * V_BYTES;
-        for (int idx = threadIdx.x; idx < KT * VB; idx += SW * 32) {
-          const int vrow = idx % KT, chunk = idx / KT;
+        constexpr int ZR = SPLITO ? HC : KT;   // V rows zeroed by this group of threads
+        const int zr0 = SPLITO ? hf * HC : 0;
+        for (int idx = SPLITO ? r : static_cast<int>(threadIdx.x); idx < ZR * VB; idx += (SPLITO ? kRows : SW * 32)) {
+          const int vrow = zr0 + idx % ZR, chunk = idx / ZR;
           const int key = ktok0 + vrow;
           if (key >= key_lo && key <= key_hi) continue;
           uint4* line = reinterpret_cast<uint4*>(vs + (vrow / kTile) * V_PIECE + chunk * kTile * 128 +
@@ -1006,27 +1054,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       __syncwarp();
       if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(7 + 6 * hf, j);
       if (lane == 0) {
+        const uint32_t pf = p_full0 + 8u * (sb * NPH + (SPLITO ? hf : 0));
         if (boundary)
-          arrive_cta0_release_ool(p_full0 + 8u * sb);
+          arrive_cta0_release_ool(pf);
         else
-          arrive_cta0(p_full0 + 8u * sb);
+          arrive_cta0(pf);
       }
     }
-    if (ntiles > 0) jenga_dev::mbar_wait(&p_empty[(ntiles - 1) % NSB], ((ntiles - 1) / NSB) & 1);
+    if (ntiles > 0) {
+#pragma unroll
+      for (int hh = 0; hh < NPH; ++hh)
+        jenga_dev::mbar_wait(&p_empty[((ntiles - 1) % NSB) * NPH + hh], ((ntiles - 1) / NSB) & 1);
+    }
     tc_fence_after();
-    {  // row sum over both halves
+    // merge the halves: row sum (and, SPLITO, the two accumulators' scales)
+    float a_own = 1.f, a_oth = 1.f;
+    {
       float* rd = red + (ntiles & 1) * 2 * kRows;  // the parity the last tile's exchange did not use
+      float* rm = red + ((ntiles & 1) ^ 1) * 2 * kRows;
       rd[hf * kRows + r] = l;
+      if (SPLITO) rm[hf * kRows + r] = m_used;
       asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64) : "memory");
-      l += rd[(hf ^ 1) * kRows + r];
+      const float l_oth = rd[(hf ^ 1) * kRows + r];
+      if (SPLITO) {
+        const float m_oth = rm[(hf ^ 1) * kRows + r];
+        const float m = fmaxf(m_used, m_oth);
+        a_own = m_used == -INFINITY ? 0.f : jenga_dev::fast_exp2(m_used - m);
+        a_oth = m_oth == -INFINITY ? 0.f : jenga_dev::fast_exp2(m_oth - m);
+      }
+      l = l * a_own + l_oth * a_oth;
     }
     const float inv = l > 0.f ? 1.f / l : 0.f;
+    const float a0 = (hf == 0 ? a_own : a_oth) * inv, a1 = (hf == 0 ? a_oth : a_own) * inv;
     T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
 #pragma unroll 1
     for (int c = hf * (D / 2); c < (hf + 1) * (D / 2); c += 32) {
       float v[32];
       if (ntiles > 0) {
         tmem_ld32(tmem + lane_addr + c, v);
+        if constexpr (SPLITO) {
+          float w[32];
+          tmem_ld32(tmem + lane_addr + D + c, w);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = v[i] * a0 + w[i] * a1;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= inv;
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -1034,10 +1108,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       if (row_ok) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i] * inv, v[i + 1] * inv),
-                                                               pack2<T>(v[i + 2] * inv, v[i + 3] * inv),
-                                                               pack2<T>(v[i + 4] * inv, v[i + 5] * inv),
-                                                               pack2<T>(v[i + 6] * inv, v[i + 7] * inv));
+          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i], v[i + 1]), pack2<T>(v[i + 2], v[i + 3]),
+                                                               pack2<T>(v[i + 4], v[i + 5]), pack2<T>(v[i + 6], v[i + 7]));
       }
     }
   }
@@ -1111,9 +1183,9 @@ template <typename T, int D, int G, int NSK, int NSV>
 int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
   constexpr int NBOX = D / kBoxCols;
   constexpr int K_BYTES = (64 / 8) * NBOX * 8 * 128, V_BYTES = 8 * (NBOX / 2) * kTile * 128;
-  constexpr int Q_BYTES = NBOX * kRows * 128, NSB = (512 - D) / 128;
+  constexpr int Q_BYTES = NBOX * kRows * 128;
   const int smem = Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + 2 * 2 * kRows * 4 +
-                   (1 + 2 * NSK + 2 * NSV + 3 * NSB) * 8 + 16 + 1024;
+                   (1 + 2 * NSK + 2 * NSV + 10) * 8 + 16 + 1024;  // 10 >= NSB * (1 + 2 * NPH)
   CUtensorMap k_map, v_map;
   if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
   auto kern = paged_prefill_tc5_wide_kernel<T, D, G, NSK, NSV>;
