@@ -87,3 +87,28 @@ def test_prefill_cross_attention(orc):
     fill_group_kv(eng, 1, [0], seed=1)
     run_prefill(orc, eng, 1, 0, [33, 70])  # text-token queries over all image keys
 
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_prefill_fuzz(orc, case):
+    """Seeded random shapes through both prefill kernels: head_dim 64 / 128 / 256, GQA
+    group 1-8, tokens per page 16-128 (the TMA producer's page / offset split), full or
+    sliding-window attention with a random window, optional soft-capping, ragged chunk
+    lengths (chunks starting mid-page, single tokens, a chunk equal to the whole prompt).
+    Every (token, head) row is checked (elementwise atol = tol * max|want|)."""
+    rng = np.random.default_rng(1000 + case)
+    hd = [128, 256, 128, 256, 64, 128, 256, 128][case % 8]
+    G = [1, 2, 4, 8][case % 4]
+    hkv = [4, 2, 2, 1][case % 4]
+    tpp = int(rng.choice([16, 32, 48, 64, 128]))
+    kind = LayerKind.kSlidingWindow if case % 3 == 1 else LayerKind.kFullAttention
+    window = int(rng.integers(40, 600)) if kind == LayerKind.kSlidingWindow else 0
+    softcap = float(rng.choice([0.0, 30.0])) if case >= 4 else 0.0
+    nreq = int(rng.integers(2, 5))
+    lens = [int(x) for x in rng.integers(1, 1400, nreq)]
+    chunks = [int(min(n, rng.choice([n, rng.integers(1, n + 1), 1]))) for n in lens]
+    geom = ModelGeometry("fz", [GroupGeometry("g", kind, 1, hkv, hkv * G, hd, torch.bfloat16, tpp, window=window)],
+                         softcap=softcap)
+    eng, ids = make_engine(geom, lens, seed=case, defer_window=True)
+    fill_group_kv(eng, 0, [0], seed=case + 7, all_live=True)
+    run_prefill(orc, eng, 0, 0, chunks, seed=case)
