@@ -66,8 +66,8 @@ def test_prefill_gemma_long_chunk_softcap(orc):
 
 
 def test_prefill_d128_long_chunk_pingpong(orc):
-    """Llama / Jamba heads (D=128, G=4: the ping-pong pair kernel) on long chunks
-    at a 5k context, full and SWA-1000 with soft-capping."""
+    """Llama / Jamba heads (D=128, G=4: the split-accumulator 128-key kernel) on long
+    chunks at a 5k context, full and SWA-1000 with soft-capping."""
     geom = ModelGeometry("llama-p", [
         GroupGeometry("full", LayerKind.kFullAttention, 1, 8, 32, 128, torch.bfloat16, 16),
         GroupGeometry("window", LayerKind.kSlidingWindow, 1, 8, 32, 128, torch.bfloat16, 16, window=1000)],
