@@ -54,8 +54,11 @@ def parse():
     p.add_argument("--tpp", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--e2e-chunks", default="3", choices=["3", "geo"],
-                   help="layer chunks of the e2e copies: three each way, or geometric (1, 2, 4, ... layers; +2%% e2e on the 176 MB/step prefix mix, -0.2..-0.7%% on the others)")
+    p.add_argument("--e2e-timeline", action="store_true",
+                   help="profiling only (with --no-graph): print when each input chunk lands vs when its first layer starts")
+    p.add_argument("--e2e-chunks", default="geo", choices=["geo", "3"],
+                   help="layer chunks of the e2e copies: geometric (1, 2, 4, ... layers: each chunk lands while "
+                        "the layers before it run) or three each way (the round-2 first-session form)")
     p.add_argument("--e2e-io", default="overlap", choices=["overlap", "serial", "none", "in-only", "out-only"],
                    help="profiling only: how the e2e leg moves q/k/v and outputs (overlap = the measured "
                         "contract: side-stream chunks; serial = before / after the step on its stream; "
@@ -401,11 +404,12 @@ def run_ours(a, rank, world, local_rank):
         eng.append()
         return eng.pack_tables()
 
-    def device_step(totals=None, ev=None, hooks=None, attention=True):
+    def device_step(totals=None, ev=None, hooks=None, attention=True, upload=True):
         """Device half: table upload, then per layer KV write + decode (fixed
         shape, so it can be graph-captured).  attention=False: everything but
         the attention launches (the roofline's subtrahend)."""
-        eng.upload_tables(None, totals)
+        if upload:
+            eng.upload_tables(None, totals)
         pg = {}
         for i, (g, l) in enumerate(wl.layers):
             kind = eng.tables[g].geom.kind
@@ -561,14 +565,13 @@ def run_ours(a, rank, world, local_rank):
         # Copies ride a side stream in layer chunks: later inputs land while the
         # first layers decode, outputs leave while the last layers decode.  Every
         # cross-stream wait / event record inside the step breaks the PDL chain
-        # (~15 us each: one chunk per layer costs +0.6 ms a step), so only three
-        # chunks each way: inputs [0,1) [1,3) [3,L) and outputs [0,L-3) [L-3,L-1)
-        # [L-1,L).  Measured (Gemma step, 22 MB in / 11 MB out; --e2e-io):
-        # outputs cost 0.05 ms, the host sync 0.05 ms, the inputs ~0.45 ms whatever
-        # the chunking (1,3 / 1,3,7,15,31 / 1,2,4,...,32 / 2,6,14,30 all within
-        # 0.7%) — H2D DMA writes into HBM under the decode's read stream cost
-        # about what they would serialised; kernels reading q / K / V straight
-        # from pinned host memory (no HBM writes) measured slower still.
+        # (~15 us each: one chunk per layer costs +0.6 ms a step), so the chunks grow
+        # geometrically (1, 2, 4, ... layers): each chunk lands while the layers
+        # before it run.  The step's page-table delta is uploaded before the chunk
+        # copies are queued — they share the H2D copy engine, and behind them the
+        # table copy held layer 0 back by their whole transfer time (the round-2
+        # first-session e2e lost 0.45 ms a Gemma step and 3 ms a prefix-mix step to
+        # exactly that; --e2e-timeline shows when each chunk lands vs its layer).
         cs = torch.cuda.Stream(device=dev)
         if a.e2e_chunks == "geo":  # 1, 2, 4, ... layers: each chunk's copy hides behind the previous chunk's layers
             geo = [0]
@@ -579,7 +582,9 @@ def run_ours(a, rank, world, local_rank):
         else:
             in_bounds = sorted({0, min(1, na), min(3, na), na})
             out_bounds = sorted({0, max(na - 3, 0), max(na - 1, 0), na})
-        ev_in = [torch.cuda.Event() for _ in range(len(in_bounds) - 1)]
+        ev_in = [torch.cuda.Event(enable_timing=a.e2e_timeline) for _ in range(len(in_bounds) - 1)]
+        tl = {"t0": torch.cuda.Event(enable_timing=True),
+              "layer": [torch.cuda.Event(enable_timing=True) for _ in range(na)]} if a.e2e_timeline else None
         ev_out = [torch.cuda.Event() for _ in range(len(out_bounds) - 1)]
         in_start = {in_bounds[c]: c for c in range(len(in_bounds) - 1)}
         out_end = {out_bounds[c + 1] - 1: c for c in range(len(out_bounds) - 1)}
@@ -594,6 +599,13 @@ def run_ours(a, rank, world, local_rank):
                 if a.e2e_io == "serial":
                     ho.copy_(out, non_blocking=True)
                 return
+            if tl is not None:
+                tl["t0"].record(torch.cuda.current_stream())
+            # the page-table delta first: the chunk copies below share the H2D copy engine,
+            # and queued behind them the table copy held layer 0 back by their whole
+            # transfer time (--e2e-timeline: layer 0 started 0.51 ms into the step, 0.43
+            # ms after the q/k/v chunks had been queued)
+            eng.upload_tables(None, totals)
             cs.wait_stream(torch.cuda.current_stream())  # previous step's readers of q/k/v are done
             with torch.cuda.stream(cs):
                 for c in range(len(in_bounds) - 1):
@@ -606,9 +618,14 @@ def run_ours(a, rank, world, local_rank):
                     vn[lo:hi].copy_(hv[lo:hi], non_blocking=True)
                     ev_in[c].record(cs)
             cur = torch.cuda.current_stream()
-            chunk_hooks = {"before": lambda j: cur.wait_event(ev_in[in_start[j]]) if j in in_start else None,
+            def before(j):
+                if j in in_start:
+                    cur.wait_event(ev_in[in_start[j]])
+                if tl is not None:
+                    tl["layer"][j].record(cur)
+            chunk_hooks = {"before": before,
                            "after": lambda j: ev_out[out_end[j]].record(cur) if j in out_end else None}
-            device_step(totals, hooks=chunk_hooks)
+            device_step(totals, hooks=chunk_hooks, upload=False)
             for c in range(len(out_bounds) - 1):
                 cs.wait_event(ev_out[c])
                 if a.e2e_io == "in-only":
@@ -664,6 +681,13 @@ def run_ours(a, rank, world, local_rank):
         if world > 1:
             e_ms = max_over_ranks(e_ms, dev)
             e_bytes = int(sum_over_ranks(e_bytes, dev))
+        if tl is not None:
+            torch.cuda.synchronize()
+            rows = [f"chunk {in_bounds[c]}-{in_bounds[c + 1]} landed {tl['t0'].elapsed_time(ev_in[c]):.3f} ms; "
+                    f"layer {in_bounds[c]} started {tl['t0'].elapsed_time(tl['layer'][in_bounds[c]]):.3f} ms"
+                    for c in range(len(in_bounds) - 1)]
+            rows.append(f"last layer started {tl['t0'].elapsed_time(tl['layer'][na - 1]):.3f} ms")
+            print("e2e timeline (last step): " + " | ".join(rows), file=sys.stderr)
         e2e = {"value": round(e_bytes / (e_ms * 1e-3) / 1e9, 1), "unit": "GB/s",
                "h2d_bytes_per_step": int(q.nbytes + kn.nbytes + vn.nbytes + pending["pl_bytes"] / a.steps),
                "d2h_bytes_per_step": int(out.nbytes),
