@@ -699,7 +699,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  const int unit = blockIdx.x >> 1, h = blockIdx.y, b = blockIdx.z;
+  // Heaviest first: with causal masks the last query blocks of a chunk attend the
+  // most keys, so the grid hands out units in descending order (shorter tail).
+  const int unit = static_cast<int>(gridDim.x >> 1) - 1 - static_cast<int>(blockIdx.x >> 1);
+  const int h = blockIdx.y, b = blockIdx.z;
   const int c_len = p.cu_q[b + 1] - p.cu_q[b];
   const int pt0 = 2 * unit * QB;
   if (pt0 >= c_len) return;  // uniform over the pair
