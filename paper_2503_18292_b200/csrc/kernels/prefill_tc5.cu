@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 #include <utility>
 
@@ -50,7 +51,7 @@ struct Prefill5Params {
   const int32_t* seq_lens;
   int kind;
   int64_t window;
-  int max_blocks, hq, hkv, tpp, q_blocks;
+  int max_blocks, hq, hkv, tpp, q_blocks, batch;
   float qscale, cap_log2, inv_cap;
 };
 
@@ -136,6 +137,32 @@ __device__ __forceinline__ void tmem_ld64(uint32_t addr, float (&v)[64]) {
       : "memory");
 #pragma unroll
   for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Two 32-column TMEM loads (any two column offsets) behind one tcgen05.wait::ld.
+__device__ __forceinline__ void tmem_ld32x2(uint32_t a0, uint32_t a1, float (&v)[32], float (&w)[32]) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%64];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, "
+      "%45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%65];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(a0), "r"(a1)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    v[i] = __uint_as_float(r[i]);
+    w[i] = __uint_as_float(r[32 + i]);
+  }
 }
 
 __device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32]) {
@@ -571,6 +598,23 @@ __device__ long long g_pf_trace[16][64];
 #define PF_TRACE(ev, j) do { } while (0)
 #endif
 
+// Q rows of one CTA: 4-D box {64 columns, G heads, QB tokens, 1 chunk} over q viewed as
+// [chunk][token][head][64 columns], landing as rows r = t*G + g of 128 B (swizzled).
+__device__ __forceinline__ void tma_load_q_pair(void* dst, const void* tmap, int32_t head, int32_t token, int32_t chunk,
+                                                uint32_t cluster_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(jenga_dev::smem_u32(dst)),
+      "l"(tmap), "r"(cluster_bar), "r"(0), "r"(head), "r"(token), "r"(chunk)
+      : "memory");
+}
+// TMA store of one staged 64-column chunk of a CTA's 128 output rows (same 4-D view as Q).
+__device__ __forceinline__ void tma_store_out(const void* tmap, const void* src, int32_t head, int32_t token,
+                                              int32_t chunk) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(tmap),
+               "r"(jenga_dev::smem_u32(src)), "r"(0), "r"(head), "r"(token), "r"(chunk)
+               : "memory");
+}
 // Whole-warp forms: the warp runs the issue loop convergently (operands are
 // warp-uniform, so they stay in uniform registers) and elect.sync picks the one
 // issuing lane inside the asm -- no per-instruction ELECT / BRA.U.ANY loop or
@@ -638,7 +682,8 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 template <typename T, int D, int G, int NSK, int NSV>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2) * 32, 1)
     paged_prefill_tc5_wide_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
-                                  const __grid_constant__ CUtensorMap v_map) {
+                                  const __grid_constant__ CUtensorMap v_map, const __grid_constant__ CUtensorMap q_map,
+                                  const __grid_constant__ CUtensorMap o_map) {
   // 128-key tiles on a CTA pair (cta_group::2, M = 256 query rows, 128 per CTA).
   // S = Q K^T is issued with N = 128 keys (64-key instructions run the tensor
   // core at ~72%: they cannot be issued faster than ~45 cycles each), so Q lives
@@ -653,8 +698,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   // reductions and TMEM stores.
   // K and V stream through separate rings (K of tile j + 1 is needed before V of
   // tile j): K slot released when the tile's S MMAs complete, V slot when its PV
-  // MMAs complete.  Shared-memory layouts (128-byte swizzle):
-  //   Q: [chunk c][128 rows][128 B]              (written by the softmax threads)
+  // MMAs complete.
+  // Persistent: one CTA pair per two SMs walks the work units (request, KV head,
+  // pair of query blocks), ordered heaviest first (the last query blocks of a causal
+  // chunk attend the most keys) and dealt to the clusters boustrophedon.  Tile-indexed state
+  // (rings, S buffers, P handoffs) runs on a per-CTA tile counter across units, so
+  // the next unit's Q (TMA, once the last S MMA of the unit read the old one) and
+  // K/V stream in while the current unit's last tiles and epilogue run; TMEM and
+  // barriers are set up once.  Shared-memory layouts (128-byte swizzle):
+  //   Q: [chunk c][128 rows][128 B]              (one 4-D TMA box {64, G heads, QB tokens, 1} per chunk)
   //   K: [8-key group][chunk c][8 rows][128 B]   (one 4-D TMA box per 16-key piece; this CTA's 64 keys)
   //   V: [16-key piece][chunk c][16 rows][128 B] (one 3-D box per piece; this CTA's half of head_dim)
   constexpr int KT = 128;
@@ -685,7 +737,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   uint8_t* qs = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* kring = qs + Q_BYTES;
   uint8_t* vring = kring + NSK * K_BYTES;
-  float* red = reinterpret_cast<float*>(vring + NSV * V_BYTES);  // [tile parity][half][row]
+  uint8_t* ostage = vring + NSV * V_BYTES;    // one 64-column chunk of the CTA's output rows
+  float* red = reinterpret_cast<float*>(ostage + kRows * 128);  // [tile parity][half][row]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 2 * kRows);
   uint64_t* q_full = bars;                    // leader: all softmax warps of the pair
   uint64_t* k_full = bars + 1;                // leader: both CTAs' TMA bytes
@@ -695,29 +748,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   uint64_t* s_full = v_empty + NSV;           // both: multicast commit      [buffer]
   uint64_t* p_full = s_full + NSB;            // leader: the softmax warps   [buffer][half]
   uint64_t* p_empty = p_full + NSB * NPH;     // both: multicast commit      [buffer][half]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_empty + NSB * NPH);
+  uint64_t* q_empty = p_empty + NSB * NPH;     // both: multicast commit after a unit's last S MMA
+  uint64_t* o_free = q_empty + 1;              // leader: all softmax warps, after a unit's O readout
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  // Heaviest first: with causal masks the last query blocks of a chunk attend the
-  // most keys, so the grid hands out units in descending order (shorter tail).
-  const int unit = static_cast<int>(gridDim.x >> 1) - 1 - static_cast<int>(blockIdx.x >> 1);
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int c_len = p.cu_q[b + 1] - p.cu_q[b];
-  const int pt0 = 2 * unit * QB;
-  if (pt0 >= c_len) return;  // uniform over the pair
-  const int n = p.seq_lens[b];
+  if (threadIdx.x == 0) PF_TRACE(15, 0);  // kernel entry (trace variant)
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int npairs = (p.q_blocks + 1) / 2;
+  const int nunits = npairs * p.hkv * p.batch;
+  struct Unit {
+    int b, h, pt0, c_len, n, key_lo, key_hi, tile_lo, ntiles;
+    bool live;
+  };
+  // unit u -> (query pair, KV head, request): the query pairs of one (request, head)
+  // are consecutive -- units in flight together share that K/V through L2 (spreading
+  // them over heads first measured 11% slower) -- last (heaviest) pair first
+  auto unit_at = [&](int u) {
+    Unit x;
+    const int qp = npairs - 1 - u % npairs;
+    x.h = (u / npairs) % p.hkv;
+    x.b = u / (npairs * p.hkv);
+    x.c_len = p.cu_q[x.b + 1] - p.cu_q[x.b];
+    x.pt0 = 2 * qp * QB;
+    x.live = x.pt0 < x.c_len;
+    x.n = p.seq_lens[x.b];
+    const int pos0 = x.n - x.c_len + x.pt0;
+    const int pos1 = x.n - x.c_len + min(x.pt0 + 2 * QB, x.c_len) - 1;  // union of the pair's query rows
+    x.key_lo = 0;
+    x.key_hi = p.kind == JENGA_KIND_CROSS_ATTENTION ? x.n - 1 : pos1;
+    if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) x.key_lo = static_cast<int>(pos0 + 1 - p.window);
+    x.tile_lo = x.key_lo / KT;
+    x.ntiles = x.live && x.key_hi >= x.key_lo ? x.key_hi / KT - x.tile_lo + 1 : 0;
+    return x;
+  };
   const bool cross = p.kind == JENGA_KIND_CROSS_ATTENTION;
-  const int pos0 = n - c_len + pt0;
-  const int pos1 = n - c_len + min(pt0 + 2 * QB, c_len) - 1;  // union of the pair's query rows
-  int key_lo = 0;
-  const int key_hi = cross ? n - 1 : pos1;
-  if (p.kind == JENGA_KIND_SLIDING_WINDOW && pos0 + 1 > p.window) key_lo = static_cast<int>(pos0 + 1 - p.window);
-  const int tile_lo = key_lo / KT;
-  const int ntiles = key_hi >= key_lo ? key_hi / KT - tile_lo + 1 : 0;
+  // this cluster's k-th unit: rounds of `nclusters` units dealt boustrophedon (the
+  // cluster that got a round's heaviest unit gets the next round's lightest), which
+  // evens out the per-cluster totals of the heaviest-first unit order
+  auto snake = [&](int k) { return k * nclusters + ((k & 1) ? nclusters - 1 - cid : cid); };
 
   if (threadIdx.x == 0) {
-    jenga_dev::mbar_init(q_full, 2 * SW);
+    jenga_dev::mbar_init(q_full, 1);
     for (int i = 0; i < NSK; ++i) {
       jenga_dev::mbar_init(&k_full[i], 1);
       jenga_dev::mbar_init(&k_empty[i], 1);
@@ -731,6 +804,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       jenga_dev::mbar_init(&p_full[i], 2 * SW / NPH);
       jenga_dev::mbar_init(&p_empty[i], 1);
     }
+    jenga_dev::mbar_init(q_empty, 1);
+    jenga_dev::mbar_init(o_free, 2 * SW);
     jenga_dev::fence_mbar_init();
   }
   if (warp == MW) {
@@ -743,79 +818,96 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int32_t* table = p.table + static_cast<int64_t>(b) * p.max_blocks;
 
   if (warp == PW) {
     // Lane l < 8 owns the 16-key page piece l of every tile: its block index by
     // multiply-shift division, its page from the warp's table look-ahead (lane i
     // holds table[base + i] / table[base + 32 + i]) by one shuffle, its arena row
-    // by one multiply-add; the lanes then issue their own TMA boxes.
-    if (lane == 0) { jenga_dev::prefetch_tmap(&k_map); jenga_dev::prefetch_tmap(&v_map); }
+    // by one multiply-add; the lanes then issue their own TMA boxes.  Per unit, the
+    // unit's Q first (once the previous unit's last S MMA has read the old Q).
+    if (lane == 0) {
+      jenga_dev::prefetch_tmap(&k_map);
+      jenga_dev::prefetch_tmap(&v_map);
+      jenga_dev::prefetch_tmap(&q_map);
+    }
     const uint64_t policy = jenga_dev::l2_policy_evict_first();
     const int64_t row_bytes = D * 2;
-    const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(h) * 2 * p.tpp;
     const int64_t page_rows = static_cast<int64_t>(p.page_stride) / row_bytes;
     const uint32_t tpp = static_cast<uint32_t>(p.tpp);
     uint32_t lg = 0;
     while ((1u << lg) < tpp) ++lg;
     const uint32_t dm = static_cast<uint32_t>(((1ull << (31 + lg)) + tpp - 1) / tpp), ds = lg - 1;  // tpp >= 16
     const int mb = p.max_blocks;
-    int base = static_cast<int>(static_cast<uint32_t>(tile_lo * KT) / tpp);
-    int cur = __ldg(table + min(base + lane, mb - 1)), nxt = __ldg(table + min(base + 32 + lane, mb - 1));
     const int piece = lane & 7;
-    auto row_for = [&](int jj) {  // warp-uniform call; this lane's piece of tile jj
-      const uint32_t tok = static_cast<uint32_t>((tile_lo + jj) * KT + piece * kTile);
-      const int blk = static_cast<int>(__umulhi(tok, dm) >> ds);
-      const int off = static_cast<int>(tok - static_cast<uint32_t>(blk) * tpp);
-      const int blk0 = __shfl_sync(0xffffffffu, blk, 0);
-      while (blk0 >= base + 32) {
-        base += 32;
-        cur = nxt;
-        nxt = __ldg(table + min(base + 32 + lane, mb - 1));
-      }
-      const int rel = blk - base;  // < 64: a tile spans at most 8 blocks
-      const int a = __shfl_sync(0xffffffffu, cur, rel & 31), c = __shfl_sync(0xffffffffu, nxt, rel & 31);
-      const int32_t page = rel < 32 ? a : c;
-      return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + off);
-    };
     const int k_lane0 = static_cast<int>(rank) * (KH / kTile);  // this CTA's half of the keys
-    auto issue_k = [&](int jj, int32_t row) {
-      const int st = jj % NSK;
-      if (jj >= NSK) jenga_dev::mbar_wait(&k_empty[st], ((jj / NSK) & 1) ^ 1);
-      const uint32_t full0 = map_to_cta0(&k_full[st]);
-#ifdef JENGA_PF_NOLOAD
-      if (lane == 0 && rank == 0) arrive_cta0(full0);  // timing-only variant: no K/V traffic
-      return;
-#endif
-      if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * K_BYTES);
-      if (lane >= k_lane0 && lane < k_lane0 + KH / kTile)
-        tma_load_4d_pair(kring + st * K_BYTES + (lane - k_lane0) * 2 * K_GROUP, &k_map, row, full0, policy);
-    };
-    auto issue_v = [&](int jj, int32_t row) {
-      const int st = jj % NSV;
-      if (jj >= NSV) jenga_dev::mbar_wait(&v_empty[st], ((jj / NSV) & 1) ^ 1);
-      const uint32_t full0 = map_to_cta0(&v_full[st]);
-#ifdef JENGA_PF_NOLOAD
-      if (lane == 0 && rank == 0) arrive_cta0(full0);
-      return;
-#endif
-      if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * V_BYTES);
-      if (lane < KT / kTile)
-        tma_load_3d_pair(vring + st * V_BYTES + lane * V_PIECE, &v_map, row + p.tpp, static_cast<int>(rank) * VB,
-                         full0, policy);
-    };
-    int32_t row_cur = 0, row_nxt = 0;
-    if (ntiles > 0) {
-      row_cur = row_for(0);
-      issue_k(0, row_cur);
-    }
-    for (int j = 0; j < ntiles; ++j) {
-      if (j + 1 < ntiles) {  // K runs one tile ahead of V
-        row_nxt = row_for(j + 1);
-        issue_k(j + 1, row_nxt);
+    int g0 = 0, nu = 0;  // tiles / live units this CTA processed before the current unit
+    for (int k = 0, u = cid; u < nunits; ++k, u = snake(k)) {
+      const Unit x = unit_at(u);
+      if (x.ntiles == 0) continue;
+      {  // Q of this unit: this CTA's 128 rows, one box per 64-column chunk
+        if (nu > 0) jenga_dev::mbar_wait(q_empty, (nu - 1) & 1);
+        const uint32_t qf0 = map_to_cta0(q_full);
+        if (lane == 0 && rank == 0) expect_tx_cta0(qf0, 2 * Q_BYTES);
+        if (lane < NBOX)
+          tma_load_q_pair(qs + lane * kRows * 128, &q_map, x.h * G, p.cu_q[x.b] + x.pt0 + static_cast<int>(rank) * QB,
+                          lane, qf0);
       }
-      issue_v(j, row_cur);
-      row_cur = row_nxt;
+      const int32_t* table = p.table + static_cast<int64_t>(x.b) * mb;
+      const int64_t base_row = static_cast<int64_t>(p.start_offset) / row_bytes + static_cast<int64_t>(x.h) * 2 * p.tpp;
+      int base = static_cast<int>(static_cast<uint32_t>(x.tile_lo * KT) / tpp);
+      int cur = __ldg(table + min(base + lane, mb - 1)), nxt = __ldg(table + min(base + 32 + lane, mb - 1));
+      auto row_for = [&](int jj) {  // warp-uniform call; this lane's piece of tile jj
+        const uint32_t tok = static_cast<uint32_t>((x.tile_lo + jj) * KT + piece * kTile);
+        const int blk = static_cast<int>(__umulhi(tok, dm) >> ds);
+        const int off = static_cast<int>(tok - static_cast<uint32_t>(blk) * tpp);
+        const int blk0 = __shfl_sync(0xffffffffu, blk, 0);
+        while (blk0 >= base + 32) {
+          base += 32;
+          cur = nxt;
+          nxt = __ldg(table + min(base + 32 + lane, mb - 1));
+        }
+        const int rel = blk - base;  // < 64: a tile spans at most 8 blocks
+        const int a = __shfl_sync(0xffffffffu, cur, rel & 31), c = __shfl_sync(0xffffffffu, nxt, rel & 31);
+        const int32_t page = rel < 32 ? a : c;
+        return static_cast<int32_t>(base_row + static_cast<int64_t>(max(page, 0)) * page_rows + off);
+      };
+      auto issue_k = [&](int jj, int32_t row) {
+        const int gg = g0 + jj, st = gg % NSK;
+        if (gg >= NSK) jenga_dev::mbar_wait(&k_empty[st], ((gg / NSK) & 1) ^ 1);
+        const uint32_t full0 = map_to_cta0(&k_full[st]);
+#ifdef JENGA_PF_NOLOAD
+        if (lane == 0 && rank == 0) arrive_cta0(full0);  // timing-only variant: no K/V traffic
+        return;
+#endif
+        if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * K_BYTES);
+        if (lane >= k_lane0 && lane < k_lane0 + KH / kTile)
+          tma_load_4d_pair(kring + st * K_BYTES + (lane - k_lane0) * 2 * K_GROUP, &k_map, row, full0, policy);
+      };
+      auto issue_v = [&](int jj, int32_t row) {
+        const int gg = g0 + jj, st = gg % NSV;
+        if (gg >= NSV) jenga_dev::mbar_wait(&v_empty[st], ((gg / NSV) & 1) ^ 1);
+        const uint32_t full0 = map_to_cta0(&v_full[st]);
+#ifdef JENGA_PF_NOLOAD
+        if (lane == 0 && rank == 0) arrive_cta0(full0);
+        return;
+#endif
+        if (lane == 0 && rank == 0) expect_tx_cta0(full0, 2 * V_BYTES);
+        if (lane < KT / kTile)
+          tma_load_3d_pair(vring + st * V_BYTES + lane * V_PIECE, &v_map, row + p.tpp, static_cast<int>(rank) * VB,
+                           full0, policy);
+      };
+      int32_t row_cur = row_for(0), row_nxt = 0;
+      issue_k(0, row_cur);
+      for (int j = 0; j < x.ntiles; ++j) {
+        if (j + 1 < x.ntiles) {  // K runs one tile ahead of V
+          row_nxt = row_for(j + 1);
+          issue_k(j + 1, row_nxt);
+        }
+        issue_v(j, row_cur);
+        row_cur = row_nxt;
+      }
+      g0 += x.ntiles;
+      ++nu;
     }
   } else if (warp == MW) {
     if (rank == 0) {  // the whole warp runs the loop; elect.sync issues
@@ -825,89 +917,94 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       const uint64_t q_desc0 = umma_desc(jenga_dev::smem_u32(qs), 16, 1024);
       const uint64_t k_desc0 = umma_desc(jenga_dev::smem_u32(kring), 16, K_GROUP);
       const uint64_t v_desc0 = umma_desc(jenga_dev::smem_u32(vring), kTile * 128, 1024);
-      auto wait_v = [&](int jj) {
-        jenga_dev::mbar_wait(&v_full[jj % NSV], (jj / NSV) & 1);
-        tc_fence_after();
-      };
-      // boundary tiles (first / last) get V rows zeroed by the softmax threads after
-      // s_full: their S is issued only once V has landed too
-      auto wait_k = [&](int jj) {
-        jenga_dev::mbar_wait(&k_full[jj % NSK], (jj / NSK) & 1);
-        tc_fence_after();
-        const int kt0 = (tile_lo + jj) * KT;
-        if (kt0 < key_lo || kt0 + KT - 1 > key_hi) wait_v(jj);
-      };
-      auto issue_s = [&](int jj) {  // S(jj) = Q K_jj^T into buffer jj % NSB
-        wait_k(jj);
-        const uint64_t kd = k_desc0 + ((jj % NSK) * K_BYTES >> 4);
-        const uint32_t d = tmem + S_COL0 + (jj % NSB) * KT;
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
-          umma2_ss_w(d, q_desc0 + (((k >> 2) * kRows * 128 + (k & 3) * 32) >> 4), kd + off, id_s, k > 0 ? 1u : 0u);
-        }
-        umma2_commit_both_w(&s_full[jj % NSB]);
-        umma2_commit_both_w(&k_empty[jj % NSK]);
-        if (lane == 0) PF_TRACE(2, jj);
-      };
-      auto issue_pv = [&](int jj) {  // O_h += P_h(jj) V_h,jj for each key half h (one half without SPLITO)
-        const uint64_t vd = v_desc0 + ((jj % NSV) * V_BYTES >> 4);
-        const uint32_t a = tmem + S_COL0 + (jj % NSB) * KT;
-        constexpr int KPH = KT / 16 / NPH;  // 16-key MMAs per handoff
-#pragma unroll
-        for (int hh = 0; hh < NPH; ++hh) {
-          jenga_dev::mbar_wait(&p_full[(jj % NSB) * NPH + hh], (jj / NSB) & 1);
-          if (lane == 0 && hh == 0) PF_TRACE(0, jj);
+      int g0 = 0, nu = 0;
+      for (int k = 0, u = cid; u < nunits; ++k, u = snake(k)) {
+        const Unit x = unit_at(u);
+        if (x.ntiles == 0) continue;
+        auto wait_v = [&](int jj) {
+          const int gg = g0 + jj;
+          jenga_dev::mbar_wait(&v_full[gg % NSV], (gg / NSV) & 1);
           tc_fence_after();
-          if (hh == 0) wait_v(jj);
+        };
+        // boundary tiles (first / last) get V rows zeroed by the softmax threads after
+        // s_full: their S is issued only once V has landed too
+        auto wait_k = [&](int jj) {
+          const int gg = g0 + jj;
+          jenga_dev::mbar_wait(&k_full[gg % NSK], (gg / NSK) & 1);
+          tc_fence_after();
+          const int kt0 = (x.tile_lo + jj) * KT;
+          if (kt0 < x.key_lo || kt0 + KT - 1 > x.key_hi) wait_v(jj);
+        };
+        auto issue_s = [&](int jj) {  // S(jj) = Q K_jj^T into buffer gg % NSB
+          wait_k(jj);
+          const int gg = g0 + jj;
+          const uint64_t kd = k_desc0 + ((gg % NSK) * K_BYTES >> 4);
+          const uint32_t d = tmem + S_COL0 + (gg % NSB) * KT;
 #pragma unroll
-          for (int k = 0; k < KPH; ++k) {
-            const int kk = hh * KPH + k;
-            // P of key half kk / 4 sits in that half's own first 32 S columns
-            umma2_ts_w(tmem + hh * D, a + (kk >> 2) * HC + (kk & 3) * 8, vd + (kk * V_PIECE >> 4), id_o,
-                       (jj > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
+            umma2_ss_w(d, q_desc0 + (((k >> 2) * kRows * 128 + (k & 3) * 32) >> 4), kd + off, id_s, k > 0 ? 1u : 0u);
           }
-          umma2_commit_both_w(&p_empty[(jj % NSB) * NPH + hh]);
+          umma2_commit_both_w(&s_full[gg % NSB]);
+          umma2_commit_both_w(&k_empty[gg % NSK]);
+          if (jj == x.ntiles - 1) umma2_commit_both_w(q_empty);  // the unit's last read of Q
+          if (lane == 0) PF_TRACE(2, gg);
+        };
+        auto issue_pv = [&](int jj) {  // O_h += P_h(jj) V_h,jj for each key half h (one half without SPLITO)
+          const int gg = g0 + jj;
+          const uint64_t vd = v_desc0 + ((gg % NSV) * V_BYTES >> 4);
+          const uint32_t a = tmem + S_COL0 + (gg % NSB) * KT;
+          constexpr int KPH = KT / 16 / NPH;  // 16-key MMAs per handoff
+#pragma unroll
+          for (int hh = 0; hh < NPH; ++hh) {
+            jenga_dev::mbar_wait(&p_full[(gg % NSB) * NPH + hh], (gg / NSB) & 1);
+            if (lane == 0 && hh == 0) PF_TRACE(0, gg);
+            tc_fence_after();
+            if (hh == 0) wait_v(jj);
+#pragma unroll
+            for (int k = 0; k < KPH; ++k) {
+              const int kk = hh * KPH + k;
+              // P of key half kk / 4 sits in that half's own first 32 S columns
+              umma2_ts_w(tmem + hh * D, a + (kk >> 2) * HC + (kk & 3) * 8, vd + (kk * V_PIECE >> 4), id_o,
+                         (jj > 0 || k > 0) ? 1u : 0u);
+            }
+            umma2_commit_both_w(&p_empty[(gg % NSB) * NPH + hh]);
+          }
+          umma2_commit_both_w(&v_empty[gg % NSV]);
+        };
+        jenga_dev::mbar_wait(q_full, nu & 1);
+        if (lane == 0) PF_TRACE(3, nu);
+        tc_fence_after();
+        for (int j = 0; j < NSB - 1 && j < x.ntiles; ++j) issue_s(j);
+        for (int j = 0; j < x.ntiles; ++j) {
+          // S(j + NSB - 1) goes to the buffer PV(j - 1) released (in order), ahead of PV(j)
+          if (j + NSB - 1 < x.ntiles) issue_s(j + NSB - 1);
+          if (j == 0 && nu > 0) {  // O is overwritten by this unit's first PV: the previous unit read it out
+            jenga_dev::mbar_wait(o_free, (nu - 1) & 1);
+            tc_fence_after();
+          }
+          issue_pv(j);
         }
-        umma2_commit_both_w(&v_empty[jj % NSV]);
-      };
-      jenga_dev::mbar_wait(q_full, 0);
-      tc_fence_after();
-      for (int j = 0; j < NSB - 1 && j < ntiles; ++j) issue_s(j);
-      for (int j = 0; j < ntiles; ++j) {
-        // S(j + NSB - 1) goes to the buffer PV(j - 1) released (in order), ahead of PV(j)
-        if (j + NSB - 1 < ntiles) issue_s(j + NSB - 1);
-        issue_pv(j);
+        g0 += x.ntiles;
+        ++nu;
       }
     }
   } else {
     const int hf = warp >> 2;                   // column half of every S tile / O
     const int r = threadIdx.x & (kRows - 1);    // query row == TMEM lane
     const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const int t0 = pt0 + static_cast<int>(rank) * QB;
-    const int tok = t0 + r / G;
-    const bool row_ok = tok < c_len;
-    const int ipos = n - c_len + tok;
     const uint32_t p_full0 = map_to_cta0(&p_full[0]);
+    const uint32_t o_free0 = map_to_cta0(o_free);
     const uint32_t pair_bar = 1 + (warp & 3);   // named barrier of the two warps sharing these rows
-    {  // this thread's half of its Q row -> shared memory, 128-byte swizzled K-major
-      const uint4* qrow = reinterpret_cast<const uint4*>(
-          static_cast<const T*>(p.q) + (static_cast<int64_t>(p.cu_q[b] + (row_ok ? tok : 0)) * p.hq + h * G + r % G) * D);
-      uint8_t* qt = qs + r * 128;
-#pragma unroll
-      for (int cc = 0; cc < NBOX / 2; ++cc) {
-        const int c = hf * (NBOX / 2) + cc;
-        uint4 x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = row_ok ? jenga_dev::ld_nc_v4(qrow + c * 8 + u) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<uint4*>(qt + c * kRows * 128 + ((u ^ (r & 7)) << 4)) = x[u];
-      }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) arrive_cta0_release(map_to_cta0(q_full));
-    }
+    int g0 = 0, nus = 0;
+    for (int k = 0, u = cid; u < nunits; ++k, u = snake(k)) {
+    const Unit x = unit_at(u);
+    if (!x.live) continue;
+    const int ntiles = x.ntiles, tile_lo = x.tile_lo, key_lo = x.key_lo, key_hi = x.key_hi, n = x.n;
+    const int t0 = x.pt0 + static_cast<int>(rank) * QB;
+    const int tok = t0 + r / G;
+    const bool row_ok = tok < x.c_len;
+    const int ipos = n - x.c_len + tok;
     int lo_r = 0, hi_r = cross ? n - 1 : ipos;
     if (p.kind == JENGA_KIND_SLIDING_WINDOW && static_cast<int64_t>(ipos) + 1 > p.window)
       lo_r = static_cast<int>(ipos + 1 - p.window);
@@ -918,11 +1015,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
     const float qi = p.qscale * p.inv_cap;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
-      const int sb = j % NSB;
+      const int gg = g0 + j;
+      const int sb = gg % NSB;
       const uint32_t s_addr = tmem + lane_addr + S_COL0 + sb * KT;
       const int kc0 = (tile_lo + j) * KT + hf * HC;   // key of this warp's first column
-      jenga_dev::mbar_wait(&s_full[sb], (j / NSB) & 1);
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(4 + 6 * hf, j);
+      jenga_dev::mbar_wait(&s_full[sb], (gg / NSB) & 1);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(4 + 6 * hf, gg);
       tc_fence_after();
 #ifdef JENGA_PF_NOSOFTMAX
       if (true) {  // timing-only variant: hand the tile straight back to the MMA issuer
@@ -934,7 +1032,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
 #endif
       float s[HC];
       tmem_ld64(s_addr + hf * HC, s);
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(5 + 6 * hf, j);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(5 + 6 * hf, gg);
       if (softcap) {
 #pragma unroll
         for (int i = 0; i < HC; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
@@ -960,7 +1058,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
           const float m_new = fmaxf(m_used, mt);
           if (j >= 1) {
             const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
-            jenga_dev::mbar_wait(&p_empty[((j - 1) % NSB) * NPH + hf], ((j - 1) / NSB) & 1);
+            jenga_dev::mbar_wait(&p_empty[((gg - 1) % NSB) * NPH + hf], ((gg - 1) / NSB) & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int c = hf * D; c < (hf + 1) * D; c += 32) {
@@ -992,7 +1090,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         const float m_new = fmaxf(m_used, mt);
         if (j >= 1) {
           const float alpha = m_used == -INFINITY ? 1.f : jenga_dev::fast_exp2(m_used - m_new);
-          jenga_dev::mbar_wait(&p_empty[(j - 1) % NSB], ((j - 1) / NSB) & 1);
+          jenga_dev::mbar_wait(&p_empty[(gg - 1) % NSB], ((gg - 1) / NSB) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int c = hf * (D / 2); c < (hf + 1) * (D / 2); c += 32) {
@@ -1032,14 +1130,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         l += t.x + t.y;
       }
       tmem_st_wait();
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(6 + 6 * hf, j);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(6 + 6 * hf, gg);
       // zero this CTA's V columns of keys outside the pair's range; the issuer waited
       // for this tile's V before S(j), so s_full(j) implies it has landed
       const int ktok0 = (tile_lo + j) * KT;
       const bool boundary = ktok0 < key_lo || ktok0 + KT - 1 > key_hi;
       if (boundary) {
         // SPLITO: each half zeroes the V rows its own PV reads (it hands off alone)
-        uint8_t* vs = vring + (j % NSV) * V_BYTES;
+        uint8_t* vs = vring + (gg % NSV) * V_BYTES;
         constexpr int ZR = SPLITO ? HC : KT;   // V rows zeroed by this group of threads
         const int zr0 = SPLITO ? hf * HC : 0;
         for (int idx = SPLITO ? r : static_cast<int>(threadIdx.x); idx < ZR * VB; idx += (SPLITO ? kRows : SW * 32)) {
@@ -1055,7 +1153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       }
       tc_fence_before();
       __syncwarp();
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(7 + 6 * hf, j);
+      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(7 + 6 * hf, gg);
       if (lane == 0) {
         const uint32_t pf = p_full0 + 8u * (sb * NPH + (SPLITO ? hf : 0));
         if (boundary)
@@ -1065,10 +1163,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       }
     }
     if (ntiles > 0) {
+      const int gl = g0 + ntiles - 1;  // the unit's last tile
 #pragma unroll
       for (int hh = 0; hh < NPH; ++hh)
-        jenga_dev::mbar_wait(&p_empty[((ntiles - 1) % NSB) * NPH + hh], ((ntiles - 1) / NSB) & 1);
+        jenga_dev::mbar_wait(&p_empty[(gl % NSB) * NPH + hh], (gl / NSB) & 1);
     }
+    if (warp == 0 && lane == 0 && rank == 0) PF_TRACE(8, nus);
     tc_fence_after();
     // merge the halves: row sum (and, SPLITO, the two accumulators' scales)
     float a_own = 1.f, a_oth = 1.f;
@@ -1086,36 +1186,83 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         a_oth = m_oth == -INFINITY ? 0.f : jenga_dev::fast_exp2(m_oth - m);
       }
       l = l * a_own + l_oth * a_oth;
+      asm volatile("bar.sync %0, %1;\n" ::"r"(pair_bar), "n"(64) : "memory");  // slots reusable by the next unit
     }
+    if (warp == 0 && lane == 0 && rank == 0) PF_TRACE(9, nus);
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const float a0 = (hf == 0 ? a_own : a_oth) * inv, a1 = (hf == 0 ? a_oth : a_own) * inv;
-    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[b] + tok) * p.hq + h * G + r % G) * D;
+    T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[x.b] + tok) * p.hq + x.h * G + r % G) * D;
+    // Output, one 64-column chunk of the CTA's 128 rows at a time: the owning half's
+    // warps scale and pack their rows into a 128-byte-swizzled staging tile and one
+    // thread writes it with a TMA store (rows of a block are (token, head) pairs 512 B
+    // apart in out: per-thread 16-byte stores ran at ~12 B/clk per SM and made the
+    // epilogue ~6k cycles).  A block that ends past the chunk (the last of a ragged
+    // chunk) is written row by row instead, so no other request's rows are touched.
+    // O is handed back to the MMA issuer (o_free) after each warp's last TMEM load.
+    const bool full_block = t0 + QB <= x.c_len;
+    constexpr int CPH = NBOX / 2;  // 64-column chunks per half
 #pragma unroll 1
-    for (int c = hf * (D / 2); c < (hf + 1) * (D / 2); c += 32) {
-      float v[32];
-      if (ntiles > 0) {
-        tmem_ld32(tmem + lane_addr + c, v);
-        if constexpr (SPLITO) {
-          float w[32];
-          tmem_ld32(tmem + lane_addr + D + c, w);
+    for (int cc = 0; cc < NBOX; ++cc) {
+      const bool mine = cc / CPH == hf;
+      if (mine) {
+        const int c = cc * 64;
+        uint32_t pk[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = v[i] * a0 + w[i] * a1;
-        } else {
+        for (int hc = 0; hc < 2; ++hc) {  // two 32-column halves of the chunk
+          float v[32];
+          if (ntiles > 0) {
+            if constexpr (SPLITO) {
+              float w[32];
+              tmem_ld32x2(tmem + lane_addr + c + hc * 32, tmem + lane_addr + D + c + hc * 32, v, w);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= inv;
+              for (int i = 0; i < 32; ++i) v[i] = v[i] * a0 + w[i] * a1;
+            } else {
+              tmem_ld32(tmem + lane_addr + c + hc * 32, v);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= inv;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[hc * 16 + i] = pack2<T>(v[2 * i], v[2 * i + 1]);
         }
-      } else {
+        if (ntiles > 0 && cc % CPH == CPH - 1) {  // this warp's last read of O for the unit
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_cta0(o_free0);
+        }
+        if (full_block) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          for (int u2 = 0; u2 < 8; ++u2)
+            *reinterpret_cast<uint4*>(ostage + r * 128 + ((u2 ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * u2], pk[4 * u2 + 1], pk[4 * u2 + 2], pk[4 * u2 + 3]);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        } else if (row_ok) {
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2)
+            *reinterpret_cast<uint4*>(outp + c + u2 * 8) =
+                make_uint4(pk[4 * u2], pk[4 * u2 + 1], pk[4 * u2 + 2], pk[4 * u2 + 3]);
+        }
       }
-      if (row_ok) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(outp + c + i) = make_uint4(pack2<T>(v[i], v[i + 1]), pack2<T>(v[i + 2], v[i + 3]),
-                                                               pack2<T>(v[i + 4], v[i + 5]), pack2<T>(v[i + 6], v[i + 7]));
+      if (full_block) {
+        asm volatile("bar.sync 5, %0;\n" ::"n"(SW * 32) : "memory");  // the chunk is staged
+        if (threadIdx.x == 0) {
+          tma_store_out(&o_map, ostage, x.h * G, p.cu_q[x.b] + t0, cc);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // staging tile reusable
+        }
+        asm volatile("bar.sync 5, %0;\n" ::"n"(SW * 32) : "memory");
       }
     }
+    if (warp == 0 && lane == 0 && rank == 0) PF_TRACE(1, nus);
+    ++nus;
+    g0 += ntiles;
+    }
   }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // output stores complete
+  if (warp == 0 && lane == 0) PF_TRACE(14, 0);  // softmax epilogue done (trace variant)
   tc_fence_before();
   cluster_sync();  // the peer's last remote arrivals and MMAs are done
   if (warp == MW) {
@@ -1183,29 +1330,56 @@ int launch_tc5(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) 
 }
 
 template <typename T, int D, int G, int NSK, int NSV>
-int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int batch, int total_tokens) {
   constexpr int NBOX = D / kBoxCols;
   constexpr int K_BYTES = (64 / 8) * NBOX * 8 * 128, V_BYTES = 8 * (NBOX / 2) * kTile * 128;
   constexpr int Q_BYTES = NBOX * kRows * 128;
-  const int smem = Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + 2 * 2 * kRows * 4 +
-                   (1 + 2 * NSK + 2 * NSV + 10) * 8 + 16 + 1024;  // 10 >= NSB * (1 + 2 * NPH)
-  CUtensorMap k_map, v_map;
+  const int smem = Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + kRows * 128 + 2 * 2 * kRows * 4 +
+                   (1 + 2 * NSK + 2 * NSV + 12) * 8 + 16 + 1024;  // 12 >= NSB * (1 + 2 * NPH) + 2
+  CUtensorMap k_map, v_map, q_map, o_map;
   if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
+  for (int which = 0; which < 2; ++which) {  // q and out [T][Hq][D] as [chunk][token][head][64 columns]
+    const CUtensorMapDataType dt =
+        dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(kBoxCols), static_cast<cuuint64_t>(prm.hq),
+                          static_cast<cuuint64_t>(total_tokens), static_cast<cuuint64_t>(NBOX)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(prm.hq) * D * 2, 128};
+    cuuint32_t box[4] = {kBoxCols, G, kRows / G, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    void* base = which == 0 ? const_cast<void*>(prm.q) : prm.out;
+    if (encode_fn()(which == 0 ? &q_map : &o_map, dt, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return jenga_dev::set_error(JENGA_ERR_CUDA,
+                                  "prefill: q/out tensor map encode failed (q and out must be 16-byte aligned)");
+  }
   auto kern = paged_prefill_tc5_wide_kernel<T, D, G, NSK, NSV>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  dim3 grid((prm.q_blocks + 1) / 2 * 2, prm.hkv, batch);  // a CTA pair per 2 query blocks
-  kern<<<grid, (2 * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map);
+  // Persistent: one CTA pair per two SMs (fewer when there are fewer work units), so a
+  // unit's prologue (Q, first K/V, first S) overlaps the previous unit's tail.  Against
+  // one CTA pair per unit (hardware-scheduled): 256-token chunks at 2k +18%, D=128
+  // +2..+11%, SWA +4%, D=256 full 2k chunks at 8k -1.7% (profiles/r02_prefill_experiments.md).
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t units = static_cast<int64_t>((prm.q_blocks + 1) / 2) * prm.hkv * batch;
+  const int64_t clusters = std::min<int64_t>(units, std::max(sms / 2, 1));
+  kern<<<dim3(static_cast<unsigned>(2 * clusters)), (2 * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map, q_map,
+                                                                                        o_map);
   return jenga_dev::check_launch("paged_prefill_tc5_wide_kernel");
 }
 
 template <typename T, int D, int NSK, int NSV>
-int dispatch_wide(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+int dispatch_wide(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch, int total_tokens) {
   switch (G) {
-    case 1: return launch_tc5_wide<T, D, 1, NSK, NSV>(prm, dtype, s, batch);
-    case 2: return launch_tc5_wide<T, D, 2, NSK, NSV>(prm, dtype, s, batch);
-    case 4: return launch_tc5_wide<T, D, 4, NSK, NSV>(prm, dtype, s, batch);
-    case 8: return launch_tc5_wide<T, D, 8, NSK, NSV>(prm, dtype, s, batch);
+    case 1: return launch_tc5_wide<T, D, 1, NSK, NSV>(prm, dtype, s, batch, total_tokens);
+    case 2: return launch_tc5_wide<T, D, 2, NSK, NSV>(prm, dtype, s, batch, total_tokens);
+    case 4: return launch_tc5_wide<T, D, 4, NSK, NSV>(prm, dtype, s, batch, total_tokens);
+    case 8: return launch_tc5_wide<T, D, 8, NSK, NSV>(prm, dtype, s, batch, total_tokens);
   }
   return JENGA_ERR_UNSUPPORTED;
 }
@@ -1233,10 +1407,10 @@ int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int 
 // TMEM: 2 x (O 128 + Q 64 + S 64)); one CTA per query block at 64, whose single
 // 64-column chunk is too narrow to split V across a pair.  64-token K/V tiles.
 template <typename T>
-int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch) {
+int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch, int total_tokens) {
   switch (D) {
-    case 256: return dispatch_wide<T, 256, JENGA_PF_NSK256, JENGA_PF_NSV256>(G, prm, dtype, s, batch);
-    case 128: return dispatch_wide<T, 128, 6, 5>(G, prm, dtype, s, batch);
+    case 256: return dispatch_wide<T, 256, JENGA_PF_NSK256, JENGA_PF_NSV256>(G, prm, dtype, s, batch, total_tokens);
+    case 128: return dispatch_wide<T, 128, 5, 5>(G, prm, dtype, s, batch, total_tokens);
     case 64: return dispatch_g<T, 64, 6>(G, prm, dtype, s, batch);
   }
   return jenga_dev::set_error(JENGA_ERR_UNSUPPORTED, "jenga_paged_prefill: head_dim must be 64, 128 or 256");
@@ -1305,8 +1479,9 @@ JENGA_EXPORT int jenga_paged_prefill(void* arena_base, jenga_layer_view view, in
   }
   prm.q = q;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int rc = dtype == JENGA_BF16 ? dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, s, batch)
-                                     : dispatch_d<__half>(head_dim, G, prm, dtype, s, batch);
+  prm.batch = batch;
+  const int rc = dtype == JENGA_BF16 ? dispatch_d<__nv_bfloat16>(head_dim, G, prm, dtype, s, batch, total_tokens)
+                                     : dispatch_d<__half>(head_dim, G, prm, dtype, s, batch, total_tokens);
   if (rc == JENGA_OK) note_launch(s, kLaunchSerializing);
   return rc;
 }
