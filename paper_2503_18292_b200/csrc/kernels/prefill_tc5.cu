@@ -1,13 +1,14 @@
 // Chunked-prefill paged attention on the 5th-generation tensor cores
 // (tcgen05.mma + TMEM), bf16/fp16.  Rows are (token, query head) pairs
 // r = t*G + g, 128 rows per query block.  Two kernels:
-//  * paged_prefill_tc5_wide_kernel (head_dim 128 and 256): a cluster of 2 CTAs,
-//    tcgen05.mma.cta_group::2 with M = 256 over two adjacent query blocks, 128-key
-//    tiles (S = Q K^T issued with N = 128), Q in shared memory, TMEM = O plus
-//    (512 - D) / 128 S buffers so S runs ahead of the softmax; each SM holds half
-//    of every K/V tile (its 64 keys of K, its half of head_dim of V); 8 softmax
-//    warps (two per TMEM lane quarter, each owning half of the key columns), a
-//    TMA producer warp and a whole-warp MMA issuer.
+//  * paged_prefill_tc5_wide_kernel (head_dim 128 and 256): persistent clusters of 2
+//    CTAs walking (query pair, KV head, request) units, tcgen05.mma.cta_group::2
+//    with M = 256 over two adjacent query blocks, 128-key tiles (S = Q K^T issued
+//    with N = 128), Q in shared memory (TMA), TMEM = O plus S buffers so S runs
+//    ahead of the softmax; each SM holds half of every K/V tile (its 64 keys of K,
+//    its half of head_dim of V); 8 softmax warps (two per TMEM lane quarter, each
+//    owning half of the key columns), a TMA producer warp and a whole-warp MMA
+//    issuer; output staged in shared memory and written by TMA stores.
 //  * paged_prefill_tc5_kernel (head_dim 64): one CTA per query block,
 //    cta_group::1, 64-key tiles, Q in TMEM (its single 64-column chunk is too
 //    narrow to split V across a pair).
