@@ -1361,12 +1361,9 @@ int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
   // unit's prologue (Q, first K/V, first S) overlaps the previous unit's tail.  Against
   // one CTA pair per unit (hardware-scheduled): 256-token chunks at 2k +18%, D=128
   // +2..+11%, SWA +4%, D=256 full 2k chunks at 8k -1.7% (profiles/r02_prefill_experiments.md).
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return jenga_dev::set_error(JENGA_ERR_CUDA, "jenga_paged_prefill: cannot query the SM count");
   const int64_t units = static_cast<int64_t>((prm.q_blocks + 1) / 2) * prm.hkv * batch;
   const int64_t clusters = std::min<int64_t>(units, std::max(sms / 2, 1));
   kern<<<dim3(static_cast<unsigned>(2 * clusters)), (2 * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map, q_map,
