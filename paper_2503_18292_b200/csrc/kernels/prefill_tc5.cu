@@ -609,13 +609,6 @@ __device__ __forceinline__ void tma_load_q_pair(void* dst, const void* tmap, int
       "l"(tmap), "r"(cluster_bar), "r"(0), "r"(head), "r"(token), "r"(chunk)
       : "memory");
 }
-// TMA store of one staged 64-column chunk of a CTA's 128 output rows (same 4-D view as Q).
-__device__ __forceinline__ void tma_store_out(const void* tmap, const void* src, int32_t head, int32_t token,
-                                              int32_t chunk) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(tmap),
-               "r"(jenga_dev::smem_u32(src)), "r"(0), "r"(head), "r"(token), "r"(chunk)
-               : "memory");
-}
 // Whole-warp forms: the warp runs the issue loop convergently (operands are
 // warp-uniform, so they stay in uniform registers) and elect.sync picks the one
 // issuing lane inside the asm -- no per-instruction ELECT / BRA.U.ANY loop or
@@ -683,8 +676,7 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 template <typename T, int D, int G, int NSK, int NSV>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2) * 32, 1)
     paged_prefill_tc5_wide_kernel(const Prefill5Params p, const __grid_constant__ CUtensorMap k_map,
-                                  const __grid_constant__ CUtensorMap v_map, const __grid_constant__ CUtensorMap q_map,
-                                  const __grid_constant__ CUtensorMap o_map) {
+                                  const __grid_constant__ CUtensorMap v_map, const __grid_constant__ CUtensorMap q_map) {
   // 128-key tiles on a CTA pair (cta_group::2, M = 256 query rows, 128 per CTA).
   // S = Q K^T is issued with N = 128 keys (64-key instructions run the tensor
   // core at ~72%: they cannot be issued faster than ~45 cycles each), so Q lives
@@ -738,7 +730,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
   uint8_t* qs = smem_raw + ((1024 - (jenga_dev::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* kring = qs + Q_BYTES;
   uint8_t* vring = kring + NSK * K_BYTES;
-  uint8_t* ostage = vring + NSV * V_BYTES;    // one 64-column chunk of the CTA's output rows
+  uint8_t* ostage = vring + NSV * V_BYTES;    // output staging, 2 KiB per softmax warp
   float* red = reinterpret_cast<float*>(ostage + kRows * 128);  // [tile parity][half][row]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 2 * kRows);
   uint64_t* q_full = bars;                    // leader: all softmax warps of the pair
@@ -1193,76 +1185,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const float a0 = (hf == 0 ? a_own : a_oth) * inv, a1 = (hf == 0 ? a_oth : a_own) * inv;
     T* outp = static_cast<T*>(p.out) + (static_cast<int64_t>(p.cu_q[x.b] + tok) * p.hq + x.h * G + r % G) * D;
-    // Output, one 64-column chunk of the CTA's 128 rows at a time: the owning half's
-    // warps scale and pack their rows into a 128-byte-swizzled staging tile and one
-    // thread writes it with a TMA store (rows of a block are (token, head) pairs 512 B
-    // apart in out: per-thread 16-byte stores ran at ~12 B/clk per SM and made the
-    // epilogue ~6k cycles).  A block that ends past the chunk (the last of a ragged
-    // chunk) is written row by row instead, so no other request's rows are touched.
-    // O is handed back to the MMA issuer (o_free) after each warp's last TMEM load.
-    const bool full_block = t0 + QB <= x.c_len;
-    constexpr int CPH = NBOX / 2;  // 64-column chunks per half
+    // Output in 32-column steps.  Each warp stages its 32 rows' 64-byte pieces in its
+    // own 2 KiB of shared memory (XOR-swizzled, conflict-free both ways) and reads them
+    // back transposed, four lanes per row, so every store instruction writes 8 rows x
+    // 64 contiguous bytes -- 8 L2 lines instead of 32 (rows are (token, head) pairs
+    // 256-512 B apart in out; the per-thread row stores and a TMA-store staging with
+    // CTA-wide barriers both left the epilogue at ~6k cycles).  O is handed back to the
+    // MMA issuer (o_free) after each warp's last TMEM load.
+    uint8_t* wst = ostage + warp * 2048;
+    const int64_t row0 = static_cast<int64_t>(p.cu_q[x.b] + t0) * p.hq + x.h * G;  // out row of r = 0
+    constexpr int OSTEPS = D / 2 / 32;
 #pragma unroll 1
-    for (int cc = 0; cc < NBOX; ++cc) {
-      const bool mine = cc / CPH == hf;
-      if (mine) {
-        const int c = cc * 64;
-        uint32_t pk[32];
+    for (int it = 0; it < OSTEPS; ++it) {
+      const int c = hf * (D / 2) + it * 32;
+      float v[32];
+      if (ntiles > 0) {
+        if constexpr (SPLITO) {
+          float w[32];
+          tmem_ld32x2(tmem + lane_addr + c, tmem + lane_addr + D + c, v, w);
 #pragma unroll
-        for (int hc = 0; hc < 2; ++hc) {  // two 32-column halves of the chunk
-          float v[32];
-          if (ntiles > 0) {
-            if constexpr (SPLITO) {
-              float w[32];
-              tmem_ld32x2(tmem + lane_addr + c + hc * 32, tmem + lane_addr + D + c + hc * 32, v, w);
+          for (int i = 0; i < 32; ++i) v[i] = v[i] * a0 + w[i] * a1;
+        } else {
+          tmem_ld32(tmem + lane_addr + c, v);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = v[i] * a0 + w[i] * a1;
-            } else {
-              tmem_ld32(tmem + lane_addr + c + hc * 32, v);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= inv;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[hc * 16 + i] = pack2<T>(v[2 * i], v[2 * i + 1]);
+          for (int i = 0; i < 32; ++i) v[i] *= inv;
         }
-        if (ntiles > 0 && cc % CPH == CPH - 1) {  // this warp's last read of O for the unit
+        if (it == OSTEPS - 1) {  // O read out: the next unit's first PV may overwrite it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_cta0(o_free0);
         }
-        if (full_block) {
+      } else {
 #pragma unroll
-          for (int u2 = 0; u2 < 8; ++u2)
-            *reinterpret_cast<uint4*>(ostage + r * 128 + ((u2 ^ (r & 7)) << 4)) =
-                make_uint4(pk[4 * u2], pk[4 * u2 + 1], pk[4 * u2 + 2], pk[4 * u2 + 3]);
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        } else if (row_ok) {
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      // stage: row `lane` of this warp, piece q at slot (lane & 1) * 4 + (q ^ ((lane >> 1) & 3))
 #pragma unroll
-          for (int u2 = 0; u2 < 8; ++u2)
-            *reinterpret_cast<uint4*>(outp + c + u2 * 8) =
-                make_uint4(pk[4 * u2], pk[4 * u2 + 1], pk[4 * u2 + 2], pk[4 * u2 + 3]);
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(wst + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+            make_uint4(pack2<T>(v[8 * q], v[8 * q + 1]), pack2<T>(v[8 * q + 2], v[8 * q + 3]),
+                       pack2<T>(v[8 * q + 4], v[8 * q + 5]), pack2<T>(v[8 * q + 6], v[8 * q + 7]));
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int rr = (lane >> 2) + 8 * k, q = lane & 3;  // warp-local row, piece
+        const uint4 d = *reinterpret_cast<const uint4*>(wst + rr * 64 + ((q ^ ((rr >> 1) & 3)) << 4));
+        const int rw = (warp & 3) * 32 + rr;  // CTA row
+        if (t0 + rw / G < x.c_len) {
+          T* dst = static_cast<T*>(p.out) + (row0 + static_cast<int64_t>(rw / G) * p.hq + rw % G) * D + c + q * 8;
+          *reinterpret_cast<uint4*>(dst) = d;
         }
       }
-      if (full_block) {
-        asm volatile("bar.sync 5, %0;\n" ::"n"(SW * 32) : "memory");  // the chunk is staged
-        if (threadIdx.x == 0) {
-          tma_store_out(&o_map, ostage, x.h * G, p.cu_q[x.b] + t0, cc);
-          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // staging tile reusable
-        }
-        asm volatile("bar.sync 5, %0;\n" ::"n"(SW * 32) : "memory");
-      }
+      __syncwarp();
     }
     if (warp == 0 && lane == 0 && rank == 0) PF_TRACE(1, nus);
     ++nus;
     g0 += ntiles;
     }
   }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // output stores complete
   if (warp == 0 && lane == 0) PF_TRACE(14, 0);  // softmax epilogue done (trace variant)
   tc_fence_before();
   cluster_sync();  // the peer's last remote arrivals and MMAs are done
@@ -1337,9 +1317,9 @@ int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
   constexpr int Q_BYTES = NBOX * kRows * 128;
   const int smem = Q_BYTES + NSK * K_BYTES + NSV * V_BYTES + kRows * 128 + 2 * 2 * kRows * 4 +
                    (1 + 2 * NSK + 2 * NSV + 12) * 8 + 16 + 1024;  // 12 >= NSB * (1 + 2 * NPH) + 2
-  CUtensorMap k_map, v_map, q_map, o_map;
+  CUtensorMap k_map, v_map, q_map;
   if (int rc = encode_kv_maps(prm, dtype, D, NBOX / 2, &k_map, &v_map)) return rc;
-  for (int which = 0; which < 2; ++which) {  // q and out [T][Hq][D] as [chunk][token][head][64 columns]
+  {  // q [T][Hq][D] as [chunk][token][head][64 columns]
     const CUtensorMapDataType dt =
         dtype == JENGA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     cuuint64_t dims[4] = {static_cast<cuuint64_t>(kBoxCols), static_cast<cuuint64_t>(prm.hq),
@@ -1347,12 +1327,11 @@ int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
     cuuint64_t strides[3] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(prm.hq) * D * 2, 128};
     cuuint32_t box[4] = {kBoxCols, G, kRows / G, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    void* base = which == 0 ? const_cast<void*>(prm.q) : prm.out;
-    if (encode_fn()(which == 0 ? &q_map : &o_map, dt, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    if (encode_fn()(&q_map, dt, 4, const_cast<void*>(prm.q), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return jenga_dev::set_error(JENGA_ERR_CUDA,
-                                  "prefill: q/out tensor map encode failed (q and out must be 16-byte aligned)");
+                                  "prefill: q tensor map encode failed (q must be 16-byte aligned)");
   }
   auto kern = paged_prefill_tc5_wide_kernel<T, D, G, NSK, NSV>;
   static std::atomic<uint64_t> configured{0};
@@ -1366,8 +1345,7 @@ int launch_tc5_wide(const Prefill5Params& prm, int dtype, cudaStream_t s, int ba
     return jenga_dev::set_error(JENGA_ERR_CUDA, "jenga_paged_prefill: cannot query the SM count");
   const int64_t units = static_cast<int64_t>((prm.q_blocks + 1) / 2) * prm.hkv * batch;
   const int64_t clusters = std::min<int64_t>(units, std::max(sms / 2, 1));
-  kern<<<dim3(static_cast<unsigned>(2 * clusters)), (2 * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map, q_map,
-                                                                                        o_map);
+  kern<<<dim3(static_cast<unsigned>(2 * clusters)), (2 * kSoftWarps + 2) * 32, smem, s>>>(prm, k_map, v_map, q_map);
   return jenga_dev::check_launch("paged_prefill_tc5_wide_kernel");
 }
 

@@ -27,6 +27,7 @@ print("per unit (softmax warp 0): p_empty(last) wait done / exchange done / outp
 for k in range(8):
     if buf[8, k]:
         print(f"  unit {k}: {buf[8, k] - t0} / {buf[9, k] - t0} / {buf[1, k] - t0}; q_full {buf[3, k] - t0}")
+print("chunk stores issued+read (thread 0, unit 0..1):", [int(buf[12, k] - t0) if buf[12, k] else 0 for k in range(8)])
 print("entry -> first s_full:", buf[4, 0] - buf[15, 0], " last s_full -> epilogue done:",
       buf[14, 0] - buf[4][buf[4] > 0].max(), " entry -> done:", buf[14, 0] - buf[15, 0])
 per = np.diff(buf[4, 10:40]).mean()
