@@ -1378,10 +1378,10 @@ int dispatch_g(int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int 
   return JENGA_ERR_UNSUPPORTED;
 }
 
-// Kernel per head_dim: CTA pairs (cta_group::2, M = 256) at 256 — each SM streams
-// half of every K/V tile; ping-ponged CTA pairs at 128 (two query tiles per CTA,
-// TMEM: 2 x (O 128 + Q 64 + S 64)); one CTA per query block at 64, whose single
-// 64-column chunk is too narrow to split V across a pair.  64-token K/V tiles.
+// Kernel per head_dim: persistent CTA pairs (cta_group::2, M = 256, 128-key tiles) at
+// 256 and 128 -- each SM streams half of every K/V tile (K ring 2 / V ring 2 stages at
+// 256, 5 / 5 at 128); one CTA per query block with 64-key tiles at 64, whose single
+// 64-column chunk is too narrow to split V across a pair.
 template <typename T>
 int dispatch_d(int D, int G, const Prefill5Params& prm, int dtype, cudaStream_t s, int batch, int total_tokens) {
   switch (D) {

@@ -1,6 +1,6 @@
 #!/bin/bash
-# --set full captures of the three prefill kernels on B=4 x 2048-token chunks at 8k
-# (full layer): D=256 CTA pair without and with Gemma's softcap, D=128 ping-pong.
+# --set full captures of the prefill kernel on B=4 x 2048-token chunks at 8k (full
+# layer): D=256 without and with Gemma's softcap, D=128.
 set -u
 OUT=${1:-gpurun_out/prefill_ncu}
 mkdir -p $OUT
