@@ -112,3 +112,26 @@ def test_prefill_fuzz(orc, case):
     eng, ids = make_engine(geom, lens, seed=case, defer_window=True)
     fill_group_kv(eng, 0, [0], seed=case + 7, all_live=True)
     run_prefill(orc, eng, 0, 0, chunks, seed=case)
+
+
+@pytest.mark.parametrize("hd,kind", [(128, LayerKind.kFullAttention), (256, LayerKind.kSlidingWindow),
+                                     (128, LayerKind.kCrossAttention)])
+def test_prefill_many_requests_persistent(orc, hd, kind):
+    """Many ragged requests: several work units per persistent CTA pair, with units past
+    their request's chunk (skipped), sliding windows that leave most keys out, and
+    single-token chunks -- the per-CTA tile / unit counters must stay in step across
+    units of different lengths."""
+    rng = np.random.default_rng(77 + hd)
+    nreq = 24
+    lens = [int(x) for x in rng.integers(1, 700, nreq)]
+    chunks = [int(min(n, rng.choice([n, rng.integers(1, n + 1), 1]))) for n in lens]
+    window = 57 if kind == LayerKind.kSlidingWindow else 0
+    G = 2 if hd == 256 else 4
+    groups = [GroupGeometry("g", kind, 1, 2, 2 * G, hd, torch.bfloat16, 16, window=window)]
+    img, g = None, 0
+    if kind == LayerKind.kCrossAttention:  # text tokens attend the image tokens the cross group stores
+        groups.insert(0, GroupGeometry("self", LayerKind.kFullAttention, 1, 2, 2 * G, hd, torch.bfloat16, 16))
+        img, g = [(lambda p, k=k: p <= 40 * (k % 5 + 1)) for k in range(nreq)], 1
+    eng, ids = make_engine(ModelGeometry("many", groups), lens, seed=hd, defer_window=True, image_flags=img)
+    fill_group_kv(eng, g, [0], seed=3, all_live=kind != LayerKind.kCrossAttention)
+    run_prefill(orc, eng, g, 0, chunks)
