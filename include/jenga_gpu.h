@@ -436,8 +436,11 @@ int jenga_paged_decode_append(void* arena_base, jenga_layer_view view, int kind,
  * request b's queries are q[cu_q[b] .. cu_q[b+1]) — its newest ordinals
  * (0-based positions seq_lens[b]-C_b .. seq_lens[b]-1), whose K/V were already
  * written with jenga_reshape_and_cache.  Causal (+ window for SWA); cross
- * attention attends all seq_lens[b] image keys.  q/out [total_tokens][Hq][D];
- * max_chunk = max C_b.  arena_base must come from jenga_arena_create. */
+ * attention attends all seq_lens[b] image keys.  q/out [total_tokens][Hq][D],
+ * 16-byte aligned (q is read by TMA; total_tokens = cu_q[batch]);
+ * max_chunk = max C_b.  arena_base must come from jenga_arena_create.  head_dim
+ * 128 / 256 run on a persistent grid (one CTA pair per two SMs) that needs no
+ * workspace. */
 int jenga_paged_prefill(void* arena_base, jenga_layer_view view, int kind, int dtype,
                         uint64_t window, const void* q, void* out, const int32_t* cu_q,
                         int total_tokens, int max_chunk, const int32_t* block_table,
