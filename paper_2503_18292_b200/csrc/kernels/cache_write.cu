@@ -144,8 +144,17 @@ __device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, u
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
 
+// Scaling copies (the in-place Mamba state update) run 4 warps per CTA: the
+// shared-memory scale pass of a 16 KiB chunk by one warp serialised ~0.5 us per chunk
+// behind the bulk copies.
+#ifndef JENGA_COPY_SCALE_THREADS
+#define JENGA_COPY_SCALE_THREADS 128
+#endif
+template <bool kScale>
+constexpr int copy_threads() { return kScale ? JENGA_COPY_SCALE_THREADS : 32; }
+
 template <int kCopyChunk, int kCopyStages, bool kScale>
-__global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
+__global__ void __launch_bounds__(copy_threads<kScale>()) paged_copy_kernel(const CopyArgs a) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ uint64_t full[kCopyStages];
   // PDL: the next kernel may get resident; our reads/writes wait for the previous one.
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
     for (int i = 0; i < kCopyStages; ++i) jenga_dev::mbar_init(&full[i], 1);
     jenga_dev::fence_mbar_init();
   }
-  if (kScale) __syncwarp();
+  if (kScale) __syncthreads();
   jenga_dev::pdl_wait();
   // arena pages stream through L2 once; a dense staging buffer (Mamba state
   // between gather, the SSM update and scatter) is kept resident
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
     jenga_dev::mbar_wait(&full[st], (k / kCopyStages) & 1);
     if (kScale) {
       float4* f = reinterpret_cast<float4*>(ring + st * kCopyChunk);
-      for (uint32_t i = threadIdx.x; i < ring_c[st].bytes / 16; i += 32) {
+      for (uint32_t i = threadIdx.x; i < ring_c[st].bytes / 16; i += blockDim.x) {
         float4 x = f[i];
         x.x *= a.scale;
         x.y *= a.scale;
@@ -198,7 +207,7 @@ __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
         f[i] = x;
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> bulk-copy reads
-      __syncwarp();
+      __syncthreads();
     }
     if (leader) {
       bulk_s2g(ring_c[st].d, ring + st * kCopyChunk, ring_c[st].bytes, dst_pol);
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(32) paged_copy_kernel(const CopyArgs a) {
     }
     if (k >= 1 && more) {
       // chunk k-1's store has read its stage: refill it with chunk k-1+kCopyStages
-      if (kScale) __syncwarp();
+      if (kScale) __syncthreads();
       if ((more = issue(issued))) ++issued;
     }
   }
@@ -288,7 +297,8 @@ int launch_copy(const CopyArgs& args, int ctas_per_sm, void* stream, const char*
   const uint64_t chunks = (args.nvec * 16 * static_cast<uint64_t>(args.n) + CHUNK - 1) / CHUNK;
   const int grid = static_cast<int>(
       std::min<uint64_t>(chunks, static_cast<uint64_t>(jenga_dev::num_sms()) * std::max(1, ctas_per_sm)));
-  jenga_dev::launch_maybe_pdl(kern, dim3(grid), dim3(32), smem, static_cast<cudaStream_t>(stream), args);
+  jenga_dev::launch_maybe_pdl(kern, dim3(grid), dim3(copy_threads<kScale>()), smem, static_cast<cudaStream_t>(stream),
+                              args);
   jenga_dev::note_launch(static_cast<cudaStream_t>(stream), jenga_dev::kLaunchArenaWriterPdl);
   return jenga_dev::check_launch(what);
 }
