@@ -246,7 +246,7 @@ class Workload:
             art = np.random.default_rng(1_000_003 * r + 17).integers(1, 1 << 40, self.article)
             qr = np.random.default_rng(7919 * r + 31 * q_round + 5)
             n = self.question + int(qr.integers(0, 17))
-            out.append([int(x) for x in art] + [int(x) for x in qr.integers(1, 1 << 40, n)])
+            out.append(np.concatenate([art, qr.integers(1, 1 << 40, n)]).astype(np.uint64))  # token ids as an array
         return out
 
     def prefix_setup(self, eng, ids, dev, chunk_requests=32):

@@ -186,11 +186,14 @@ std::vector<GroupLookupInput> PageLists::build_lookup_inputs(const Request& r) c
   for (size_t g = 0; g < kv_->num_groups(); ++g) {
     GroupLookupInput& in = inputs[g];
     const LayerGroupSpec& grp = kv_->group(g);
+    in.stored_positions.reserve(r.prompt_len);
     for (uint64_t pos = 1; pos <= r.prompt_len; ++pos)
       if (group_stores_position(g, r, pos)) in.stored_positions.push_back(pos);
     if (grp.kind == LayerKind::kVisionEmbedding) continue;  // never cached
     const uint64_t t = grp.kind == LayerKind::kMamba ? grp.checkpoint_interval_tokens : grp.tokens_per_page;
     const uint64_t full_blocks = in.stored_positions.size() / t;
+    in.blocks.reserve(full_blocks);
+    in.block_end_ordinal.reserve(full_blocks);
     uint64_t parent = block_chain_salt(grp.name);
     for (uint64_t b = 0; b < full_blocks; ++b) {
       BlockContent c;

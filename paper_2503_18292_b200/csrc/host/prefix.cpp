@@ -82,11 +82,18 @@ PrefixRangeSet possible_prefixes(const LayerGroupSpec& g, const std::vector<bool
       break;
     }
     case LayerKind::kSlidingWindow: {
-      uint64_t run = 0;
+      // maximal runs of valid p appended whole (same set as appending each p)
+      uint64_t run = 0, open = 0;
       for (uint64_t p = 1; p <= n; ++p) {
         run = is_hit[p - 1] ? run + 1 : 0;
-        if (run >= std::min(g.window_tokens, p)) out.append(p);
+        const bool ok = run >= std::min(g.window_tokens, p);
+        if (ok && open == 0) open = p;
+        if (!ok && open != 0) {
+          out.append_range(open, p - 1);
+          open = 0;
+        }
       }
+      if (open != 0) out.append_range(open, n);
       break;
     }
     case LayerKind::kMamba: {
@@ -110,11 +117,17 @@ PrefixRangeSet stored_to_global_prefixes(const PrefixRangeSet& valid, const std:
   if (sequence_length == 0) return out;
   const uint64_t m = stored.size();
   uint64_t prev_hi = 0;
+  // counts rise monotonically: walk valid's ranges alongside instead of a binary
+  // search per count
+  const auto& vr = valid.ranges();
+  size_t vi = 0;
   for (uint64_t count = 0; count <= m; ++count) {
     const uint64_t lo = count == 0 ? 1 : stored[count - 1];
     const uint64_t hi = count == m ? sequence_length : stored[count] - 1;
     if (lo > hi) continue;
-    if (count == 0 || valid.contains(count)) {
+    while (vi < vr.size() && vr[vi].second < count) ++vi;
+    const bool in_valid = vi < vr.size() && count >= vr[vi].first;
+    if (count == 0 || in_valid) {
       JENGA_CHECK(lo > prev_hi, "stored positions out of order");
       out.append_range(lo, hi);
       prev_hi = hi;
@@ -163,17 +176,33 @@ LookupResult KvAllocator::lookup_and_pin(const std::vector<GroupLookupInput>& in
     const uint64_t m = static_cast<uint64_t>(
         std::upper_bound(in.stored_positions.begin(), in.stored_positions.end(), p) - in.stored_positions.begin());
     if (m == 0) continue;
-    bool defined = true;
-    const std::vector<uint64_t> req = required_tokens(spec_.groups[g], m, &defined);
-    JENGA_CHECK(defined, "common prefix invalid for a group policy");
-    uint64_t last_block = UINT64_MAX;
-    for (uint64_t ord : req) {
-      const uint64_t b = static_cast<uint64_t>(
-          std::lower_bound(in.block_end_ordinal.begin(), in.block_end_ordinal.end(), ord) -
-          in.block_end_ordinal.begin());
-      if (b == last_block) continue;
-      last_block = b;
-      JENGA_CHECK(b < in.blocks.size(), "required ordinal beyond blocks");
+    // required_tokens(g, m) is one contiguous ordinal range per kind (empty for
+    // vision): pin every block that holds one of them, in block order -- the blocks
+    // the reference's per-ordinal walk pins, without materialising the ordinals
+    const LayerGroupSpec& gs = spec_.groups[g];
+    uint64_t ord_lo = 1, ord_hi = m;
+    switch (gs.kind) {
+      case LayerKind::kFullAttention:
+      case LayerKind::kCrossAttention:
+        break;
+      case LayerKind::kSlidingWindow:
+        ord_lo = m > gs.window_tokens ? m - gs.window_tokens + 1 : 1;
+        break;
+      case LayerKind::kMamba:
+        JENGA_CHECK(m % gs.checkpoint_interval_tokens == 0, "common prefix invalid for a group policy");
+        ord_lo = m;
+        break;
+      case LayerKind::kVisionEmbedding:
+        ord_lo = 1;
+        ord_hi = 0;  // nothing required
+        break;
+    }
+    if (ord_lo > ord_hi) continue;
+    const auto& be = in.block_end_ordinal;
+    const uint64_t b_lo = static_cast<uint64_t>(std::lower_bound(be.begin(), be.end(), ord_lo) - be.begin());
+    const uint64_t b_hi = static_cast<uint64_t>(std::lower_bound(be.begin(), be.end(), ord_hi) - be.begin());
+    JENGA_CHECK(b_hi < in.blocks.size(), "required ordinal beyond blocks");
+    for (uint64_t b = b_lo; b <= b_hi; ++b) {
       auto page = cache_.find(g, in.blocks[b]);
       JENGA_CHECK(page.has_value(), "hit block vanished before pinning");
       pin(g, *page, request);
