@@ -143,6 +143,85 @@ __global__ void __launch_bounds__(256, 1) softmax_rate(int iters, long long* out
   }
 }
 
+// NW softmax warps per TMEM lane quarter (4*NW warps), each owning 128/NW columns of
+// every 128-key tile, synchronised per tile by a named barrier among the quarter's warps
+// (the kernel's rescale vote); exp: 3 of 4 pairs on the MUFU, 1 on FFMA2.
+template <int NW>
+__global__ void __launch_bounds__(512, 1) softmax_split(int iters, long long* out, float* sink) {
+  constexpr int HC = 128 / NW;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, q = warp >> 2;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tm = slot + ((uint32_t)((warp & 3) * 32) << 16) + q * HC;
+  {
+    uint32_t z[32];
+    for (int i = 0; i < 32; ++i) z[i] = __float_as_uint(-0.01f * (i + (threadIdx.x & 7)));
+    for (int c = 0; c < HC; c += 32) st32(tm + c, z);
+    if (HC < 32) st32(tm, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  float m_used = 0.f, l = 0.f;
+  const float sc = 0.0883883f;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float s[HC];
+    for (int c = 0; c < HC; c += 32) ld32(tm + c, s + c);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    float m8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m8[i] = s[i];
+#pragma unroll
+    for (int i = 8; i < HC; i += 8)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], s[i + u]);
+    float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+    uint32_t grow;
+    asm volatile("{\n\t.reg .pred p, r;\n\tsetp.gt.f32 p, %1, %2;\n\tbar.red.or.pred r, %3, %4, p;\n\tselp.u32 %0, 1, 0, r;\n\t}\n"
+                 : "=r"(grow) : "f"(mt * sc), "f"(m_used + 1e9f), "r"(1 + (warp & 3)), "r"(NW * 32) : "memory");
+    m_used = fmaxf(m_used, mt * sc) + 1e-7f * it + grow;
+    const float neg = -m_used;
+    uint32_t pk[HC / 2];
+    float2 rs[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    const float2 sc2 = make_float2(sc, sc), ng2 = make_float2(neg, neg);
+#pragma unroll
+    for (int i = 0; i < HC; i += 2) {
+      const float2 x = ffma2(make_float2(s[i], s[i + 1]), sc2, ng2);
+      float2 e;
+      if ((i & 7) == 6) e = exp2_poly2(x);
+      else e = make_float2(ex2(x.x), ex2(x.y));
+      rs[(i >> 1) & 3] = fadd2(rs[(i >> 1) & 3], e);
+      pk[i / 2] = pack_bf16(e.x, e.y);
+    }
+    const float2 r = fadd2(fadd2(rs[0], rs[1]), fadd2(rs[2], rs[3]));
+    l += r.x + r.y;
+    if (HC / 2 >= 32) {
+      st32(tm + 256, pk);
+    } else {
+      uint32_t w[32];
+      for (int i = 0; i < 32; ++i) w[i] = pk[i % (HC / 2)];
+      st32(tm + 256, w);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  if (l == 12345.f) sink[threadIdx.x] = l;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(slot));
+  }
+}
+
 int main() {
   long long* d_out; float* sink; long long h[148];
   cudaMalloc(&d_out, 148 * sizeof(long long)); cudaMalloc(&sink, 4096 * sizeof(float));
@@ -161,5 +240,18 @@ int main() {
   run(softmax_rate<0>, 0);
   run(softmax_rate<1>, 1);
   run(softmax_rate<2>, 2);
+  auto runs = [&](auto kern, int nw) {
+    const int iters = 256;
+    kern<<<148, nw * 4 * 32>>>(iters, d_out, sink);
+    kern<<<148, nw * 4 * 32>>>(iters, d_out, sink);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("failed\n"); return; }
+    cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    double tot = 0; for (int i = 0; i < 148; ++i) tot += h[i]; tot /= 148;
+    printf("{\"split_warps_per_quarter\": %d, \"cyc_per_128key_tile\": %.0f, \"exp_per_clk_per_sm\": %.2f}\n", nw,
+           tot / iters, 128.0 * 128 * iters / tot);
+  };
+  runs(softmax_split<1>, 1);
+  runs(softmax_split<2>, 2);
+  runs(softmax_split<4>, 4);
   return 0;
 }
