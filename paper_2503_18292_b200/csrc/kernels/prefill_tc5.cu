@@ -78,12 +78,6 @@ __device__ __forceinline__ uint32_t idesc_f16(int m, int n, int b_mn) {
          (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
 
 // A operand from TMEM (K-major, two 16-bit elements per 32-bit column).
 __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -547,15 +541,12 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 // Remote arrive on the leader's barrier.  The default (.release.cta) form is a
-// bare SYNCS.ARRIVE; P / Q visibility to the MMA comes from tcgen05.wait::st +
+// bare SYNCS.ARRIVE; P visibility to the MMA comes from tcgen05.wait::st +
 // tcgen05.fence::before_thread_sync.  Only generic shared-memory writes the
 // leader's MMA must see (zeroed V rows) need the cluster-scope release, whose
 // MEMBAR.GPU + ERRBAR cost ~25% of the kernel when paid every tile.
 __device__ __forceinline__ void arrive_cta0(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
-}
-__device__ __forceinline__ void arrive_cta0_release(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
 }
 // Cluster-scope release arrive out of line: inlined under a branch, ptxas
 // predicates its MEMBAR.GPU / ERRBAR sequence, whose fixed stall cycles are paid
