@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--tpp", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-prefill", action="store_true",
+                   help="skip the chunked-prefill line added to the gemma2-9b result (after the timed decode)")
     p.add_argument("--e2e-timeline", action="store_true",
                    help="profiling only (with --no-graph): print when each input chunk lands vs when its first layer starts")
     p.add_argument("--e2e-chunks", default="geo", choices=["geo", "3"],
@@ -922,6 +924,35 @@ def run_reference(a):
                                         "d2h_bytes_per_step": 0}}
 
 
+def prefill_line(a):
+    """SURVEY §8(f) row 1 next to the decode result (outside its timed region): the
+    chunked-prefill attention of the same model's layers -- 4 requests x 2048-token
+    chunks at 8k context, Gemma-2-9B heads (Hq=16, Hkv=8, D=256), the model's logit
+    softcap and without it, full and SWA-4096 layers -- as TFLOP/s (4*D*Hq flop per
+    attended (query, key) pair; CUDA events, 10 launches after 2 warm-ups) against the
+    measured cuBLAS bf16 peak."""
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+    sys.path.insert(0, str(ROOT / "profiles"))
+    import bench_prefill
+    cap = a.softcap if a.softcap is not None else 50.0
+    plain = bench_prefill.run(4, 8192, 2048, quiet=True)
+    capped = bench_prefill.run(4, 8192, 2048, softcap=cap, quiet=True)
+    pk, src = peaks()
+    tf = plain["full"]["attn_TFLOPs"]
+    return {"metric": "chunked-prefill attention TFLOP/s (4*D*Hq flop per attended pair)",
+            "kernel": "paged_prefill_tc5_wide_kernel<bf16, D=256, G=2> (persistent tcgen05 CTA pairs)",
+            "config": "4 requests x 2048-token chunks at 8192 context, Gemma-2-9B heads, bf16",
+            "value": tf, "unit": "TFLOP/s", "peak": pk.get("bf16_tflops"), "peak_source": src,
+            "frac": round(tf / pk["bf16_tflops"], 4) if pk.get("bf16_tflops") else None,
+            "swa_4096": plain["swa"]["attn_TFLOPs"],
+            f"softcap_{cap:g}": {"full": capped["full"]["attn_TFLOPs"], "swa_4096": capped["swa"]["attn_TFLOPs"]},
+            "kv_write_GBps": plain["full"]["kv_write_GBps"]}
+
+
 def main():
     a = parse()
     if a.impl == "ours" and a.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -949,6 +980,11 @@ def main():
         else:
             dist.init_process_group(backend)
     res = run_ours(a, rank, world, local_rank)
+    if rank == 0 and world == 1 and not a.no_prefill and a.workload == "gemma2-9b":
+        try:
+            res["prefill"] = prefill_line(a)
+        except Exception as e:  # the extra line must not sink the decode result
+            res["prefill"] = {"value": None, "error": str(e)[:200]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline and a.workload in ("gemma2-9b", "prefix-mix"):
         from paper_2503_18292_b200.geometry import gemma2_9b as _g
         gemma2_9b = (lambda tpp: _g(tpp, softcap=a.softcap)) if a.softcap is not None else _g

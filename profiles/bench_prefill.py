@@ -20,7 +20,7 @@ from paper_2503_18292_b200.engine import DecodeEngine  # noqa: E402
 from paper_2503_18292_b200.geometry import gemma2_9b  # noqa: E402
 
 
-def run(B, ctx, chunk, iters=10, heads=(16, 8, 256), softcap=0.0):
+def run(B, ctx, chunk, iters=10, heads=(16, 8, 256), softcap=0.0, quiet=False):
     H, Hkv, D = heads
     geom = gemma2_9b(16)
     for g in geom.groups:
@@ -77,7 +77,9 @@ def run(B, ctx, chunk, iters=10, heads=(16, 8, 256), softcap=0.0):
         flops = 4 * D * H * pairs * B
         res[name] = {"attn_us": round(a_us, 1), "attn_TFLOPs": round(flops / a_us / 1e6, 1),
                      "kv_write_us": round(w_us, 1), "kv_write_GBps": round(2 * T * Hkv * D * 2 * 2 / w_us / 1e3, 1)}
-    print(json.dumps(res), flush=True)
+    if not quiet:
+        print(json.dumps(res), flush=True)
+    return res
 
 
 if __name__ == "__main__":
