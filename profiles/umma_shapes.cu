@@ -253,7 +253,11 @@ __global__ void exp_rate(int iters, long long* out, float* sink) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       float y;
-      if constexpr (POLY == 2) {  // two exponentials per MUFU instruction if bf16x2 is native
+      if constexpr (POLY == 4) {
+        asm volatile("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x[i]));
+      } else if constexpr (POLY == 5) {
+        asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[i] - 2.f));
+      } else if constexpr (POLY == 2) {  // two exponentials per MUFU instruction if bf16x2 is native
         uint32_t in = __float_as_uint(x[i]) & 0xffff0000u, o;
         in |= in >> 16;
         asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(o) : "r"(in));
@@ -382,5 +386,7 @@ int main() {
   ex(exp_rate<1>, "poly3");
   ex(exp_rate<2>, "mufu bf16x2 (per instruction; x2 exps)");
   ex(exp_rate<3>, "mufu bf16 scalar");
+  ex(exp_rate<4>, "mufu tanh.approx.f32");
+  ex(exp_rate<5>, "mufu rcp.approx.ftz.f32");
   return 0;
 }
