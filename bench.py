@@ -586,7 +586,8 @@ def run_ours(a, rank, world, local_rank):
             out_bounds = sorted({0, max(na - 3, 0), max(na - 1, 0), na})
         ev_in = [torch.cuda.Event(enable_timing=a.e2e_timeline) for _ in range(len(in_bounds) - 1)]
         tl = {"t0": torch.cuda.Event(enable_timing=True),
-              "layer": [torch.cuda.Event(enable_timing=True) for _ in range(na)]} if a.e2e_timeline else None
+              "layer": [torch.cuda.Event(enable_timing=True) for _ in range(na)]} \
+            if a.e2e_timeline and graph is None else None  # eager steps only
         ev_out = [torch.cuda.Event() for _ in range(len(out_bounds) - 1)]
         in_start = {in_bounds[c]: c for c in range(len(in_bounds) - 1)}
         out_end = {out_bounds[c + 1] - 1: c for c in range(len(out_bounds) - 1)}
