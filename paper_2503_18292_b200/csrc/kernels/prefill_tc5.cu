@@ -580,6 +580,9 @@ __device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* tmap, in
       : "memory");
 }
 
+#ifndef JENGA_PF_TRACE_Q
+#define JENGA_PF_TRACE_Q 0  // TMEM lane quarter (SM sub-partition) whose softmax warps are traced
+#endif
 #ifdef JENGA_PF_TRACE
 // Profiling-only (variant builds): clock64 stamps of the pipeline events of the
 // first CTA pair's leader, [event][tile] for tiles < 64.
@@ -1004,7 +1007,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       const uint32_t s_addr = tmem + lane_addr + S_COL0 + sb * KT;
       const int kc0 = (tile_lo + j) * KT + hf * HC;   // key of this warp's first column
       jenga_dev::mbar_wait(&s_full[sb], (gg / NSB) & 1);
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(4 + 6 * hf, gg);
+      if ((warp & 3) == JENGA_PF_TRACE_Q && lane == 0 && rank == 0) PF_TRACE(4 + 6 * hf, gg);
       tc_fence_after();
 #ifdef JENGA_PF_NOSOFTMAX
       if (true) {  // timing-only variant: hand the tile straight back to the MMA issuer
@@ -1016,7 +1019,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
 #endif
       float s[HC];
       tmem_ld64(s_addr + hf * HC, s);
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(5 + 6 * hf, gg);
+      if ((warp & 3) == JENGA_PF_TRACE_Q && lane == 0 && rank == 0) PF_TRACE(5 + 6 * hf, gg);
       if (softcap) {
 #pragma unroll
         for (int i = 0; i < HC; ++i) s[i] = p.cap_log2 * tanhf(s[i] * qi);
@@ -1114,7 +1117,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
         l += t.x + t.y;
       }
       tmem_st_wait();
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(6 + 6 * hf, gg);
+      if ((warp & 3) == JENGA_PF_TRACE_Q && lane == 0 && rank == 0) PF_TRACE(6 + 6 * hf, gg);
       // zero this CTA's V columns of keys outside the pair's range; the issuer waited
       // for this tile's V before S(j), so s_full(j) implies it has landed
       const int ktok0 = (tile_lo + j) * KT;
@@ -1137,7 +1140,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((2 * kSoftWarps + 2)
       }
       tc_fence_before();
       __syncwarp();
-      if ((warp & 3) == 0 && lane == 0 && rank == 0) PF_TRACE(7 + 6 * hf, gg);
+      if ((warp & 3) == JENGA_PF_TRACE_Q && lane == 0 && rank == 0) PF_TRACE(7 + 6 * hf, gg);
       if (lane == 0) {
         const uint32_t pf = p_full0 + 8u * (sb * NPH + (SPLITO ? hf : 0));
         if (boundary)
