@@ -92,9 +92,15 @@ __global__ void __launch_bounds__(256) reshape_and_cache_kernel(
 // kCopyStages-1 loads stay in flight; items with a negative index are skipped.
 // 16 KiB x 6 stages, 2 CTAs per SM (2 x 96 KiB rings per SM): the fastest of
 // the chunk / depth / occupancy sweep in profiles/r01_copy_sweep.jsonl.
+#ifndef JENGA_COPY_STAGES
+#define JENGA_COPY_STAGES 6
+#endif
+#ifndef JENGA_COPY_CTAS_PER_SM
+#define JENGA_COPY_CTAS_PER_SM 2
+#endif
 constexpr int kCopyChunkBytes = 16384;
-constexpr int kCopyStages = 6;
-constexpr int kCopyCtasPerSm = 2;
+constexpr int kCopyStages = JENGA_COPY_STAGES;
+constexpr int kCopyCtasPerSm = JENGA_COPY_CTAS_PER_SM;
 
 struct CopyArgs {
   const uint8_t* src_base;
