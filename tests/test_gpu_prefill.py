@@ -92,7 +92,7 @@ def test_prefill_cross_attention(orc):
 @pytest.mark.parametrize("case", range(16))
 def test_prefill_fuzz(orc, case):
     """Seeded random shapes through both prefill kernels: head_dim 64 / 128 / 256, GQA
-    group 1-8, tokens per page 16-128 (the TMA producer's page / offset split), full or
+    group 1-8, bf16 or fp16, tokens per page 16-128 (the TMA producer's page / offset split), full or
     sliding-window attention with a random window, optional soft-capping, ragged chunk
     lengths (chunks starting mid-page, single tokens, a chunk equal to the whole prompt).
     Every (token, head) row is checked (elementwise atol = tol * max|want|)."""
@@ -107,7 +107,8 @@ def test_prefill_fuzz(orc, case):
     nreq = int(rng.integers(2, 5))
     lens = [int(x) for x in rng.integers(1, 1400, nreq)]
     chunks = [int(min(n, rng.choice([n, rng.integers(1, n + 1), 1]))) for n in lens]
-    geom = ModelGeometry("fz", [GroupGeometry("g", kind, 1, hkv, hkv * G, hd, torch.bfloat16, tpp, window=window)],
+    dtype = torch.float16 if case % 5 == 2 else torch.bfloat16
+    geom = ModelGeometry("fz", [GroupGeometry("g", kind, 1, hkv, hkv * G, hd, dtype, tpp, window=window)],
                          softcap=softcap)
     eng, ids = make_engine(geom, lens, seed=case, defer_window=True)
     fill_group_kv(eng, 0, [0], seed=case + 7, all_live=True)
