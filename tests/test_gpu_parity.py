@@ -398,3 +398,52 @@ def test_mamba_state_update_in_place(orc, decay, l0, nl):
     np.testing.assert_array_equal(got, want)
     if decay != 1.0:
         assert not np.array_equal(got, before)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_decode_append_fuzz(orc, case):
+    """Seeded random shapes through the fused decode-append (the bench's kernel):
+    head_dim 64 / 128 / 256, GQA group 1-8, tokens per page 16-64, full or sliding
+    window (random width, including windows inside the newest tile), soft-capping,
+    bf16 / fp16, random context lengths.  Fused == unfused bit for bit (output and
+    arena bytes) and every (request, head) row vs the oracle (elementwise)."""
+    rng = np.random.default_rng(500 + case)
+    hd = [256, 128, 64][case % 3]
+    G = [2, 4, 1, 8][case % 4]
+    hkv = int(rng.choice([1, 2, 4, 8]))
+    tpp = int(rng.choice([16, 32, 48, 64]))
+    kind = LayerKind.kSlidingWindow if case % 2 else LayerKind.kFullAttention
+    window = int(rng.choice([7, 100, 1000])) if kind == LayerKind.kSlidingWindow else 0
+    softcap = 50.0 if case % 5 == 1 else 0.0
+    dtype = torch.float16 if case % 6 == 3 else torch.bfloat16
+    lens = [int(x) for x in rng.integers(1, 2500, int(rng.integers(2, 9)))]
+    hq = hkv * G
+    geom = ModelGeometry("fz", [GroupGeometry("g", kind, 2, hkv, hq, hd, dtype, tpp, window=window)], softcap=softcap)
+    eng, ids = make_engine(geom, lens, seed=case)
+    fill_group_kv(eng, 0, [1], seed=case + 1)
+    B = len(lens)
+    gen = torch.Generator(device=eng.device).manual_seed(100 + case)
+    q = torch.randn((B, hq, hd), generator=gen, device=eng.device).to(dtype)
+    k = torch.randn((B, hkv, hd), generator=gen, device=eng.device).to(dtype)
+    v = torch.randn((B, hkv, hd), generator=gen, device=eng.device).to(dtype)
+    at = eng.arena.tensor()
+    saved = at.clone()
+    out_a = torch.empty_like(q)
+    eng.write_kv(0, 1, k, v)
+    eng.decode(0, 1, q, out_a)
+    torch.cuda.synchronize()
+    arena_a = at.clone()
+    at.copy_(saved)
+    out_b = torch.empty_like(q)
+    eng.decode_append(0, 1, q, k, v, out_b)
+    torch.cuda.synchronize()
+    assert torch.equal(at, arena_a), "fused append wrote different arena bytes"
+    assert torch.equal(out_b, out_a), "fused append changed the attention output"
+    t = eng.tables[0]
+    want = orc.paged_decode(arena_host(eng), tuple(eng.view(0, 1)), int(kind), ORC_DTYPE[dtype], window,
+                            q.view(torch.int16).cpu().numpy(), t.block_table[:B].cpu().numpy(),
+                            t.seq_lens[:B].cpu().numpy(), hq, hkv, hd, tpp, hd ** -0.5, softcap, nthreads=8)
+    got = out_b.float().cpu().numpy()
+    tol = TOL[dtype]
+    assert rel_err(got, want) <= tol
+    np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
