@@ -79,18 +79,21 @@ __device__ __forceinline__ uint32_t idesc_f16(int m, int n, int b_mn) {
 }
 
 
-// A operand from TMEM (K-major, two 16-bit elements per 32-bit column).
-__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+
+
+// cta_group::1 whole-warp forms (the head_dim 64 kernel).
+__device__ __forceinline__ void umma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   jenga_dev::smem_u32(bar))
-               : "memory");
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          jenga_dev::smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
+    {  // the whole warp runs the loop; elect.sync issues (as in the 128-key kernel)
       const uint32_t id_s = idesc_f16<T>(kRows, KT, 0);
       const uint32_t id_o = idesc_f16<T>(kRows, D, 1);
       // O += P_jj V_jj: P (bf16/fp16, packed over S) from TMEM, V [KT][D] MN-major
@@ -344,10 +347,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         const uint32_t v_u = jenga_dev::smem_u32(ring + (jj % NS) * STAGE + KV_BYTES);
 #pragma unroll
         for (int k = 0; k < KT / 16; ++k)
-          umma_ts(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o,
+          umma_ts_w(tmem, tmem + S_COL + sb * KT + k * 8, umma_desc(v_u + k * V_PIECE, kTile * 128, 1024), id_o,
                   (jj > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&p_empty[sb]);          // O updated
-        umma_commit(&kv_empty[jj % NS]);    // K/V stage free
+        umma_commit_w(&p_empty[sb]);          // O updated
+        umma_commit_w(&kv_empty[jj % NS]);    // K/V stage free
       };
       jenga_dev::mbar_wait(q_full, 0);
       // In-order issue: S_{j} (into the buffer P_{j-2} occupied) follows PV_{j-2}.
@@ -358,9 +361,9 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         const uint32_t k_u = jenga_dev::smem_u32(ring + st * STAGE);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)   // S = Q K^T: Q from TMEM, K [KT][D] K-major
-          umma_ts(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
+          umma_ts_w(tmem + S_COL + sb * KT, tmem + Q_COL + k * 8,
                   umma_desc(k_u + (k >> 2) * 1024 + (k & 3) * 32, 16, K_GROUP), id_s, k > 0 ? 1u : 0u);
-        umma_commit(&s_full[sb]);
+        umma_commit_w(&s_full[sb]);
         if (j >= 1) issue_pv(j - 1);
       }
       if (ntiles > 0) issue_pv(ntiles - 1);
