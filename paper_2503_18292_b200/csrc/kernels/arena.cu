@@ -5,6 +5,8 @@
 // purely by the AddressMap arithmetic — no per-layer tensors.
 #include <map>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "common.cuh"
 
@@ -23,7 +25,14 @@ int set_error(int code, const std::string& msg) { return jenga_host_err::set(cod
 
 namespace {
 std::mutex g_stream_mu;
-std::map<std::pair<int, uintptr_t>, bool> g_pdl_writer_pending;  // (device, stream) -> early-trigger writer in chain
+// (device, stream) -> the early-triggering arena writers still possibly in the
+// PDL chain: `unknown` for any writer without a footprint, else the column
+// footprints [start, start + len) of every page of stride `stride`.
+struct PendingWriters {
+  bool unknown = false;
+  std::vector<std::tuple<uint64_t, uint64_t, uint64_t>> cols;  // (stride, start, len)
+};
+std::map<std::pair<int, uintptr_t>, PendingWriters> g_pending;
 
 std::pair<int, uintptr_t> stream_key(cudaStream_t s) {
   int dev = 0;
@@ -35,14 +44,31 @@ std::pair<int, uintptr_t> stream_key(cudaStream_t s) {
 void note_launch(cudaStream_t stream, LaunchClass c) {
   std::lock_guard<std::mutex> lock(g_stream_mu);
   if (c == kLaunchArenaWriterPdl)
-    g_pdl_writer_pending[stream_key(stream)] = true;
+    g_pending[stream_key(stream)].unknown = true;
   else
-    g_pdl_writer_pending.erase(stream_key(stream));
+    g_pending.erase(stream_key(stream));
+}
+
+void note_column_writer(cudaStream_t stream, uint64_t stride, uint64_t start, uint64_t len) {
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  auto& w = g_pending[stream_key(stream)];
+  if (w.cols.size() >= 64) w.unknown = true;  // bounded bookkeeping: degrade to "unknown"
+  else w.cols.emplace_back(stride, start, len);
 }
 
 bool early_kv_ok(cudaStream_t stream) {
   std::lock_guard<std::mutex> lock(g_stream_mu);
-  return g_pdl_writer_pending.count(stream_key(stream)) == 0;
+  return g_pending.count(stream_key(stream)) == 0;
+}
+
+bool early_columns_ok(cudaStream_t stream, uint64_t stride, uint64_t start, uint64_t len) {
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  auto it = g_pending.find(stream_key(stream));
+  if (it == g_pending.end()) return true;
+  if (it->second.unknown) return false;
+  for (const auto& [s, b, l] : it->second.cols)  // same page grid, disjoint columns
+    if (s != stride || (start < b + l && b < start + len)) return false;
+  return true;
 }
 
 int num_sms() {

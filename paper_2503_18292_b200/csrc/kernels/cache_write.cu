@@ -113,6 +113,7 @@ struct CopyArgs {
   int n;
   int src_keep, dst_keep;  // 1: L2 evict_last (a dense staging buffer reused next kernel), 0: evict_first
   float scale;     // kScale kernels: every fp32 element is multiplied by it on the way through
+  int early;       // 1: the first kCopyStages loads may precede griddepcontrol.wait (common.cuh, column writers)
 };
 
 struct CopyChunk {
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(copy_threads<kScale>()) paged_copy_kernel(cons
     jenga_dev::fence_mbar_init();
   }
   if (kScale) __syncthreads();
-  jenga_dev::pdl_wait();
+  if (!a.early) jenga_dev::pdl_wait();
   // arena pages stream through L2 once; a dense staging buffer (Mamba state
   // between gather, the SSM update and scatter) is kept resident
   const uint64_t src_pol = a.src_keep ? jenga_dev::l2_policy_evict_last() : jenga_dev::l2_policy_evict_first();
@@ -199,6 +200,9 @@ __global__ void __launch_bounds__(copy_threads<kScale>()) paged_copy_kernel(cons
   };
   for (; issued < kCopyStages && (more = issue(issued)); ++issued) {
   }
+  // early: the ring filled while the previous grid drained; every store and
+  // later load follows its completion
+  if (a.early) jenga_dev::pdl_wait();
   for (int k = 0; k < issued; ++k) {
     const int st = k % kCopyStages;
     jenga_dev::mbar_wait(&full[st], (k / kCopyStages) & 1);
@@ -305,25 +309,36 @@ int launch_copy(const CopyArgs& args, int ctas_per_sm, void* stream, const char*
       std::min<uint64_t>(chunks, static_cast<uint64_t>(jenga_dev::num_sms()) * std::max(1, ctas_per_sm)));
   jenga_dev::launch_maybe_pdl(kern, dim3(grid), dim3(copy_threads<kScale>()), smem, static_cast<cudaStream_t>(stream),
                               args);
-  jenga_dev::note_launch(static_cast<cudaStream_t>(stream), jenga_dev::kLaunchArenaWriterPdl);
   return jenga_dev::check_launch(what);
 }
 
 int launch_paged_copy(const void* src_base, uint64_t src_off, uint64_t src_stride, const int64_t* src_idx,
                       void* dst_base, uint64_t dst_off, uint64_t dst_stride, const int64_t* dst_idx,
                       uint64_t bytes, int n, void* stream, const char* what, int src_keep, int dst_keep,
-                      const float* scale = nullptr) {
+                      const float* scale = nullptr, bool column_writer = false) {
   using namespace jenga_dev;
   if (n <= 0 || bytes == 0) return JENGA_OK;
   if (bytes % 16 != 0 || src_off % 16 != 0 || dst_off % 16 != 0 || src_stride % 16 != 0 ||
       dst_stride % 16 != 0 || reinterpret_cast<uintptr_t>(src_base) % 16 || reinterpret_cast<uintptr_t>(dst_base) % 16)
     return set_error(JENGA_ERR_UNSUPPORTED, std::string(what) + ": sizes/offsets must be 16-byte multiples");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // an in-place column writer (src == dst run on one page grid) may load
+  // early behind other column writers with disjoint columns
+#ifndef JENGA_COPY_EARLY
+#define JENGA_COPY_EARLY 1  // 0: profiling variant without the early state loads
+#endif
+  const bool early = JENGA_COPY_EARLY && column_writer && early_columns_ok(s, dst_stride, dst_off, bytes);
   const CopyArgs args{static_cast<const uint8_t*>(src_base), src_off, src_stride, src_idx,
                       static_cast<uint8_t*>(dst_base), dst_off, dst_stride, dst_idx, bytes / 16, n,
-                      src_keep, dst_keep, scale ? *scale : 1.f};
-  if (scale != nullptr && *scale != 1.f)
-    return launch_copy<kCopyChunkBytes, kCopyStages, true>(args, kCopyCtasPerSm, stream, what);
-  return launch_copy<kCopyChunkBytes, kCopyStages>(args, kCopyCtasPerSm, stream, what);
+                      src_keep, dst_keep, scale ? *scale : 1.f, early ? 1 : 0};
+  const int rc = scale != nullptr && *scale != 1.f
+                     ? launch_copy<kCopyChunkBytes, kCopyStages, true>(args, kCopyCtasPerSm, stream, what)
+                     : launch_copy<kCopyChunkBytes, kCopyStages>(args, kCopyCtasPerSm, stream, what);
+  if (column_writer)
+    note_column_writer(s, dst_stride, dst_off, bytes);
+  else
+    note_launch(s, kLaunchArenaWriterPdl);
+  return rc;
 }
 
 }  // namespace
@@ -389,7 +404,7 @@ JENGA_EXPORT int jenga_mamba_state_update(void* arena_base, jenga_layer_view vie
   const uint64_t run = static_cast<uint64_t>(num_layers) * view.exec_page_size;
   return launch_paged_copy(arena_base, view.start_offset, view.page_stride, page_globals, arena_base,
                            view.start_offset, view.page_stride, page_globals, run, batch, stream,
-                           "mamba_state_update", 0, 0, &decay);
+                           "mamba_state_update", 0, 0, &decay, /*column_writer=*/true);
 }
 
 JENGA_EXPORT int jenga_page_copy(void* arena_base, uint64_t small_page_bytes, const int64_t* src_globals,

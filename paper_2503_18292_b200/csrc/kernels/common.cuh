@@ -220,9 +220,20 @@ int num_sms();  // SMs of the current device (cached per device)
 // mark; decode launches leave it as it is (their only arena write is the
 // newest token's row, which the consumer itself patches or waits for).  The
 // decode launcher asks early_kv_ok(): false -> its producer waits first.
+//
+// Column writers: the in-place Mamba state update writes only bytes
+// [start, start + len) of every page of stride `stride` (one run of layer
+// slices per page).  It records that footprint instead of the blanket mark, and
+// it may itself load its state before griddepcontrol.wait when every pending
+// writer is such a column writer on the same page grid with disjoint columns
+// (early_columns_ok) — consecutive Mamba layers then stream their states while
+// the previous layer drains.  The page-index arrays they read early come, like
+// block tables, from launches without the attribute.
 enum LaunchClass { kLaunchArenaWriterPdl = 0, kLaunchSerializing = 1 };
 void note_launch(cudaStream_t stream, LaunchClass c);
+void note_column_writer(cudaStream_t stream, uint64_t stride, uint64_t start, uint64_t len);
 bool early_kv_ok(cudaStream_t stream);
+bool early_columns_ok(cudaStream_t stream, uint64_t stride, uint64_t start, uint64_t len);
 
 // Launch with the programmatic-stream-serialization attribute.
 template <typename... KArgs, typename... Args>

@@ -35,6 +35,11 @@ __host__ __device__ constexpr int decode_ctas_per_sm(int head_dim) {
 __host__ __device__ constexpr int decode_ring_bytes(int head_dim) {
   return head_dim >= 256 ? JENGA_DECODE_RING_BYTES_D256 : JENGA_DECODE_RING_BYTES_D128;
 }
+// KV heads per thread-block cluster for launches of at most two waves
+// (decode_tc.cu launch_tc); 1 disables clusters (profiling variant).
+#ifndef JENGA_DECODE_CLUSTER
+#define JENGA_DECODE_CLUSTER 4
+#endif
 // Consumer warps per CTA (each owns the stages s with s % CW == its index).
 #ifndef JENGA_DECODE_CONSUMERS_D256
 #define JENGA_DECODE_CONSUMERS_D256 4

@@ -460,7 +460,35 @@ int launch_tc(const DecodeParams& prm, const CUtensorMap& tmap, int batch, cudaS
   auto kern = paged_decode_tc_kernel<T, D, G, NS>;
   static std::atomic<uint64_t> configured{0};
   if (int rc = configure_smem(kern, smem, configured)) return rc;
-  jenga_dev::launch_maybe_pdl(kern, decode_grid(prm, batch), dim3((CW + 1) * 32), smem, stream, prm, tmap);
+  // Launches of at most two waves go out as clusters of 4 KV heads of one
+  // request (co-scheduled on one GPC): +1.3% on the Gemma G=8 shard (one
+  // partial wave), +0.8% on Llama-vision (1.7 waves), neutral at G=4 / Jamba,
+  // -2.4% on the prefix mix (7 waves: cluster-granular refills fragment the
+  // SMs), hence the wave bound (profiles/r02_decode_experiments.md).
+  const dim3 grid = decode_grid(prm, batch);
+  const int64_t ctas = static_cast<int64_t>(grid.x) * grid.y * grid.z;
+  const int64_t slots = static_cast<int64_t>(jenga_dev::num_sms()) * decode_ctas_per_sm(D);
+  if (JENGA_DECODE_CLUSTER > 1 && prm.hkv % JENGA_DECODE_CLUSTER == 0 && ctas <= 2 * slots) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3((CW + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = JENGA_DECODE_CLUSTER;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, kern, prm, tmap) == cudaSuccess) return jenga_dev::check_launch("paged_decode_tc_kernel");
+    (void)cudaGetLastError();  // cluster shape not schedulable here: plain launch below
+  }
+  {
+    jenga_dev::launch_maybe_pdl(kern, grid, dim3((CW + 1) * 32), smem, stream, prm, tmap);
+  }
   return jenga_dev::check_launch("paged_decode_tc_kernel");
 }
 

@@ -447,3 +447,42 @@ def test_decode_append_fuzz(orc, case):
     tol = TOL[dtype]
     assert rel_err(got, want) <= tol
     np.testing.assert_allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
+
+
+def test_mamba_per_layer_updates_early_loads(orc):
+    """Per-layer in-place updates in model order (the Jamba bench's per-layer
+    step): each launch after the first loads its states before
+    griddepcontrol.wait because the pending writers are column writers with
+    disjoint layer columns (common.cuh).  A repeated layer, an overlapping
+    two-layer run and an attention KV write (blanket PDL writer) in the
+    sequence must fall back to waiting.  The arena must equal the oracle's
+    sequential application, byte for byte, at the bench's batch (64 requests,
+    ~40 MB per launch, so launches overlap)."""
+    geom = ModelGeometry("hyb", [
+        GroupGeometry("attn", LayerKind.kFullAttention, 1, 8, 32, 128, torch.bfloat16, 16),
+        GroupGeometry("ssm", LayerKind.kMamba, 28, state_bytes=(8192 * 3 + 8192 * 16) * 4)])
+    lens = [1 + (i % 5) for i in range(64)]
+    eng, ids = make_engine(geom, lens, poison=False)
+    g = 1
+    pg = eng.mamba_page_globals(g).clone()
+    pg[7] = -1
+    at = eng.arena.tensor()
+    at.view(torch.float32).normal_(generator=torch.Generator(device=eng.device).manual_seed(9))
+    want = arena_host(eng).copy()
+    seq = [(l, 1, 0.999) for l in range(28)]
+    seq[6:6] = [(5, 1, 0.5)]          # layer 5 again right after itself
+    seq[12:12] = [(10, 2, 0.75)]      # a run overlapping the last two layers
+    seq[20:20] = [("kv", 0, 0)]       # attention KV write: unknown footprint
+    for l, nl, decay in seq:
+        if l == "kv":
+            req, ords, kvs, slots = fill_group_kv(eng, 0, [0], seed=4)
+            K, V = kvs[0]
+            orc.reshape_and_cache(want, tuple(eng.view(0, 0)), ORC_DTYPE[torch.bfloat16], 8, 128, 16,
+                                  K.view(torch.int16).cpu().numpy(), V.view(torch.int16).cpu().numpy(),
+                                  slots.cpu().numpy())
+            continue
+        view = eng.view(g, l)
+        ops.mamba_state_update(eng.arena, view, nl, pg, decay)
+        orc.mamba_update(want, tuple(view), nl, pg.cpu().numpy(), decay)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(arena_host(eng), want)
