@@ -399,6 +399,13 @@ int jenga_reshape_and_cache(void* arena_base, jenga_layer_view view, int dtype,
  * wait before its first load; every library launch on one stream is therefore
  * ordered as issued.  Kernels of your own that write the arena between library
  * launches must not use the programmatic-serialization attribute.
+ * jenga_mamba_state_update records a column footprint instead (bytes
+ * [start_offset, start_offset + num_layers * exec_page_size) of every page of
+ * stride page_stride) and loads its own states early when every pending writer
+ * is such a footprint on the same page grid with disjoint columns — per-layer
+ * updates in model order overlap one layer's drain with the next one's loads.
+ * Like block tables and seq_lens, the page_globals it reads early must come
+ * from a launch without the attribute (any torch / plain CUDA launch). 
  *
  * Paged decode attention through the two-level table.
  *   kind: JENGA_KIND_FULL / SLIDING_WINDOW / CROSS_ATTENTION
