@@ -3,6 +3,7 @@
 // identical operation sequences; the data structures are our own (bitmap
 // first-fit instead of ordered sets, flat unit tables instead of maps).
 #include <algorithm>
+#include <functional>
 
 #include "jenga_host.hpp"
 
@@ -120,7 +121,6 @@ TypeAllocator::TypeAllocator(GroupGeometry geo, int owner_id, LargePagePool* poo
   JENGA_CHECK(geo_.slots_per_large >= 1, "slots_per_large must be >= 1");
   units_.resize(pool_->num_pages());
   empty_.resize(uint64_t{pool_->num_pages()} * geo_.slots_per_large);
-  lru_it_.resize(uint64_t{pool_->num_pages()} * geo_.slots_per_large);
   fe_it_.resize(pool_->num_pages());
 }
 
@@ -220,9 +220,47 @@ std::optional<SmallPageId> TypeAllocator::try_allocate_any(uint64_t request) {
 }
 
 // Step 5 candidate — reference type_allocator.cpp:117-120
+bool TypeAllocator::lru_entry_live(const LruKey& k) const {
+  const uint64_t g = std::get<2>(k);
+  const SmallPageId id = from_global(g);
+  const Unit& u = units_[id.large.index];
+  if (!u.owned || id.slot >= u.slots.size()) return false;
+  const SmallPageRecord& r = u.slots[id.slot];
+  return r.state == SmallPageState::kEvictable && lru_key(r, g) == k;
+}
+
+void TypeAllocator::lru_rebuild() const {
+  lru_heap_.clear();
+  for (uint32_t first = 0; first < units_.size(); ++first) {
+    const Unit& u = units_[first];
+    if (!u.owned || u.evictable_count == 0) continue;
+    for (uint32_t s = 0; s < u.slots.size(); ++s)
+      if (u.slots[s].state == SmallPageState::kEvictable) lru_heap_.push_back(lru_key(u.slots[s], global_index(first, s)));
+  }
+  std::make_heap(lru_heap_.begin(), lru_heap_.end(), std::greater<LruKey>());
+}
+
+void TypeAllocator::lru_push(const LruKey& k) {
+  if (lru_heap_.size() >= 2 * lru_live_ + 4096) {
+    lru_rebuild();  // already holds k when the page is evictable with it
+    return;
+  }
+  lru_heap_.push_back(k);
+  std::push_heap(lru_heap_.begin(), lru_heap_.end(), std::greater<LruKey>());
+}
+
+void TypeAllocator::lru_drop_stale_top() const {
+  while (!lru_heap_.empty() && !lru_entry_live(lru_heap_.front())) {
+    std::pop_heap(lru_heap_.begin(), lru_heap_.end(), std::greater<LruKey>());
+    lru_heap_.pop_back();
+  }
+}
+
 std::optional<SmallPageId> TypeAllocator::lru_evictable_small() const {
-  if (lru_.empty()) return std::nullopt;
-  return from_global(std::get<2>(*lru_.begin()));
+  if (lru_live_ == 0) return std::nullopt;
+  lru_drop_stale_top();
+  JENGA_CHECK(!lru_heap_.empty(), "LRU heap lost an evictable page");
+  return from_global(std::get<2>(lru_heap_.front()));
 }
 
 // reference type_allocator.cpp:122-138
@@ -233,7 +271,7 @@ uint64_t TypeAllocator::evict_small(SmallPageId id) {
   JENGA_CHECK(r.has_cache_key, "evictable page lost its cache key");
   const uint64_t key = r.cache_key;
   const uint64_t g = global_index(id.large.index, id.slot);
-  lru_.erase(lru_it_[g]);
+  lru_live_--;  // its heap entry goes stale with the state change
   if (u.evictable_count == u.slots.size()) fully_evictable_.erase(fe_it_[id.large.index]);
   u.evictable_count--;
   r.state = SmallPageState::kEmpty;
@@ -271,7 +309,8 @@ void TypeAllocator::free(SmallPageId id, std::optional<uint64_t> cache_key) {
     r.has_cache_key = true;
     u.evictable_count++;
     if (u.evictable_count == u.slots.size()) fe_it_[id.large.index] = fully_evictable_.insert(id.large.index).first;
-    lru_it_[g] = lru_.insert(lru_key(r, g)).first;
+    lru_live_++;
+    lru_push(lru_key(r, g));
     return;
   }
   r.state = SmallPageState::kEmpty;
@@ -286,7 +325,7 @@ void TypeAllocator::pin(SmallPageId id, uint64_t request) {
   Unit& u = unit_of(id);
   SmallPageRecord& r = u.slots[id.slot];
   JENGA_CHECK(r.state == SmallPageState::kEvictable, "pin on a non-evictable page");
-  lru_.erase(lru_it_[global_index(id.large.index, id.slot)]);
+  lru_live_--;  // its heap entry goes stale with the state change
   if (u.evictable_count == u.slots.size()) fully_evictable_.erase(fe_it_[id.large.index]);
   u.evictable_count--;
   r.state = SmallPageState::kUsed;
@@ -299,11 +338,9 @@ void TypeAllocator::pin(SmallPageId id, uint64_t request) {
 // reference type_allocator.cpp:192-203
 void TypeAllocator::touch(SmallPageId id, uint64_t step) {
   SmallPageRecord& r = rec(id);
-  if (r.state == SmallPageState::kEvictable) {
-    const uint64_t g = global_index(id.large.index, id.slot);
-    lru_.erase(lru_it_[g]);
-    r.last_access = step;
-    lru_it_[g] = lru_.insert(lru_key(r, g)).first;
+  if (r.state == SmallPageState::kEvictable && r.last_access != step) {
+    r.last_access = step;  // the old entry goes stale
+    lru_push(lru_key(r, global_index(id.large.index, id.slot)));
   } else {
     r.last_access = step;
   }
@@ -312,11 +349,9 @@ void TypeAllocator::touch(SmallPageId id, uint64_t step) {
 // reference type_allocator.cpp:205-216
 void TypeAllocator::set_prefix_length(SmallPageId id, uint64_t len) {
   SmallPageRecord& r = rec(id);
-  if (r.state == SmallPageState::kEvictable) {
-    const uint64_t g = global_index(id.large.index, id.slot);
-    lru_.erase(lru_it_[g]);
-    r.prefix_length = len;
-    lru_it_[g] = lru_.insert(lru_key(r, g)).first;
+  if (r.state == SmallPageState::kEvictable && r.prefix_length != len) {
+    r.prefix_length = len;  // the old entry goes stale
+    lru_push(lru_key(r, global_index(id.large.index, id.slot)));
   } else {
     r.prefix_length = len;
   }
@@ -387,6 +422,10 @@ FragmentationReport TypeAllocator::fragmentation_report() const {
 // reference type_allocator.cpp:293-337
 void TypeAllocator::check_invariants() const {
   uint64_t used = 0, evictable = 0, empty = 0, owned = 0, fully = 0;
+  JENGA_CHECK(std::is_heap(lru_heap_.begin(), lru_heap_.end(), std::greater<LruKey>()), "LRU heap order broken");
+  std::set<LruKey> heap_live;
+  for (const LruKey& k : lru_heap_)
+    if (lru_entry_live(k)) heap_live.insert(k);
   for (uint32_t first = 0; first < units_.size(); ++first) {
     const Unit& u = units_[first];
     if (!u.owned) continue;
@@ -407,7 +446,7 @@ void TypeAllocator::check_invariants() const {
           ++evictable;
           ++uv;
           JENGA_CHECK(r.has_cache_key, "evictable page without cache key");
-          JENGA_CHECK(lru_.count(lru_key(r, g)) == 1, "evictable page missing from LRU index");
+          JENGA_CHECK(heap_live.count(lru_key(r, g)) == 1, "evictable page missing from LRU index");
           break;
         case SmallPageState::kEmpty:
           ++empty;
@@ -426,7 +465,7 @@ void TypeAllocator::check_invariants() const {
   }
   JENGA_CHECK(owned == owned_units_, "owned unit count drifted");
   JENGA_CHECK(used == used_, "used count drifted");
-  JENGA_CHECK(evictable == lru_.size(), "LRU index size drifted");
+  JENGA_CHECK(evictable == lru_live_ && evictable == heap_live.size(), "LRU index size drifted");
   JENGA_CHECK(empty == empty_.count(), "empty index size drifted");
   JENGA_CHECK(fully == fully_evictable_.size(), "fully-evictable set size drifted");
 }

@@ -201,7 +201,7 @@ class TypeAllocator {
   FragmentationReport fragmentation_report() const;
 
   uint64_t used_pages() const { return used_; }
-  uint64_t evictable_pages() const { return lru_.size(); }
+  uint64_t evictable_pages() const { return lru_live_; }
   uint64_t empty_pages() const { return empty_.count(); }
   uint64_t owned_units() const { return owned_units_; }
   bool has_associated_empty(uint64_t request) const;
@@ -232,17 +232,26 @@ class TypeAllocator {
   static LruKey lru_key(const SmallPageRecord& r, uint64_t g) {
     return LruKey{r.last_access, UINT64_MAX - r.prefix_length, g};
   }
+  bool lru_entry_live(const LruKey& k) const;
+  void lru_push(const LruKey& k);
+  void lru_drop_stale_top() const;
+  void lru_rebuild() const;
 
   GroupGeometry geo_;
   int owner_id_;
   LargePagePool* pool_;
   std::vector<Unit> units_;               // indexed by large page index
   uint64_t owned_units_ = 0;
-  std::set<LruKey> lru_;                  // begin() = eviction front
-  // node of each evictable page in lru_ / unit in fully_evictable_ (by global
-  // / unit index): a pin or touch erases by iterator instead of searching the
-  // (tens of thousands of entries under prefix caching) ordered set
-  std::vector<std::set<LruKey>::iterator> lru_it_;
+  // Eviction order: a lazy-deletion min-heap of LruKey (front = the reference's
+  // LRU victim).  A pin or eviction only changes the page's state and a touch
+  // pushes the page's new key, so the entries they leave behind are stale:
+  // an entry is live while its page is evictable with exactly that key.  Stale
+  // entries are dropped when they surface at the front and by a rebuild once
+  // they outnumber the live ones (pins of tens of thousands of cached pages
+  // per admission wave no longer rebalance an ordered set).
+  mutable std::vector<LruKey> lru_heap_;
+  uint64_t lru_live_ = 0;                 // evictable pages
+  // unit in fully_evictable_ by unit index (erase by iterator)
   FirstFitBitmap empty_;                  // global indices of empty owned slots
   // request -> its associated empty slots (global indices, kept sorted)
   std::unordered_map<uint64_t, std::vector<uint64_t>> empty_by_request_;
