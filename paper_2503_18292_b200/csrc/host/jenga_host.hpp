@@ -548,6 +548,7 @@ class PageLists {
 
  private:
   Request& req(uint64_t id);
+  bool store_position(Request& r, size_t g, uint64_t pos, uint64_t now);
   std::vector<GroupLookupInput> build_lookup_inputs(const Request& r) const;
   void append_chain(Request& r, size_t g);
   void free_block(Request& r, size_t g, uint64_t b, bool allow_cache, uint64_t now);

@@ -69,7 +69,12 @@ void PageLists::append_chain(Request& r, size_t g) {
 
 // reference simulator.cpp:217-282
 bool PageLists::store_position(uint64_t id, size_t g, uint64_t pos, uint64_t now) {
-  Request& r = req(id);
+  return store_position(req(id), g, pos, now);
+}
+
+// the request already resolved (the per-position loops of append / prefill)
+bool PageLists::store_position(Request& r, size_t g, uint64_t pos, uint64_t now) {
+  const uint64_t id = r.id;
   JENGA_CHECK(g < r.groups.size(), "group index out of range");
   const LayerGroupSpec& grp = kv_->group(g);
   // draft groups record draft-sequence ordinals (simulator.cpp:603-607)
@@ -167,7 +172,7 @@ bool PageLists::append(uint64_t id, uint64_t token, bool is_image, uint64_t imag
   for (size_t g = 0; g < kv_->num_groups(); ++g) {
     if (kv_->group(g).kind == LayerKind::kVisionEmbedding) continue;
     if (!group_stores_position(g, r, pos)) continue;
-    if (!store_position(id, g, pos, now)) {
+    if (!store_position(r, g, pos, now)) {
       // The reference pops the token on a failed decode (simulator.cpp:557-561).
       Request& rr = req(id);
       rr.tokens.pop_back();
@@ -328,7 +333,7 @@ uint64_t PageLists::prefill(uint64_t id, uint64_t budget, uint64_t now, bool* oo
       if (!group_stores_position(g, r, pos)) continue;
       const GroupRuntime& rt = r.groups[g];
       if (!rt.stored_positions.empty() && pos <= rt.stored_positions.back()) continue;  // pinned block
-      if (!store_position(id, g, pos, now)) {
+      if (!store_position(r, g, pos, now)) {
         r.needs_release = true;
         if (oom) *oom = true;
         return done;
