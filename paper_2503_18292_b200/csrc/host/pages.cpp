@@ -199,16 +199,50 @@ std::vector<GroupLookupInput> PageLists::build_lookup_inputs(const Request& r) c
     const uint64_t full_blocks = in.stored_positions.size() / t;
     in.blocks.reserve(full_blocks);
     in.block_end_ordinal.reserve(full_blocks);
-    uint64_t parent = block_chain_salt(grp.name);
     for (uint64_t b = 0; b < full_blocks; ++b) {
       BlockContent c;
-      c.parent_key = parent;
       c.tokens.reserve(t);
       for (uint64_t i = 0; i < t; ++i) c.tokens.push_back(r.tokens[in.stored_positions[b * t + i] - 1]);
-      c.key = chain_block_key(c.parent_key, c.tokens);
-      parent = c.key;
       in.blocks.push_back(std::move(c));
       in.block_end_ordinal.push_back((b + 1) * t);
+    }
+  }
+  // Block-chain keys (chain_block_key: one serially dependent mix per token).
+  // Groups holding the same tokens block for block (same block size, same
+  // stored positions; e.g. a full and a sliding-window group over a text
+  // prompt) differ only in their salt: their chains run interleaved, two
+  // independent dependency chains per loop, with each token's mix shared.
+  std::vector<bool> done(kv_->num_groups(), false);
+  for (size_t g = 0; g < kv_->num_groups(); ++g) {
+    if (done[g] || inputs[g].blocks.empty()) continue;
+    done[g] = true;
+    size_t h = g + 1;
+    for (; h < kv_->num_groups(); ++h)
+      if (!done[h] && inputs[h].block_end_ordinal == inputs[g].block_end_ordinal &&
+          inputs[h].stored_positions == inputs[g].stored_positions)
+        break;
+    auto& a = inputs[g].blocks;
+    uint64_t ka = block_chain_salt(kv_->group(g).name);
+    if (h == kv_->num_groups()) {
+      for (BlockContent& c : a) {
+        c.parent_key = ka;
+        c.key = ka = chain_block_key(ka, c.tokens);
+      }
+      continue;
+    }
+    done[h] = true;
+    auto& b = inputs[h].blocks;
+    uint64_t kb = block_chain_salt(kv_->group(h).name);
+    for (size_t i = 0; i < a.size(); ++i) {
+      a[i].parent_key = ka;
+      b[i].parent_key = kb;
+      for (const uint64_t tok : a[i].tokens) {
+        const uint64_t m = mix64(tok);  // chain_block_key's per-token step: mix64(k ^ mix64(tok))
+        ka = mix64(ka ^ m);
+        kb = mix64(kb ^ m);
+      }
+      a[i].key = ka;
+      b[i].key = kb;
     }
   }
   return inputs;
